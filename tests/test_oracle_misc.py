@@ -1,0 +1,125 @@
+"""Pins for O4 (barrier protocol model), O5 (partition simulator), the
+preemption closed form and the input generators."""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import graphgen as gg
+from conftest import golden
+from oracle import barrier_model as bm
+from oracle import partition_sim as ps
+from oracle import preemption as pre
+from oracle import textbook as tb
+
+
+# ---------------- O4 ----------------
+def test_barrier_protocol_exhaustive_n3():
+    total = 0
+    for M0 in (1, 2, 3):
+        for seq in itertools.product([1, 2, 3], repeat=3):
+            n, term = bm.explore(3, M0, list(seq), 3)
+            assert term >= 1
+            total += n
+    assert total > 10_000
+
+
+def test_barrier_protocol_n2_four_episodes():
+    for seq in itertools.product([1, 2], repeat=4):
+        bm.explore(2, 2, list(seq), 4)
+
+
+@pytest.mark.parametrize("bug,msg", [("kill_by_M_only", "P2"), ("no_wait_gen", "P1")])
+def test_barrier_model_catches_known_protocol_bugs(bug, msg):
+    found = None
+    for M0 in (1, 2, 3):
+        for seq in itertools.product([1, 2, 3], repeat=3):
+            try:
+                bm.explore(3, M0, list(seq), 3, bugs={bug})
+            except bm.ProtocolViolation as e:
+                found = str(e)
+                break
+        if found:
+            break
+    assert found is not None and found.startswith(msg)
+
+
+# ---------------- O5 ----------------
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
+def test_partition_sim_matches_textbook(P):
+    g = gg.rmat(9, seed=11)
+    ro, col = g.row_offsets.numpy(), g.col_idx.numpy().astype(np.int64)
+    for s in gg.sample_sources(g, 2):
+        lv, sizes = ps.bfs_partitioned(ro, col, g.num_vertices, s, P)
+        ref = tb.bfs(g, s)
+        np.testing.assert_array_equal(lv, ref)
+        assert sizes == tb.level_sizes(ref)
+
+
+def test_partition_sim_grid_closed_form():
+    g = gg.grid(9, 6)
+    lv, _ = ps.bfs_partitioned(g.row_offsets.numpy(), g.col_idx.numpy().astype(np.int64), 54, 0, 4)
+    r, c = np.divmod(np.arange(54), 6)
+    np.testing.assert_array_equal(lv, r + c)
+
+
+# ---------------- preemption model (Table 3) ----------------
+def test_preemption_closed_form_table3():
+    fx = golden("table3_preemption.json")
+    for row in fx["rows"]:
+        assert abs(pre.preemption_overhead(row["P_ms"], row["D_ms"]) - row["kernel_level"]) <= fx["rounding"]
+    assert pre.preemption_overhead(10, 0) == 1.0
+    with pytest.raises(ValueError):
+        pre.preemption_overhead(10, 10)
+
+
+# ---------------- generators ----------------
+def test_grid_shape_and_sorted_neighbours():
+    g = gg.grid(2048, 2048) if False else gg.grid(64, 32)
+    V = 64 * 32
+    assert g.num_edges == 2 * (2 * 64 * 32 - 64 - 32)
+    ro, col = g.row_offsets.numpy(), g.col_idx.numpy()
+    for v in [0, 31, 32, 1000, V - 1]:
+        nb = col[ro[v]:ro[v + 1]]
+        assert (np.diff(nb) > 0).all()
+        r, c = divmod(v, 32)
+        exp = sorted([x for x in [v - 32 if r else None, v - 1 if c else None,
+                                  v + 1 if c < 31 else None, v + 32 if r < 63 else None] if x is not None])
+        assert nb.tolist() == exp
+
+
+def test_rmat_properties_and_determinism():
+    g1 = gg.rmat(10, seed=7)
+    g2 = gg.rmat(10, seed=7)
+    assert gg.graph_hash(g1) == gg.graph_hash(g2)
+    assert gg.graph_hash(gg.rmat(10, seed=8)) != gg.graph_hash(g1)
+    ro, col = g1.row_offsets.numpy(), g1.col_idx.numpy()
+    src = np.repeat(np.arange(g1.num_vertices), np.diff(ro))
+    assert (src != col).all()                                      # no self loops
+    key = src.astype(np.int64) * g1.num_vertices + col
+    assert (np.diff(key) > 0).all()                                # sorted, no duplicates
+    rev = np.sort(col.astype(np.int64) * g1.num_vertices + src)
+    np.testing.assert_array_equal(rev, key)                        # symmetric
+    deg = np.diff(ro)
+    assert deg.max() > 20 * deg.mean()                             # skewed (R-MAT)
+    # chunked generation gives the same graph
+    assert gg.graph_hash(gg.rmat(10, seed=7, chunk=1000)) == gg.graph_hash(g1)
+
+
+def test_weights_symmetric_and_in_range():
+    g = gg.with_weights(gg.rmat(9, seed=3), seed=5)
+    w = g.weights.numpy()
+    assert w.min() >= 1 and w.max() <= 1000
+    ro, col = g.row_offsets.numpy(), g.col_idx.numpy()
+    src = np.repeat(np.arange(g.num_vertices), np.diff(ro))
+    d = {(int(a), int(b)): int(x) for a, b, x in zip(src, col, w)}
+    assert all(d[(b, a)] == x for (a, b), x in d.items())
+
+
+def test_splitmix64_reference_values():
+    # splitmix64 of state 0 / 1 (Vigna's reference generator, first outputs)
+    assert gg.splitmix64_int(0) == 0xE220A8397B1DCDAF
+    t = gg.splitmix64(torch.tensor([0, 1, -1], dtype=torch.int64))
+    assert [int(x) & ((1 << 64) - 1) for x in t] == [gg.splitmix64_int(0), gg.splitmix64_int(1),
+                                                      gg.splitmix64_int((1 << 64) - 1)]
