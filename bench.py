@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""bench.py -- cooperative BFS on B200 (BASELINE.json metric: GTEPS; configs[2]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--scale S] [--quick]
+
+A step = one cooperative BFS (the whole hot path of SURVEY §8(a): persistent
+launch, init, per-level expand/claim/compact, resizing barriers, termination)
+from one source of RMAT-24 (Graph500 parameters, seed 1), inputs
+resident in HBM.  Sources are distinct degree>0 vertices (seed 2).  The CSR
+(2.2 GB) is larger than the 126 MB L2 and L2 is additionally flushed (256 MB
+write) before every timed step.  Time: CUDA events on the launching stream
+around each call; value = GTEPS (Graph500 convention: undirected edges of the
+reached component / time).  Extra objects report the multitasked run (periodic
+competing task), the non-cooperative persistent baseline, ns per barrier vs the
+L2 atomic round trip, and SSSP on the 2048x2048 grid (configs[1]).
+
+--impl reference times the oracle (oracle/textbook.c, 1 host core) on the same
+workload: the base contract's reference arm for this tier.
+Under torchrun (N>1): rank 0 prints; per-rank independent replicas of the
+single-GPU step are timed (max over ranks) until the partitioned path is the
+default.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BFS/SSSP GTEPS at 1/2/4/8 B200 (alone vs multitasked); barrier ns; kill latency"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for n, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_graph(scale, device):
+    import graphgen as gg
+    t = time.time()
+    g = gg.rmat(scale, seed=1, device=device, chunk=1 << 26)
+    return g, time.time() - t
+
+
+def oracle_gteps(g_host, sources, budget_s, deg):
+    """Time the oracle (C textbook BFS, 1 core) on as many sources as fit the budget."""
+    import numpy as np
+    from oracle import textbook as tb
+    ro = g_host.row_offsets.numpy().astype(np.int64)
+    col = g_host.col_idx.numpy()
+    V = g_host.num_vertices
+    edges = 0
+    secs = 0.0
+    n = 0
+    for s in sources:
+        t = time.perf_counter()
+        lv = tb.bfs_arrays(V, ro, col, s)
+        secs += time.perf_counter() - t
+        edges += int(deg[lv >= 0].sum()) // 2
+        n += 1
+        if secs >= budget_s:
+            break
+    return edges / secs / 1e9, n, secs
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    import torch
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    g, _ = make_graph(args.scale, dev)
+    import graphgen as gg
+    srcs = gg.sample_sources(g, 64, seed=2)
+    gh = g.to("cpu")
+    deg = gh.degrees().numpy()
+    del g
+    import numpy as np
+    from oracle import textbook as tb
+    ro = gh.row_offsets.numpy().astype(np.int64)
+    col = gh.col_idx.numpy()
+    V = gh.num_vertices
+    times, edges = [], []
+    for i in range(args.warmup + args.steps):
+        s = srcs[i % len(srcs)]
+        t = time.perf_counter()
+        lv = tb.bfs_arrays(V, ro, col, s)
+        dt = time.perf_counter() - t
+        if i >= args.warmup:
+            times.append(dt)
+            edges.append(int(deg[lv >= 0].sum()) // 2)
+    val = sum(edges) / sum(times) / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GTEPS", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (RMAT, Graph500 parameters, seeded)",
+            "config": {"workload": f"BFS RMAT-{args.scale} (configs[2]) from {args.steps} sources",
+                       "scale": args.scale, "edgefactor": 16, "vertices": V, "directed_edges": gh.num_edges},
+            "cpu_baseline": {"value": val, "unit": "GTEPS", "cores": 1, "kind": "oracle",
+                             "sample": f"{args.steps} full single-source BFS runs of oracle/textbook.c"},
+            "e2e": {"value": val, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, ws, rank, local):
+    import numpy as np
+    import torch
+    import graphgen as gg
+    from paper_1707_01989_b200 import coop
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    coop.load()
+    info = coop.device_query(local, args.threads)
+    g, gen_s = make_graph(args.scale, dev)
+    V, E = g.num_vertices, g.num_edges
+    deg = g.degrees()
+    srcs = gg.sample_sources(g, 64, seed=2)
+    out = torch.empty(V, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    n_steps = args.warmup + args.steps
+
+    def one(i, **kw):
+        s = srcs[(i + rank * 7) % len(srcs)]
+        flush.fill_(i & 0xFF)                                # L2 flush (untimed)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record(stream)                                    # materialise the cudaEvent handles;
+        k1.record(stream)                                    # libcoop re-records them around the kernel
+        e0.record(stream)
+        _, st = coop.bfs(g, s, out, threads_per_wg=args.threads, ev_kernel_start=k0, ev_kernel_end=k1,
+                         event_cap=kw.pop("event_cap", 0), **kw)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1), k0.elapsed_time(k1), st
+
+    # ---- main: standalone cooperative BFS (NeverResize)
+    for i in range(args.warmup):
+        one(i)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    times, ktimes, edges, reached, scanned = [], [], [], [], []
+    with ClockSampler(local) as clk:
+        for i in range(args.warmup, n_steps):
+            t, kt, st = one(i)
+            times.append(t)
+            ktimes.append(kt)
+            edges.append(st.edges_scanned // 2)
+            scanned.append(st.edges_scanned)
+            reached.append(st.reached)
+    torch.cuda.synchronize(dev)
+    tot_ms = sum(times)
+    if ws > 1:
+        t = torch.tensor([tot_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot_ms = float(t.item())
+        ed = torch.tensor([float(sum(edges))], device=dev)
+        torch.distributed.all_reduce(ed)
+        all_edges = float(ed.item())
+    else:
+        all_edges = float(sum(edges))
+    gteps = all_edges / (tot_ms * 1e-3) / 1e9
+    # roofline of the persistent kernel: algorithmic bytes per launch / kernel time
+    peak, peak_src = _peaks()
+    s_o = 4
+    alg_bytes = [4 * sc + (12 + 2 * s_o) * r + 4 * V + V // 8 for sc, r in zip(scanned, reached)]
+    achieved = sum(alg_bytes) / (sum(ktimes) * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("bfs_rmat24", {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    extras = {}
+    if rank == 0 and not args.quick:
+        extras = run_extras(args, g, srcs, out, flush, stream, dev, info, times)
+
+    # ---- end to end through the C ABI with HOST buffers (H2D graph + D2H levels inside)
+    e2e = None
+    if rank == 0:
+        ro_h = g.row_offsets.to(torch.int32).cpu().pin_memory()
+        col_h = g.col_idx.cpu().pin_memory()
+        lv_h = torch.empty(V, dtype=torch.int32).pin_memory()
+        et, ee = [], []
+        for i in range(1 + 3):
+            s = srcs[i]
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            _, st = coop.bfs_host(ro_h, col_h, s, lv_h, threads_per_wg=args.threads)
+            dt = time.perf_counter() - t0
+            if i >= 1:
+                et.append(dt)
+                ee.append(st.edges_scanned // 2)
+        e2e = {"value": sum(ee) / sum(et) / 1e9, "unit": "GTEPS",
+               "h2d_bytes_per_step": int(ro_h.numel() * 4 + col_h.numel() * 4),
+               "d2h_bytes_per_step": int(V * 4), "steps": len(et)}
+        del ro_h, col_h
+    # ---- CPU oracle baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        gh = g.to("cpu")
+        dh = gh.degrees().numpy()
+        v, n, secs = oracle_gteps(gh, srcs, args.cpu_budget, dh)
+        cpu = {"value": v, "unit": "GTEPS", "cores": 1, "kind": "oracle",
+               "sample": f"{n} single-source BFS runs of oracle/textbook.c on the same RMAT-{args.scale} "
+                         f"({secs:.1f} s of CPU work)"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": gteps, "unit": "GTEPS", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (RMAT, Graph500 parameters a,b,c=.57,.19,.19, edgefactor 16, seed 1, relabelled)",
+            "config": {"workload": f"BFS RMAT-{args.scale} (configs[2]), standalone cooperative, NeverResize",
+                       "scale": args.scale, "vertices": V, "directed_edges": E, "sources": args.steps,
+                       "wgs": info["max_coresident"], "threads_per_wg": args.threads,
+                       "l2": "flushed (256 MB write) before every step; CSR 2.2 GB > L2",
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
+                       "graph_gen_s": round(gen_s, 2)},
+            "kernel_ms_per_step": sum(ktimes) / len(ktimes),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "coop_kernel<BfsApp<uint32_t>,%d>" % args.threads,
+                         "alg_bytes_per_launch": sum(alg_bytes) / len(alg_bytes)},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+            **extras,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times):
+    import torch
+    import graphgen as gg
+    from paper_1707_01989_b200 import coop
+    ex = {}
+    N = info["max_coresident"]
+
+    def timed(fn):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1), r
+
+    k = min(args.steps, 8)
+    # non-cooperative persistent baseline (plain global barrier), same N and block size
+    t_plain, t_coop = [], []
+    for i in range(k + 1):
+        tp, (_, stp) = timed(lambda: coop.bfs(g, srcs[i], out, threads_per_wg=args.threads,
+                                                barrier_mode=coop.BARRIER_PLAIN))
+        tc, (_, stc) = timed(lambda: coop.bfs(g, srcs[i], out, threads_per_wg=args.threads))
+        if i:
+            t_plain.append(tp)
+            t_coop.append(tc)
+    ex["noncoop_baseline"] = {"ms_coop": statistics.median(t_coop), "ms_noncoop": statistics.median(t_plain),
+                              "slowdown": statistics.median(t_coop) / statistics.median(t_plain)}
+    # multitasked: scheduler CTA posts a task every P with Q = N/4 WGs (scaled light preset)
+    mt = {}
+    for name, (P_us, E_us) in {"stress": (200, 20)}.items():
+        q = max(1, (N - 1) // 4)
+        blocks = 4 * q
+        block_ns = int(E_us * 1000 * (N - 1) / blocks)
+        tt, lat, gat, tasks = [], [], [], 0
+        for i in range(k + 1):
+            t, (_, st) = timed(lambda: coop.bfs(g, srcs[i], out, threads_per_wg=args.threads,
+                                                policy=coop.POLICY_SCHEDULER, task_wgs=q, task_blocks=blocks,
+                                                task_block_ns=block_ns, task_period_ns=P_us * 1000,
+                                                task_first_ns=0, event_cap=4096))
+            if i:
+                tt.append(t)
+                tasks += st.tasks_completed
+                for e in st.task_events:
+                    if e["t_first_start"]:
+                        lat.append((e["t_first_start"] - e["t_arrive"]) / 1e3)
+                    if e["t_last_surrender"]:
+                        gat.append((e["t_last_surrender"] - e["t_arrive"]) / 1e3)
+        # standalone reference with the scheduler CTA present (N-1 workers)
+        def pct(v, p):
+            v = sorted(v)
+            return v[min(len(v) - 1, int(p * len(v)))] if v else None
+        mt[name] = {"period_us": P_us, "work_us_at_full": E_us, "task_wgs": q,
+                    "ms_per_bfs": statistics.median(tt),
+                    "slowdown_vs_standalone": statistics.median(tt) / statistics.median(t_coop),
+                    "kill_latency_us_p50": pct(lat, 0.5), "kill_latency_us_p99": pct(lat, 0.99),
+                    "gather_us_p50": pct(gat, 0.5), "gather_us_p99": pct(gat, 0.99),
+                    "tasks_completed": tasks, "gteps": None}
+    ex["multitask"] = mt
+    # barrier ns vs L2 atomic RTT (configs[3] points)
+    rtt = coop.l2_atomic_rtt(200000)
+    bar = {}
+    for n in (148, 592, 1184):
+        r = coop.barrier_bench(n, 200000, threads=128, plain=True)
+        r2 = coop.barrier_bench(n, 200000, threads=128, resize_prob=1 / 64, seed=3)
+        bar[str(n)] = {"plain_ns": r["ns_per_barrier"], "resizing_p1_64_ns": r2["ns_per_barrier"],
+                       "kills": r2["kills"], "forks": r2["forks"]}
+    ex["barrier"] = {"l2_atomic_rtt_ns": rtt, "per_ctas": bar}
+    # SSSP on the 2048x2048 grid (configs[1])
+    gw = gg.with_weights(gg.grid(2048, 2048, device=dev), seed=1)
+    gw.max_weight = 1000
+    dout = torch.empty(gw.num_vertices, dtype=torch.int32, device=dev)
+    ts = []
+    for i in range(3):
+        t, (_, st) = timed(lambda: coop.sssp(gw, 0, dout, threads_per_wg=256, max_wgs=148))
+        if i:
+            ts.append(t)
+    m_und = gw.num_edges // 2
+    ex["sssp_grid2048"] = {"ms": statistics.median(ts), "gteps": m_und / (statistics.median(ts) * 1e-3) / 1e9,
+                           "rounds": st.levels, "ns_per_round": statistics.median(ts) * 1e6 / max(1, st.levels)}
+    return ex
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--threads", type=int, default=512)
+    ap.add_argument("--quick", action="store_true", help="skip the extra objects")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    run_ours(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,235 @@
+/*
+ * coop.h -- C ABI of libcoop: cooperative kernels (Sorensen, Evrard, Donaldson,
+ * arXiv 1707.01989) on NVIDIA B200 (sm_100a).
+ *
+ * The library runs the paper's hot path -- Fig. 4's cooperative graph
+ * traversal as BFS and as worklist SSSP -- inside ONE
+ * persistent kernel per call.  Its CTAs are the paper's workgroups: at most N
+ * are resident (occupancy-bound execution), M of them are
+ * active with contiguous ids [0, M).  They meet at a
+ * resizing global barrier (efficient "query" form
+ * PAPER.md:936-950) where the scheduler may kill the top ids (offer_kill,
+ * PAPER.md:529-550) or fork new ids that receive workgroup 0's transmitted
+ * state (request_fork).  Killed CTAs park in an in-kernel
+ * worker loop that runs a competing non-cooperative task (megakernel,
+ * PAPER.md:805-826); a scheduler CTA posts the task and the
+ * resource messages.
+ *
+ * Conventions (all functions):
+ *   - Every function returns a coop_status and never aborts or throws.  On any
+ *     status other than COOP_OK, outputs are unspecified and
+ *     coop_last_error() describes the failure (thread-local string).
+ *   - "device" pointers are CUDA device pointers on the current device (e.g.
+ *     torch tensor data_ptr()); "host" pointers are ordinary CPU memory.
+ *   - The caller owns graph, output and stats buffers.  The library owns its
+ *     scratch (queues, bitmaps, control words), cached per device and reused.
+ *   - Blocking calls (coop_bfs, coop_sssp, ...) enqueue on opts->stream and
+ *     synchronise that stream before returning.  One in-flight call per stream.
+ *   - Nothing in the library falls back to the CPU.
+ */
+#ifndef COOP_H
+#define COOP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define COOP_ABI_VERSION 1
+
+typedef enum {
+    COOP_OK = 0,
+    COOP_ERR_INVALID_ARG = 1,      /* bad pointer, size, source out of range, bad option */
+    COOP_ERR_CUDA = 2,             /* a CUDA runtime call failed (no device, launch failure, ...) */
+    COOP_ERR_NOT_CORESIDENT = 3,   /* N (+ scheduler CTA) exceeds the co-resident CTA capacity */
+    COOP_ERR_FORK_BOUND = 4,       /* a grant would exceed N - M */
+    COOP_ERR_NO_CAPACITY = 5,      /* a task asks for more than N - 1 workgroups (WG 0 is never killed) */
+    COOP_ERR_TIMEOUT = 6,          /* in-kernel watchdog fired (a spin exceeded opts->timeout_ns) */
+    COOP_ERR_OVERFLOW = 7,         /* SSSP: (V-1) * max_weight >= 2^32 - 1, distances not representable */
+    COOP_ERR_NCCL = 8,             /* reserved for the partitioned multi-GPU path */
+    COOP_ERR_INVARIANT = 9,        /* COOP_FLAG_CHECK: a barrier / contiguity invariant was violated */
+    COOP_ERR_BUSY = 10             /* handle API: operation not valid in the handle's state */
+} coop_status;
+
+/* Resizing-barrier implementation. */
+typedef enum {
+    COOP_BARRIER_QUERY = 0,   /* query barrier: all W demanded WGs leave in one episode */
+    COOP_BARRIER_PLAIN = 1,   /* NON-cooperative baseline: plain global barrier, all N CTAs, no scheduler
+                                 interaction (Fig. 3); used for the overhead comparison */
+    COOP_BARRIER_NAIVE = 2    /* naive barrier: a WG offers kill once on entry, so ~1 WG leaves per episode */
+} coop_barrier_mode;
+
+/* Who decides M' at each resizing barrier (the nondeterministic scheduler choice). */
+typedef enum {
+    COOP_POLICY_NEVER = 0,     /* never resize */
+    COOP_POLICY_SCRIPTED = 1,  /* M' = script[episode] (0 = unchanged); waits for parked CTAs so the script is exact */
+    COOP_POLICY_RANDOM = 2,    /* with probability resize_prob, M' ~ U[1, N] (counter RNG keyed by seed, episode) */
+    COOP_POLICY_SCHEDULER = 3  /* scheduler CTA: periodic competing task, demand/grant resource messages */
+} coop_policy;
+
+#define COOP_FLAG_CHECK 0x1u   /* per-episode arrival / contiguity / message-passing checks -> COOP_ERR_INVARIANT */
+
+/* CSR graph, device memory, neighbour lists of vertex v at [row_offsets[v], row_offsets[v+1]). */
+typedef struct {
+    int64_t num_vertices;       /* V >= 1 */
+    int64_t num_edges;          /* E = row_offsets[V] (directed entries) */
+    const void *row_offsets;    /* device, V+1 entries, uint32 (offset_bits=32) or int64 (offset_bits=64) */
+    int32_t offset_bits;        /* 32 or 64 */
+    const int32_t *col_idx;     /* device, E entries in [0, V) */
+    const uint32_t *weights;    /* device, E entries >= 1 (SSSP), NULL for BFS */
+    uint32_t max_weight;        /* SSSP: max of weights (0 = unknown: the library computes it) */
+} coop_csr;
+
+typedef struct {
+    uint32_t max_wgs;           /* N: 0 = max co-resident for threads_per_wg */
+    uint32_t init_wgs;          /* M0 in [1, N]: 0 = N */
+    uint32_t threads_per_wg;    /* 0 = 512; supported: 128, 256, 512, 1024 */
+    uint32_t barrier_mode;      /* coop_barrier_mode */
+    uint32_t barriers_per_level;/* 1 (fused) or 2 (Fig. 4 exactly: RB; reset; level++; RB) */
+    uint32_t policy;            /* coop_policy */
+    const uint32_t *script;     /* host: SCRIPTED M' per resizing episode, 0 = unchanged */
+    uint32_t script_len;
+    uint32_t flags;             /* COOP_FLAG_* */
+    uint64_t seed;              /* RANDOM policy */
+    double resize_prob;         /* RANDOM policy */
+    /* SCHEDULER policy: the competing non-cooperative task (synthetic, K11 of SURVEY) */
+    uint32_t task_wgs;          /* Q: workgroups demanded per task instance, 1 <= Q <= N-1 */
+    uint32_t task_blocks;       /* independent blocks per instance */
+    uint64_t task_block_ns;     /* busy time of one block */
+    uint64_t task_period_ns;    /* P: arrival period of task instances */
+    uint64_t task_first_ns;     /* delay of the first arrival after kernel start */
+    uint32_t task_max;          /* max instances per call (0 = unbounded) */
+    uint64_t timeout_ns;        /* watchdog for every spin loop: 0 = 20 s */
+    void *stream;               /* cudaStream_t (NULL = legacy default stream) */
+    void *ev_kernel_start;      /* optional cudaEvent_t recorded on `stream` right before the persistent kernel */
+    void *ev_kernel_end;        /* optional cudaEvent_t recorded on `stream` right after it (kernel-only timing) */
+} coop_opts;
+
+/* One competing-task instance, all times from %globaltimer (ns). */
+typedef struct {
+    uint64_t t_arrive;          /* scheduler posted the demand */
+    uint64_t t_first_surrender; /* first demanded WG killed */
+    uint64_t t_last_surrender;  /* demand fully satisfied (gather time = this - t_arrive) */
+    uint64_t t_first_start;     /* first task block started (kill latency = this - t_arrive) */
+    uint64_t t_end;             /* last task block finished */
+    uint32_t demanded;          /* Q */
+    uint32_t surrendered;       /* WGs killed for this instance */
+} coop_task_event;
+
+typedef struct {
+    uint64_t kernel_ns;         /* %globaltimer, WG 0 from kernel entry to termination */
+    uint64_t edges_scanned;     /* sum of degrees of expanded frontier entries */
+    uint64_t frontier_total;    /* sum of frontier sizes */
+    uint64_t reached;           /* vertices with a finite result */
+    uint32_t levels;            /* non-empty frontiers (BFS depth+1 / SSSP rounds) */
+    uint32_t episodes;          /* resizing barriers executed */
+    uint32_t kills, forks;      /* workgroups killed / forked */
+    uint32_t min_m, max_m;      /* range of M over the run */
+    uint32_t n_wgs;             /* N launched */
+    uint32_t threads_per_wg;
+    uint32_t tasks_posted, tasks_completed;
+    uint32_t *m_trace;          /* optional caller-owned HOST buffer: M after each resizing episode */
+    uint32_t m_trace_cap;
+    uint32_t *level_sizes;      /* optional caller-owned HOST buffer: frontier size per level */
+    uint32_t level_sizes_cap;
+    coop_task_event *task_events; /* optional caller-owned HOST buffer */
+    uint32_t task_events_cap;
+} coop_stats;
+
+typedef struct {
+    int device;
+    int sm_count;
+    int max_ctas_per_sm;        /* for threads_per_wg of the query */
+    int max_coresident;         /* sm_count * max_ctas_per_sm */
+    int regs_per_thread;
+    size_t l2_bytes;
+    size_t hbm_bytes;
+} coop_device_info;
+
+typedef struct {
+    uint64_t iters;             /* resizing barriers executed */
+    double ns_per_barrier;      /* cudaEvent time / iters */
+    uint64_t kernel_ns;
+    uint32_t kills, forks;
+    uint32_t violations;        /* 0 unless an invariant failed (status is then COOP_ERR_INVARIANT) */
+} coop_barrier_stats;
+
+/* ---- library ---- */
+int coop_abi_version(void);
+const char *coop_status_string(coop_status s);
+const char *coop_last_error(void);   /* thread-local description of the last failure */
+
+/* Co-residency capacity of the BFS/SSSP kernel for threads_per_wg on `device`. */
+coop_status coop_device_query(int device, uint32_t threads_per_wg, coop_device_info *out);
+
+/*
+ * Cooperative BFS (Fig. 4; bfs of Table 1).
+ * levels_out: device int32[V]; on COOP_OK levels_out[v] = hop distance from
+ * `source`, -1 if unreachable.  Bit-exact for every kill/fork schedule.
+ */
+coop_status coop_bfs(const coop_csr *g, int64_t source, int32_t *levels_out,
+                     const coop_opts *opts, coop_stats *stats);
+
+/*
+ * Cooperative worklist SSSP (l-sssp of Table 1; reading R8 of DESIGN.md).
+ * dist_out: device uint32[V]; on COOP_OK dist_out[v] = min path weight,
+ * 0xFFFFFFFF if unreachable.  Needs g->weights.  COOP_ERR_OVERFLOW if
+ * (V-1) * max_weight >= 2^32 - 1.
+ */
+coop_status coop_sssp(const coop_csr *g, int64_t source, uint32_t *dist_out,
+                      const coop_opts *opts, coop_stats *stats);
+
+/*
+ * End-to-end variants: graph arrays and the output are HOST pointers.  The
+ * call copies the CSR to the device, runs the cooperative kernel and copies
+ * the result back (all inside the call; device memory is cached between calls).
+ */
+coop_status coop_bfs_host(int64_t num_vertices, const void *row_offsets, int32_t offset_bits,
+                          const int32_t *col_idx, int64_t source, int32_t *levels_out,
+                          const coop_opts *opts, coop_stats *stats);
+coop_status coop_sssp_host(int64_t num_vertices, const void *row_offsets, int32_t offset_bits,
+                           const int32_t *col_idx, const uint32_t *weights, uint32_t max_weight,
+                           int64_t source, uint32_t *dist_out, const coop_opts *opts, coop_stats *stats);
+
+/*
+ * Resizing-barrier microbenchmark (BASELINE.json configs[3]): n_ctas CTAs of
+ * `threads` threads execute `iters` resizing barriers; with probability
+ * resize_prob per episode M' ~ U[1, n_ctas].  barrier_mode QUERY or PLAIN.
+ * flags COOP_FLAG_CHECK adds the arrival-count, contiguity and
+ * message-passing checks.
+ */
+coop_status coop_barrier_bench(uint32_t n_ctas, uint32_t threads, uint64_t iters, double resize_prob,
+                               uint64_t seed, uint32_t barrier_mode, uint32_t flags,
+                               coop_barrier_stats *out);
+
+/*
+ * L2 atomic round trip: one thread issues `iters` dependent atomicAdd on one
+ * word; returns ns per atomic (the denominator for ns/barrier).
+ */
+coop_status coop_l2_atomic_rtt(uint64_t iters, double *ns_per_atomic);
+
+/* ---- asynchronous handle API (host <-> GPU channel) ---- */
+typedef struct coop_handle coop_handle;
+
+/* Launch cooperative BFS (kind 0) or SSSP (kind 1) asynchronously; opts->policy
+ * must be COOP_POLICY_SCHEDULER.  Resource messages and tasks then come from the
+ * host through a host-mapped mailbox polled by the scheduler CTA (the paper's
+ * SVM channel) in addition to the periodic generator (task_period_ns
+ * = 0 disables it). `out` is levels (int32*) or dist (uint32*), device. */
+coop_status coop_launch(int kind, const coop_csr *g, int64_t source, void *out,
+                        const coop_opts *opts, coop_handle **handle);
+/* Post one task instance of task_wgs WGs (validated: 1 <= task_wgs <= N-1 else NO_CAPACITY). */
+coop_status coop_submit_task(coop_handle *h, uint32_t task_wgs, uint32_t task_blocks,
+                             uint64_t task_block_ns, uint64_t *task_id);
+coop_status coop_demand(coop_handle *h, uint32_t kills);   /* resource message: surrender `kills` WGs */
+coop_status coop_grant(coop_handle *h, uint32_t forks);    /* resource message: fork up to `forks` WGs */
+coop_status coop_query(coop_handle *h, uint32_t *W);       /* outstanding demand (query) */
+coop_status coop_current_m(coop_handle *h, uint32_t *M);   /* active workgroups right now */
+coop_status coop_wait(coop_handle *h, coop_stats *stats);  /* wait for termination, fill stats */
+void coop_destroy(coop_handle *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COOP_H */

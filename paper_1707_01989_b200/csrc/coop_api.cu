@@ -1,0 +1,708 @@
+// coop_api.cu -- host side of libcoop: the C ABI declared in include/coop.h.
+//
+// Each blocking call: validate -> size the persistent grid from the occupancy
+// API (co-residency) -> stage the control block -> one
+// cooperative-attribute launch (co-residency is guaranteed or the launch
+// fails; grid.sync is never used) -> read back the control block -> map the
+// device error word to a coop_status.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "../../include/coop.h"
+#include "apps.cuh"
+
+using namespace coop;
+
+// ------------------------------------------------------------------ errors
+static thread_local char g_err[512];
+
+static coop_status fail(coop_status s, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return s;
+}
+#define CUDA_TRY(x)                                                                          \
+    do {                                                                                     \
+        cudaError_t e_ = (x);                                                                \
+        if (e_ != cudaSuccess) {                                                             \
+            cudaGetLastError();                                                              \
+            return fail(COOP_ERR_CUDA, "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                                 \
+        }                                                                                    \
+    } while (0)
+
+extern "C" int coop_abi_version(void) { return COOP_ABI_VERSION; }
+
+extern "C" const char *coop_status_string(coop_status s) {
+    switch (s) {
+        case COOP_OK: return "COOP_OK";
+        case COOP_ERR_INVALID_ARG: return "COOP_ERR_INVALID_ARG";
+        case COOP_ERR_CUDA: return "COOP_ERR_CUDA";
+        case COOP_ERR_NOT_CORESIDENT: return "COOP_ERR_NOT_CORESIDENT";
+        case COOP_ERR_FORK_BOUND: return "COOP_ERR_FORK_BOUND";
+        case COOP_ERR_NO_CAPACITY: return "COOP_ERR_NO_CAPACITY";
+        case COOP_ERR_TIMEOUT: return "COOP_ERR_TIMEOUT";
+        case COOP_ERR_OVERFLOW: return "COOP_ERR_OVERFLOW";
+        case COOP_ERR_NCCL: return "COOP_ERR_NCCL";
+        case COOP_ERR_INVARIANT: return "COOP_ERR_INVARIANT";
+        case COOP_ERR_BUSY: return "COOP_ERR_BUSY";
+    }
+    return "COOP_ERR_UNKNOWN";
+}
+
+extern "C" const char *coop_last_error(void) { return g_err; }
+
+// ------------------------------------------------------------------ kernels
+template <class App, int BLOCK>
+static void *kernel_ptr() {
+    constexpr int MINB = BLOCK >= 1024 ? 1 : 1024 / BLOCK;
+    return reinterpret_cast<void *>(&coop_kernel<App, BLOCK, MINB>);
+}
+
+template <class App>
+static void *pick_block(uint32_t threads) {
+    switch (threads) {
+        case 256: return kernel_ptr<App, 256>();
+        case 512: return kernel_ptr<App, 512>();
+        case 1024: return kernel_ptr<App, 1024>();
+        default: return nullptr;
+    }
+}
+
+static void *select_kernel(uint32_t app, int off64, uint32_t threads) {
+    if (app == APP_BFS) return off64 ? pick_block<BfsApp<int64_t>>(threads) : pick_block<BfsApp<uint32_t>>(threads);
+    if (app == APP_SSSP) return off64 ? pick_block<SsspApp<int64_t>>(threads) : pick_block<SsspApp<uint32_t>>(threads);
+    switch (threads) {
+        case 128: return kernel_ptr<BarrierApp, 128>();
+        case 256: return kernel_ptr<BarrierApp, 256>();
+        case 512: return kernel_ptr<BarrierApp, 512>();
+        case 1024: return kernel_ptr<BarrierApp, 1024>();
+    }
+    return nullptr;
+}
+
+__global__ void max_u32_kernel(const uint32_t *w, int64_t n, uint32_t *out) {
+    uint32_t m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, w[i]);
+    for (int s = 16; s; s >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, s));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+__global__ void l2_rtt_kernel(unsigned long long *word, uint64_t iters, unsigned long long *out_ns) {
+    unsigned long long v = 0;
+    const uint64_t t0 = globaltimer();
+    for (uint64_t i = 0; i < iters; ++i) v = atomicAdd(word + (v & 0), 1ull);   // dependent chain
+    const uint64_t t1 = globaltimer();
+    out_ns[0] = t1 - t0;
+    out_ns[1] = v;
+}
+
+// ------------------------------------------------------------------ scratch
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t n) {
+        if (n <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max<size_t>(n, 256);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+};
+
+struct Scratch {
+    int device = -1;
+    DevBuf ctl, mb, visited, qlev, ql0, ql1, qh0, qh1, stamp, mtrace, lsizes, events, script, wmax;
+    DevBuf h_ro, h_col, h_w, h_out;   // end-to-end (host-pointer) calls
+    Ctl *host_ctl = nullptr;          // pinned staging
+    std::mutex mu;
+};
+
+static Scratch g_scratch[16];
+
+static coop_status get_scratch(Scratch **out) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 16) return fail(COOP_ERR_INVALID_ARG, "device %d out of range", dev);
+    Scratch *s = &g_scratch[dev];
+    if (!s->host_ctl) CUDA_TRY(cudaHostAlloc((void **)&s->host_ctl, sizeof(Ctl), cudaHostAllocDefault));
+    s->device = dev;
+    *out = s;
+    return COOP_OK;
+}
+
+// ------------------------------------------------------------------ device info
+static coop_status occupancy(void *kern, uint32_t threads, int *sm_count, int *per_sm) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, (int)threads, 0));
+    return COOP_OK;
+}
+
+extern "C" coop_status coop_device_query(int device, uint32_t threads_per_wg, coop_device_info *out) {
+    if (!out) return fail(COOP_ERR_INVALID_ARG, "out is NULL");
+    if (threads_per_wg == 0) threads_per_wg = 512;
+    void *k = select_kernel(APP_BFS, 0, threads_per_wg);
+    if (!k) return fail(COOP_ERR_INVALID_ARG, "threads_per_wg %u not supported (256/512/1024)", threads_per_wg);
+    int cur = 0;
+    CUDA_TRY(cudaGetDevice(&cur));
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    int sms = 0, per = 0;
+    coop_status st = occupancy(k, threads_per_wg, &sms, &per);
+    cudaFuncAttributes fa;
+    CUDA_TRY(cudaFuncGetAttributes(&fa, k));
+    CUDA_TRY(cudaSetDevice(cur));
+    if (st != COOP_OK) return st;
+    out->device = device;
+    out->sm_count = sms;
+    out->max_ctas_per_sm = per;
+    out->max_coresident = sms * per;
+    out->regs_per_thread = fa.numRegs;
+    out->l2_bytes = (size_t)prop.l2CacheSize;
+    out->hbm_bytes = prop.totalGlobalMem;
+    return COOP_OK;
+}
+
+// ------------------------------------------------------------------ launch core
+struct RunReq {
+    uint32_t app;
+    const coop_csr *g;
+    int64_t source;
+    void *out;
+    const coop_opts *opts;
+    coop_stats *stats;
+    uint64_t iters;             // barrier bench
+    HostChannel *host;          // handle API (device pointer of mapped host memory)
+    bool async;                 // do not synchronise (handle API)
+};
+
+static coop_status fill_stats(const Ctl &c, const KParams &kp, coop_stats *st, cudaStream_t stream) {
+    if (!st) return COOP_OK;
+    st->kernel_ns = c.t_end > c.t_start ? c.t_end - c.t_start : 0;
+    st->edges_scanned = c.edges_scanned;
+    st->frontier_total = c.frontier_total;
+    st->reached = c.reached;
+    st->levels = c.levels;
+    st->episodes = c.episode;
+    st->kills = c.kills;
+    st->forks = c.forks;
+    st->min_m = c.min_m;
+    st->max_m = c.max_m;
+    st->n_wgs = kp.P;
+    st->tasks_posted = c.tasks_posted;
+    st->tasks_completed = c.tasks_completed;
+    if (st->m_trace && st->m_trace_cap) {
+        uint32_t n = std::min(st->m_trace_cap, std::min(c.episode, kp.m_trace_cap));
+        if (n) CUDA_TRY(cudaMemcpyAsync(st->m_trace, kp.m_trace, n * 4, cudaMemcpyDeviceToHost, stream));
+    }
+    if (st->level_sizes && st->level_sizes_cap) {
+        uint32_t n = std::min(st->level_sizes_cap, std::min(c.levels + 1, kp.level_cap));
+        if (n) CUDA_TRY(cudaMemcpyAsync(st->level_sizes, kp.level_sizes, n * 4, cudaMemcpyDeviceToHost, stream));
+    }
+    if (st->task_events && st->task_events_cap) {
+        uint32_t n = std::min(st->task_events_cap, c.n_events);
+        std::vector<TaskEventDev> tmp(n);
+        if (n) {
+            CUDA_TRY(cudaMemcpyAsync(tmp.data(), kp.events, n * sizeof(TaskEventDev), cudaMemcpyDeviceToHost, stream));
+            CUDA_TRY(cudaStreamSynchronize(stream));
+        }
+        for (uint32_t i = 0; i < n; ++i) {
+            st->task_events[i].t_arrive = tmp[i].t_arrive;
+            st->task_events[i].t_first_surrender = tmp[i].t_first_surrender;
+            st->task_events[i].t_last_surrender = tmp[i].t_last_surrender;
+            st->task_events[i].t_first_start = tmp[i].t_first_start;
+            st->task_events[i].t_end = tmp[i].t_end;
+            st->task_events[i].demanded = tmp[i].demanded;
+            st->task_events[i].surrendered = tmp[i].surrendered;
+        }
+    }
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    return COOP_OK;
+}
+
+static coop_status map_err(const Ctl &c) {
+    switch (c.err) {
+        case DERR_NONE: return COOP_OK;
+        case DERR_TIMEOUT: return fail(COOP_ERR_TIMEOUT, "in-kernel watchdog fired (episode %u)", c.episode);
+        case DERR_INVARIANT: return fail(COOP_ERR_INVARIANT, "barrier invariant violated (%u violations)", c.violations);
+        case DERR_OVERFLOW: return fail(COOP_ERR_OVERFLOW, "distance overflow");
+    }
+    return fail(COOP_ERR_INVARIANT, "unknown device error %u", c.err);
+}
+
+struct Prepared {
+    KParams kp;
+    void *kern;
+    uint32_t grid, threads;
+    cudaStream_t stream;
+    Scratch *s;
+    cudaEvent_t ev0, ev1;
+};
+
+static coop_status prepare(const RunReq &r, Prepared *pr) {
+    static const coop_opts kDefault = {};
+    const coop_opts &o = r.opts ? *r.opts : kDefault;
+    Scratch *s = nullptr;
+    coop_status st = get_scratch(&s);
+    if (st != COOP_OK) return st;
+    KParams kp;
+    memset(&kp, 0, sizeof kp);
+    kp.app = r.app;
+    const uint32_t threads = o.threads_per_wg ? o.threads_per_wg : (r.app == APP_BARRIER ? 128u : 512u);
+    int off64 = 0;
+    if (r.app != APP_BARRIER) {
+        const coop_csr *g = r.g;
+        if (!g) return fail(COOP_ERR_INVALID_ARG, "graph is NULL");
+        if (g->num_vertices < 1 || g->num_vertices > (int64_t)INT32_MAX)
+            return fail(COOP_ERR_INVALID_ARG, "num_vertices %lld out of range [1, 2^31-1]", (long long)g->num_vertices);
+        if (g->num_edges < 0) return fail(COOP_ERR_INVALID_ARG, "num_edges < 0");
+        if (g->offset_bits != 32 && g->offset_bits != 64) return fail(COOP_ERR_INVALID_ARG, "offset_bits must be 32 or 64");
+        if (g->offset_bits == 32 && g->num_edges > (int64_t)UINT32_MAX)
+            return fail(COOP_ERR_INVALID_ARG, "num_edges needs 64-bit offsets");
+        if (!g->row_offsets || (!g->col_idx && g->num_edges > 0))
+            return fail(COOP_ERR_INVALID_ARG, "row_offsets/col_idx NULL");
+        if (r.source < 0 || r.source >= g->num_vertices)
+            return fail(COOP_ERR_INVALID_ARG, "source %lld out of range [0, %lld)", (long long)r.source, (long long)g->num_vertices);
+        if (!r.out) return fail(COOP_ERR_INVALID_ARG, "output buffer is NULL");
+        if (r.app == APP_SSSP && !g->weights && g->num_edges > 0) return fail(COOP_ERR_INVALID_ARG, "SSSP needs weights");
+        off64 = g->offset_bits == 64;
+        kp.V = g->num_vertices;
+        kp.ro = g->row_offsets;
+        kp.off64 = off64;
+        kp.col = g->col_idx;
+        kp.w = g->weights;
+        kp.source = r.source;
+        if (r.app == APP_BFS) kp.level_out = static_cast<int32_t *>(r.out);
+        else kp.dist_out = static_cast<uint32_t *>(r.out);
+    }
+    void *kern = select_kernel(r.app, off64, threads);
+    if (!kern) return fail(COOP_ERR_INVALID_ARG, "threads_per_wg %u not supported", threads);
+    int sms = 0, per = 0;
+    st = occupancy(kern, threads, &sms, &per);
+    if (st != COOP_OK) return st;
+    const uint32_t cap = (uint32_t)(sms * per);
+    const bool plain = o.barrier_mode == COOP_BARRIER_PLAIN;
+    if (o.barrier_mode > COOP_BARRIER_NAIVE) return fail(COOP_ERR_INVALID_ARG, "bad barrier_mode %u", o.barrier_mode);
+    if (o.policy > COOP_POLICY_SCHEDULER) return fail(COOP_ERR_INVALID_ARG, "bad policy %u", o.policy);
+    const bool sched = !plain && (o.policy == COOP_POLICY_SCHEDULER);
+    uint32_t P = o.max_wgs ? o.max_wgs : cap - (sched ? 1 : 0);
+    if (P < 1 || P > kMaxCtas) return fail(COOP_ERR_INVALID_ARG, "max_wgs %u out of range [1, %u]", P, kMaxCtas);
+    if (P + (sched ? 1 : 0) > cap)
+        return fail(COOP_ERR_NOT_CORESIDENT, "%u workgroups%s exceed the co-resident capacity %u (%d SMs x %d)",
+                    P, sched ? " + scheduler" : "", cap, sms, per);
+    uint32_t M0 = o.init_wgs ? o.init_wgs : P;
+    if (M0 < 1 || M0 > P) return fail(COOP_ERR_INVALID_ARG, "init_wgs %u not in [1, %u]", M0, P);
+    if (plain) M0 = P;
+    const uint32_t bpl = o.barriers_per_level ? o.barriers_per_level : 1;
+    if (bpl != 1 && bpl != 2) return fail(COOP_ERR_INVALID_ARG, "barriers_per_level must be 1 or 2");
+    if (o.policy == COOP_POLICY_SCRIPTED && o.script_len && !o.script) return fail(COOP_ERR_INVALID_ARG, "script NULL");
+    if (o.resize_prob < 0 || o.resize_prob > 1) return fail(COOP_ERR_INVALID_ARG, "resize_prob not in [0,1]");
+    if (sched && (o.task_period_ns || r.host)) {
+        if (o.task_period_ns && (o.task_wgs < 1 || o.task_wgs > P - 1))
+            return fail(COOP_ERR_NO_CAPACITY, "task_wgs %u not in [1, N-1=%u] (WG 0 is never killed, P:543)", o.task_wgs, P - 1);
+    }
+    if (r.app == APP_SSSP) {
+        uint32_t wmax = r.g->max_weight;
+        if (!wmax && r.g->num_edges > 0) {
+            CUDA_TRY(s->wmax.ensure(4));
+            cudaStream_t st0 = static_cast<cudaStream_t>(o.stream);
+            CUDA_TRY(cudaMemsetAsync(s->wmax.p, 0, 4, st0));
+            max_u32_kernel<<<296, 256, 0, st0>>>(r.g->weights, r.g->num_edges, static_cast<uint32_t *>(s->wmax.p));
+            CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(cudaMemcpyAsync(&wmax, s->wmax.p, 4, cudaMemcpyDeviceToHost, st0));
+            CUDA_TRY(cudaStreamSynchronize(st0));
+        }
+        if ((uint64_t)(r.g->num_vertices - 1) * wmax >= 0xFFFFFFFFull)
+            return fail(COOP_ERR_OVERFLOW, "(V-1)*max_weight = %llu >= 2^32-1", (unsigned long long)(r.g->num_vertices - 1) * wmax);
+    }
+
+    // ---- scratch
+    const uint64_t V = r.app == APP_BARRIER ? 0 : (uint64_t)kp.V;
+    const uint64_t E = r.app == APP_BARRIER ? 0 : (uint64_t)r.g->num_edges;
+    CUDA_TRY(s->ctl.ensure(sizeof(Ctl)));
+    CUDA_TRY(s->mb.ensure(sizeof(Mailbox) * P));
+    CUDA_TRY(s->stamp.ensure(4ull * kMaxCtas));
+    const uint32_t mcap = 1u << 16, lcap = 1u << 16, ecap = 4096;
+    CUDA_TRY(s->mtrace.ensure(4ull * mcap));
+    CUDA_TRY(s->lsizes.ensure(4ull * lcap));
+    CUDA_TRY(s->events.ensure(sizeof(TaskEventDev) * ecap));
+    if (r.app == APP_BFS) {
+        const size_t le = off64 ? sizeof(LightEntry64) : sizeof(LightEntry);
+        CUDA_TRY(s->visited.ensure(4 * ((V + 31) / 32)));
+        CUDA_TRY(s->ql0.ensure(le * V));
+        CUDA_TRY(s->ql1.ensure(le * V));
+        const size_t nh = E / kHeavyDeg + 1;
+        CUDA_TRY(s->qh0.ensure(sizeof(HeavyEntry) * nh));
+        CUDA_TRY(s->qh1.ensure(sizeof(HeavyEntry) * nh));
+        kp.visited = static_cast<uint32_t *>(s->visited.p);
+        kp.qheavy[0] = static_cast<HeavyEntry *>(s->qh0.p);
+        kp.qheavy[1] = static_cast<HeavyEntry *>(s->qh1.p);
+    } else if (r.app == APP_SSSP) {
+        CUDA_TRY(s->qlev.ensure(4 * V));
+        CUDA_TRY(s->ql0.ensure(4 * V));
+        CUDA_TRY(s->ql1.ensure(4 * V));
+        kp.qlev = static_cast<uint32_t *>(s->qlev.p);
+    }
+    kp.qlight[0] = s->ql0.p;
+    kp.qlight[1] = s->ql1.p;
+    kp.ctl = static_cast<Ctl *>(s->ctl.p);
+    kp.mb = static_cast<Mailbox *>(s->mb.p);
+    kp.stamp = static_cast<uint32_t *>(s->stamp.p);
+    kp.m_trace = static_cast<uint32_t *>(s->mtrace.p);
+    kp.m_trace_cap = mcap;
+    kp.level_sizes = static_cast<uint32_t *>(s->lsizes.p);
+    kp.level_cap = lcap;
+    kp.events = static_cast<TaskEventDev *>(s->events.p);
+    kp.events_cap = ecap;
+    cudaStream_t stream = static_cast<cudaStream_t>(o.stream);
+    if (o.policy == COOP_POLICY_SCRIPTED && o.script_len) {
+        CUDA_TRY(s->script.ensure(4ull * o.script_len));
+        CUDA_TRY(cudaMemcpyAsync(s->script.p, o.script, 4ull * o.script_len, cudaMemcpyHostToDevice, stream));
+        kp.script = static_cast<const uint32_t *>(s->script.p);
+        kp.script_len = o.script_len;
+    }
+    kp.host = r.host;
+    kp.P = P;
+    kp.M0 = M0;
+    kp.policy = plain ? COOP_POLICY_NEVER : o.policy;
+    kp.barrier_mode = o.barrier_mode;
+    kp.bpl = bpl;
+    kp.flags = o.flags;
+    kp.has_sched = sched ? 1 : 0;
+    kp.seed = o.seed;
+    kp.resize_thresh = (uint32_t)std::min(4294967295.0, o.resize_prob * 4294967296.0);
+    kp.timeout_ns = o.timeout_ns ? o.timeout_ns : 20000000000ull;
+    kp.iters = r.iters;
+    kp.task_wgs = o.task_wgs;
+    kp.task_blocks = o.task_blocks ? o.task_blocks : 1;
+    kp.task_max = o.task_max;
+    kp.task_block_ns = o.task_block_ns;
+    kp.task_period_ns = sched ? o.task_period_ns : 0;
+    kp.task_first_ns = o.task_first_ns;
+
+    // ---- control block
+    Ctl *h = s->host_ctl;
+    memset(h, 0, sizeof(Ctl));
+    h->W = pack_w(0, M0, 0);
+    h->mhist[0] = M0;
+    h->min_m = M0;
+    h->max_m = M0;
+    h->task_next = 0xFFFFFFFFu;
+    for (uint32_t b = M0; b < P; ++b) h->pool[b >> 5] |= 1u << (b & 31);
+    CUDA_TRY(cudaMemcpyAsync(kp.ctl, h, sizeof(Ctl), cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemsetAsync(kp.mb, 0, sizeof(Mailbox) * P, stream));
+    if (sched) CUDA_TRY(cudaMemsetAsync(kp.events, 0, sizeof(TaskEventDev) * ecap, stream));
+    pr->kp = kp;
+    pr->kern = kern;
+    pr->grid = P + (sched ? 1 : 0);
+    pr->threads = threads;
+    pr->stream = stream;
+    pr->s = s;
+    pr->ev0 = static_cast<cudaEvent_t>(o.ev_kernel_start);
+    pr->ev1 = static_cast<cudaEvent_t>(o.ev_kernel_end);
+    return COOP_OK;
+}
+
+static coop_status launch(Prepared &pr) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(pr.grid);
+    cfg.blockDim = dim3(pr.threads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = pr.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;   // co-residency guarantee only; no grid.sync anywhere
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void *args[] = {&pr.kp};
+    if (pr.ev0) CUDA_TRY(cudaEventRecord(pr.ev0, pr.stream));
+    CUDA_TRY(cudaLaunchKernelExC(&cfg, pr.kern, args));
+    if (pr.ev1) CUDA_TRY(cudaEventRecord(pr.ev1, pr.stream));
+    return COOP_OK;
+}
+
+static coop_status finish(Prepared &pr, coop_stats *stats) {
+    Ctl *h = pr.s->host_ctl;
+    CUDA_TRY(cudaMemcpyAsync(h, pr.kp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.stream));
+    CUDA_TRY(cudaStreamSynchronize(pr.stream));
+    coop_status st = map_err(*h);
+    Ctl copy = *h;
+    if (stats) {
+        stats->threads_per_wg = pr.threads;
+        coop_status s2 = fill_stats(copy, pr.kp, stats, pr.stream);
+        if (st == COOP_OK) st = s2;
+    }
+    return st;
+}
+
+// The per-device scratch belongs to one call at a time; never block on it (a
+// handle that was launched but not waited owns it until coop_wait/destroy).
+#define SCRATCH_LOCK(s)                                                                           \
+    std::unique_lock<std::mutex> lk((s)->mu, std::try_to_lock);                                   \
+    if (!lk.owns_lock())                                                                          \
+        return fail(COOP_ERR_BUSY, "device scratch in use by another call or an un-waited handle")
+
+static coop_status run_blocking(const RunReq &r) {
+    Prepared pr;
+    Scratch *s = nullptr;
+    coop_status st = get_scratch(&s);
+    if (st != COOP_OK) return st;
+    SCRATCH_LOCK(s);
+    st = prepare(r, &pr);
+    if (st != COOP_OK) return st;
+    st = launch(pr);
+    if (st != COOP_OK) return st;
+    return finish(pr, r.stats);
+}
+
+extern "C" coop_status coop_bfs(const coop_csr *g, int64_t source, int32_t *levels_out, const coop_opts *opts,
+                                coop_stats *stats) {
+    RunReq r = {APP_BFS, g, source, levels_out, opts, stats, 0, nullptr, false};
+    return run_blocking(r);
+}
+
+extern "C" coop_status coop_sssp(const coop_csr *g, int64_t source, uint32_t *dist_out, const coop_opts *opts,
+                                 coop_stats *stats) {
+    RunReq r = {APP_SSSP, g, source, dist_out, opts, stats, 0, nullptr, false};
+    return run_blocking(r);
+}
+
+// ------------------------------------------------------------------ end-to-end (host pointers)
+static coop_status run_host(uint32_t app, int64_t V, const void *ro, int32_t offset_bits, const int32_t *col,
+                            const uint32_t *w, uint32_t max_weight, int64_t source, void *out,
+                            const coop_opts *opts, coop_stats *stats) {
+    if (V < 1 || !ro || !out) return fail(COOP_ERR_INVALID_ARG, "bad host arguments");
+    if (offset_bits != 32 && offset_bits != 64) return fail(COOP_ERR_INVALID_ARG, "offset_bits must be 32 or 64");
+    Scratch *s = nullptr;
+    coop_status st = get_scratch(&s);
+    if (st != COOP_OK) return st;
+    const size_t ob = offset_bits / 8;
+    uint64_t E = 0;
+    if (offset_bits == 32) E = static_cast<const uint32_t *>(ro)[V];
+    else E = (uint64_t) static_cast<const int64_t *>(ro)[V];
+    if (E && !col) return fail(COOP_ERR_INVALID_ARG, "col_idx NULL");
+    if (app == APP_SSSP && E && !w) return fail(COOP_ERR_INVALID_ARG, "SSSP needs weights");
+    cudaStream_t stream = opts ? static_cast<cudaStream_t>(opts->stream) : nullptr;
+    {
+        SCRATCH_LOCK(s);
+        CUDA_TRY(s->h_ro.ensure(ob * (V + 1)));
+        CUDA_TRY(s->h_col.ensure(4 * std::max<uint64_t>(E, 1)));
+        if (app == APP_SSSP) CUDA_TRY(s->h_w.ensure(4 * std::max<uint64_t>(E, 1)));
+        CUDA_TRY(s->h_out.ensure(4 * V));
+        CUDA_TRY(cudaMemcpyAsync(s->h_ro.p, ro, ob * (V + 1), cudaMemcpyHostToDevice, stream));
+        if (E) CUDA_TRY(cudaMemcpyAsync(s->h_col.p, col, 4 * E, cudaMemcpyHostToDevice, stream));
+        if (app == APP_SSSP && E) CUDA_TRY(cudaMemcpyAsync(s->h_w.p, w, 4 * E, cudaMemcpyHostToDevice, stream));
+    }
+    coop_csr g = {V, (int64_t)E, s->h_ro.p, offset_bits, static_cast<const int32_t *>(s->h_col.p),
+                  app == APP_SSSP ? static_cast<const uint32_t *>(s->h_w.p) : nullptr, max_weight};
+    RunReq r = {app, &g, source, s->h_out.p, opts, stats, 0, nullptr, false};
+    st = run_blocking(r);
+    if (st != COOP_OK) return st;
+    CUDA_TRY(cudaMemcpyAsync(out, s->h_out.p, 4 * V, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    return COOP_OK;
+}
+
+extern "C" coop_status coop_bfs_host(int64_t num_vertices, const void *row_offsets, int32_t offset_bits,
+                                     const int32_t *col_idx, int64_t source, int32_t *levels_out,
+                                     const coop_opts *opts, coop_stats *stats) {
+    return run_host(APP_BFS, num_vertices, row_offsets, offset_bits, col_idx, nullptr, 0, source, levels_out,
+                    opts, stats);
+}
+
+extern "C" coop_status coop_sssp_host(int64_t num_vertices, const void *row_offsets, int32_t offset_bits,
+                                      const int32_t *col_idx, const uint32_t *weights, uint32_t max_weight,
+                                      int64_t source, uint32_t *dist_out, const coop_opts *opts, coop_stats *stats) {
+    return run_host(APP_SSSP, num_vertices, row_offsets, offset_bits, col_idx, weights, max_weight, source,
+                    dist_out, opts, stats);
+}
+
+// ------------------------------------------------------------------ microbenchmarks
+extern "C" coop_status coop_barrier_bench(uint32_t n_ctas, uint32_t threads, uint64_t iters, double resize_prob,
+                                          uint64_t seed, uint32_t barrier_mode, uint32_t flags,
+                                          coop_barrier_stats *out) {
+    if (!out) return fail(COOP_ERR_INVALID_ARG, "out is NULL");
+    if (iters == 0) return fail(COOP_ERR_INVALID_ARG, "iters must be > 0");
+    if (barrier_mode != COOP_BARRIER_QUERY && barrier_mode != COOP_BARRIER_PLAIN)
+        return fail(COOP_ERR_INVALID_ARG, "barrier_mode must be QUERY or PLAIN");
+    coop_opts o = {};
+    o.max_wgs = n_ctas;
+    o.threads_per_wg = threads ? threads : 128;
+    o.barrier_mode = barrier_mode;
+    o.policy = (resize_prob > 0 && barrier_mode == COOP_BARRIER_QUERY) ? COOP_POLICY_RANDOM : COOP_POLICY_NEVER;
+    o.resize_prob = resize_prob;
+    o.seed = seed;
+    o.flags = flags;
+    o.timeout_ns = 60000000000ull;
+    coop_stats st = {};
+    Scratch *s = nullptr;
+    coop_status rc = get_scratch(&s);
+    if (rc != COOP_OK) return rc;
+    SCRATCH_LOCK(s);
+    RunReq r = {APP_BARRIER, nullptr, 0, nullptr, &o, &st, iters, nullptr, false};
+    Prepared pr;
+    rc = prepare(r, &pr);
+    if (rc != COOP_OK) return rc;
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    CUDA_TRY(cudaEventRecord(e0, pr.stream));
+    rc = launch(pr);
+    CUDA_TRY(cudaEventRecord(e1, pr.stream));
+    if (rc != COOP_OK) return rc;
+    rc = finish(pr, &st);
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    out->iters = iters;
+    out->ns_per_barrier = ms * 1e6 / (double)iters;
+    out->kernel_ns = st.kernel_ns;
+    out->kills = st.kills;
+    out->forks = st.forks;
+    out->violations = pr.s->host_ctl->violations;
+    return rc;
+}
+
+extern "C" coop_status coop_l2_atomic_rtt(uint64_t iters, double *ns_per_atomic) {
+    if (!ns_per_atomic || iters == 0) return fail(COOP_ERR_INVALID_ARG, "bad arguments");
+    unsigned long long *d = nullptr;
+    CUDA_TRY(cudaMalloc(&d, 4 * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemset(d, 0, 4 * sizeof(unsigned long long)));
+    l2_rtt_kernel<<<1, 1>>>(d, iters, d + 2);
+    CUDA_TRY(cudaGetLastError());
+    unsigned long long h[2];
+    CUDA_TRY(cudaMemcpy(h, d + 2, sizeof h, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    *ns_per_atomic = (double)h[0] / (double)iters;
+    return COOP_OK;
+}
+
+// ------------------------------------------------------------------ handle API
+struct coop_handle {
+    Prepared pr;
+    HostChannel *hc = nullptr;      // host view (mapped pinned)
+    HostChannel *dc = nullptr;      // device view
+    uint32_t seq = 0;
+    bool waited = false;
+    uint64_t next_task_id = 0;
+};
+
+extern "C" coop_status coop_launch(int kind, const coop_csr *g, int64_t source, void *out, const coop_opts *opts,
+                                   coop_handle **handle) {
+    if (!handle || !opts) return fail(COOP_ERR_INVALID_ARG, "handle/opts NULL");
+    if (kind != 0 && kind != 1) return fail(COOP_ERR_INVALID_ARG, "kind must be 0 (BFS) or 1 (SSSP)");
+    if (opts->policy != COOP_POLICY_SCHEDULER || opts->barrier_mode == COOP_BARRIER_PLAIN)
+        return fail(COOP_ERR_INVALID_ARG, "coop_launch needs policy SCHEDULER and a cooperative barrier");
+    coop_handle *h = new (std::nothrow) coop_handle();
+    if (!h) return fail(COOP_ERR_INVALID_ARG, "out of host memory");
+    cudaError_t e = cudaHostAlloc((void **)&h->hc, sizeof(HostChannel), cudaHostAllocMapped);
+    if (e != cudaSuccess) { delete h; return fail(COOP_ERR_CUDA, "cudaHostAlloc: %s", cudaGetErrorString(e)); }
+    memset((void *)h->hc, 0, sizeof(HostChannel));
+    e = cudaHostGetDevicePointer((void **)&h->dc, h->hc, 0);
+    if (e != cudaSuccess) { cudaFreeHost(h->hc); delete h; return fail(COOP_ERR_CUDA, "cudaHostGetDevicePointer"); }
+    RunReq r = {kind == 0 ? APP_BFS : APP_SSSP, g, source, out, opts, nullptr, 0, h->dc, true};
+    Scratch *s = nullptr;
+    coop_status st = get_scratch(&s);
+    if (st == COOP_OK) {
+        if (!s->mu.try_lock()) {   // held until coop_wait/destroy: the scratch belongs to this launch
+            st = fail(COOP_ERR_BUSY, "device scratch in use by another call or an un-waited handle");
+            cudaFreeHost(h->hc);
+            delete h;
+            return st;
+        }
+        st = prepare(r, &h->pr);
+        if (st == COOP_OK) st = launch(h->pr);
+        if (st != COOP_OK) s->mu.unlock();
+    }
+    if (st != COOP_OK) { cudaFreeHost(h->hc); delete h; return st; }
+    *handle = h;
+    return COOP_OK;
+}
+
+static coop_status post(coop_handle *h, uint32_t kind, uint32_t a, uint32_t b, uint64_t c) {
+    if (h->waited) return fail(COOP_ERR_BUSY, "handle already waited");
+    // single-slot channel: wait until the scheduler CTA consumed the previous packet
+    for (long spins = 0; h->hc->ack != h->seq; ++spins) {
+        if (h->hc->done_mirror) return fail(COOP_ERR_BUSY, "kernel already terminated");
+        if (spins > 200000000L) return fail(COOP_ERR_TIMEOUT, "scheduler CTA did not consume the packet");
+    }
+    h->hc->kind = kind;
+    h->hc->a = a;
+    h->hc->b = b;
+    h->hc->c = c;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    h->hc->seq = ++h->seq;
+    return COOP_OK;
+}
+
+extern "C" coop_status coop_submit_task(coop_handle *h, uint32_t task_wgs, uint32_t task_blocks,
+                                        uint64_t task_block_ns, uint64_t *task_id) {
+    if (!h) return fail(COOP_ERR_INVALID_ARG, "handle NULL");
+    if (task_wgs < 1 || task_wgs > h->pr.kp.P - 1)
+        return fail(COOP_ERR_NO_CAPACITY, "task_wgs %u not in [1, N-1=%u]", task_wgs, h->pr.kp.P - 1);
+    coop_status st = post(h, 1, task_wgs, task_blocks ? task_blocks : 1, task_block_ns);
+    if (st == COOP_OK && task_id) *task_id = h->next_task_id;
+    if (st == COOP_OK) h->next_task_id++;
+    return st;
+}
+
+extern "C" coop_status coop_demand(coop_handle *h, uint32_t kills) {
+    if (!h) return fail(COOP_ERR_INVALID_ARG, "handle NULL");
+    if (kills > h->pr.kp.P - 1) return fail(COOP_ERR_NO_CAPACITY, "demand %u > N-1", kills);
+    return post(h, 2, kills, 0, 0);
+}
+
+extern "C" coop_status coop_grant(coop_handle *h, uint32_t forks) {
+    if (!h) return fail(COOP_ERR_INVALID_ARG, "handle NULL");
+    if (forks > h->pr.kp.P) return fail(COOP_ERR_FORK_BOUND, "grant %u > N=%u (k <= N-M, P:565)", forks, h->pr.kp.P);
+    return post(h, 3, forks, 0, 0);
+}
+
+extern "C" coop_status coop_query(coop_handle *h, uint32_t *W) {
+    if (!h || !W) return fail(COOP_ERR_INVALID_ARG, "NULL argument");
+    *W = h->hc->demand_mirror;
+    return COOP_OK;
+}
+
+extern "C" coop_status coop_current_m(coop_handle *h, uint32_t *M) {
+    if (!h || !M) return fail(COOP_ERR_INVALID_ARG, "NULL argument");
+    *M = h->hc->cur_m;
+    return COOP_OK;
+}
+
+extern "C" coop_status coop_wait(coop_handle *h, coop_stats *stats) {
+    if (!h) return fail(COOP_ERR_INVALID_ARG, "handle NULL");
+    if (h->waited) return fail(COOP_ERR_BUSY, "already waited");
+    h->waited = true;
+    coop_status st = finish(h->pr, stats);
+    h->pr.s->mu.unlock();
+    return st;
+}
+
+extern "C" void coop_destroy(coop_handle *h) {
+    if (!h) return;
+    if (!h->waited) {
+        cudaStreamSynchronize(h->pr.stream);
+        h->pr.s->mu.unlock();
+    }
+    cudaFreeHost(h->hc);
+    delete h;
+}

@@ -1,0 +1,151 @@
+// coop_internal.h -- layouts shared by the host side (coop_api.cu) and the
+// device runtime (coop_rt.cuh).  Not part of the public ABI.
+#pragma once
+#include <stdint.h>
+
+namespace coop {
+
+constexpr uint32_t kMaxCtas = 4096;                  // physical CTA slots (pool bitmap size)
+constexpr uint32_t kPoolWords = kMaxCtas / 32;
+constexpr uint32_t kHeavyDeg = 256;                  // BFS: frontier entries with deg >= this are edge-balanced
+constexpr uint64_t kMask40 = (1ull << 40) - 1;
+
+// runtime actions broadcast inside a CTA
+enum : uint32_t { ACT_CONT = 0, ACT_KILLED = 1, ACT_DONE = 2, ACT_ABORT = 3, ACT_RUN_BODY = 4,
+                  ACT_RUN_TASK = 5, ACT_EXIT = 6, ACT_IDLE = 7 };
+// body entry points (the paper's "designated point within the kernel")
+enum : uint32_t { ENTRY_START = 0, ENTRY_AFTER_RB1 = 1, ENTRY_AFTER_RB2 = 2 };
+// error codes written to Ctl::err (host maps to coop_status)
+enum : uint32_t { DERR_NONE = 0, DERR_TIMEOUT = 1, DERR_INVARIANT = 2, DERR_OVERFLOW = 3 };
+enum : uint32_t { APP_BFS = 0, APP_SSSP = 1, APP_BARRIER = 2 };
+
+// Transmit struct: the transmit-annotated state of Fig. 4 (level, in_nodes,
+// out_nodes) plus what a forked CTA needs to join (reading R7).
+struct Transmit {
+    uint32_t level;
+    uint32_t in_sel;
+    uint32_t gen;      // barrier generation the forked CTA joins
+    uint32_t M;        // active count after the episode
+    uint32_t lid;      // logical id assigned to the forked CTA
+    uint32_t entry;    // ENTRY_AFTER_RB1 / ENTRY_AFTER_RB2
+    uint32_t pad[2];
+};
+
+struct __align__(64) Mailbox {
+    uint32_t flag;     // generation of the last assignment (0 = never)
+    uint32_t pad0[7];
+    Transmit tx;
+};
+
+struct LightEntry { uint32_t beg; uint32_t deg; };                 // BFS frontier entry, 32-bit offsets
+struct LightEntry64 { uint64_t beg; uint32_t deg; uint32_t pad; };  // 64-bit offsets
+struct HeavyEntry { uint64_t beg; uint64_t prefix; uint32_t deg; uint32_t pad; };
+
+struct TaskEventDev {
+    unsigned long long t_arrive, t_first_surrender, t_last_surrender, t_first_start, t_end;
+    uint32_t demanded, surrendered;
+};
+
+// Control block in device memory.  Hot words sit on their own 128-B lines.
+struct __align__(128) Ctl {
+    unsigned long long W;              // barrier word {gen:32 | M:16 | arrived:16}
+    unsigned long long pad_w[15];
+    // line: scheduler channel (resource messages)
+    uint32_t demand;                   // WGs the scheduler wants back (query() = min(demand, M-1))
+    uint32_t grant;                    // WGs the scheduler offers at the next fork point
+    uint32_t pad_c[30];
+    // line: frontier counters
+    uint32_t qsize[2];                 // light queue sizes (in/out selected by the transmitted in_sel)
+    unsigned long long heavy[2];       // packed {count:24 | edges:40}
+    uint32_t pad_q[26];
+    // line: status
+    uint32_t done;                     // set by WG 0 at termination (parked CTAs and scheduler exit)
+    uint32_t err;                      // DERR_*
+    uint32_t episode;                  // resizing episodes executed
+    uint32_t cur_task;                 // index of the task instance in flight (+1), 0 = none
+    uint32_t pad_s[28];
+    // line: transmit published by WG 0 before each arrival
+    Transmit tx0;
+    uint32_t pad_t[24];
+    // task (competing non-cooperative kernel, megakernel worker pool P:817-826)
+    uint32_t task_next;                // next block to claim
+    uint32_t task_total;               // blocks of the instance in flight
+    uint32_t task_done;                // blocks finished
+    uint32_t task_wgs;                 // Q of the instance in flight
+    unsigned long long task_block_ns;
+    uint32_t pad_k[26];
+    // stats (atomics at CTA exit / in serial sections)
+    unsigned long long edges_scanned, frontier_total, reached, t_start, t_end;
+    uint32_t kills, forks, levels, min_m, max_m, tasks_posted, tasks_completed, n_events;
+    // invariant checks (COOP_FLAG_CHECK)
+    uint32_t chk_arr[2];
+    uint32_t violations;
+    uint32_t mhist[8];                 // M' of generation g (index g & 7), written before the release of W
+    uint32_t pad_x[5];
+    uint32_t idmap[2][kPoolWords];
+    // idle-and-forkable physical CTAs (the scheduler context's "available" set)
+    uint32_t pool[kPoolWords];
+    // host-mapped channel mirror: last host sequence numbers consumed
+    uint32_t host_seq_seen;
+    uint32_t pad_h[31];
+};
+
+// Host -> GPU packet channel (host-mapped pinned memory; the paper's SVM atomics).
+struct HostChannel {
+    volatile uint32_t seq;             // incremented by the host for every packet
+    volatile uint32_t kind;            // 1 = task, 2 = demand, 3 = grant
+    volatile uint32_t a, b;            // task: wgs, blocks; demand/grant: count
+    volatile unsigned long long c;     // task: block ns
+    volatile uint32_t ack;             // scheduler CTA: last seq consumed
+    volatile uint32_t cur_m;           // scheduler CTA mirrors W.M for coop_current_m
+    volatile uint32_t demand_mirror;
+    volatile uint32_t done_mirror;
+};
+
+struct KParams {
+    // graph (immutable kernel parameters)
+    int64_t V;
+    const void *ro;
+    int off64;
+    const int32_t *col;
+    const uint32_t *w;
+    int64_t source;
+    // outputs
+    int32_t *level_out;
+    uint32_t *dist_out;
+    // scratch
+    Ctl *ctl;
+    Mailbox *mb;
+    uint32_t *visited;          // BFS bitmap [ceil(V/32)]
+    uint32_t *qlev;             // SSSP dedupe [V]
+    void *qlight[2];            // BFS light entries / SSSP vertex ids
+    HeavyEntry *qheavy[2];
+    uint32_t *stamp;            // barrier bench message passing [kMaxCtas]
+    uint32_t *m_trace; uint32_t m_trace_cap;
+    uint32_t *level_sizes; uint32_t level_cap;
+    TaskEventDev *events; uint32_t events_cap;
+    const uint32_t *script; uint32_t script_len;
+    HostChannel *host;          // host-mapped channel or nullptr
+    // configuration
+    uint32_t app;
+    uint32_t P;                 // physical worker CTAs (N)
+    uint32_t M0;
+    uint32_t policy;
+    uint32_t barrier_mode;
+    uint32_t bpl;               // barriers per level (1 or 2)
+    uint32_t flags;
+    uint32_t has_sched;         // 1: CTA P is the scheduler CTA
+    uint64_t seed;
+    uint32_t resize_thresh;     // resize_prob * 2^32
+    uint64_t timeout_ns;
+    uint64_t iters;             // barrier bench
+    // periodic task generator
+    uint32_t task_wgs, task_blocks, task_max;
+    uint64_t task_block_ns, task_period_ns, task_first_ns;
+};
+
+__host__ __device__ inline unsigned long long pack_w(uint32_t gen, uint32_t M, uint32_t arrived) {
+    return ((unsigned long long)gen << 32) | ((unsigned long long)(M & 0xFFFF) << 16) | (arrived & 0xFFFF);
+}
+
+}  // namespace coop

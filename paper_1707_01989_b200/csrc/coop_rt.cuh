@@ -1,0 +1,629 @@
+// coop_rt.cuh -- device runtime of the cooperative-kernel model on sm_100a.
+//
+// One persistent launch = the paper's megakernel: P worker
+// CTAs (the N workgroups) + optionally one scheduler CTA.  A
+// worker is either ACTIVE in the cooperative body with a logical id in
+// [0, M) or PARKED in the worker loop, where it runs blocks of the competing
+// non-cooperative task and waits to be forked.
+//
+// Resizing global barrier = one episode on a packed word
+//   W = {gen:32 | M:16 | arrived:16}      (modelled in oracle/barrier_model.py)
+//   arrive : thread 0: fence; old = atomicAdd(W, 1); last iff old.arrived+1 == old.M
+//   serial : warp 0 of the last arriver, while all M CTAs wait: query the
+//            scheduler (W_q = min(demand, M-1)), pick M', fork new
+//            ids [M, M') onto idle parked CTAs (mailbox + transmit of WG 0,
+//            P:892-903), run the app's serial work (Fig. 4 reset(out)),
+//            record M' in mhist[gen+1], then release W := {gen+1, M', 0}.
+//   waiters: spin until W.gen != gen; killed iff W.gen != gen+1 or id >= M'
+//            (ids >= M' leave: the query barrier's "ids >= M-W").
+// NAIVE mode: on entry the top WG (id M-1 > 0) offers kill; if the
+// scheduler has demand it leaves by CAS W {g,M,a} -> {g,M-1,a}.
+#pragma once
+#include <stdint.h>
+#include "coop_internal.h"
+#include "../../include/coop.h"
+
+namespace coop {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release32(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed32(uint32_t *p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_sys32(const volatile uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ uint32_t w_gen(unsigned long long w) { return (uint32_t)(w >> 32); }
+__device__ __forceinline__ uint32_t w_M(unsigned long long w) { return (uint32_t)(w >> 16) & 0xFFFF; }
+__device__ __forceinline__ uint32_t w_arr(unsigned long long w) { return (uint32_t)w & 0xFFFF; }
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+        uint32_t n = __shfl_up_sync(FULL, v, s);
+        if (lane >= (uint32_t)s) v += n;
+    }
+    return v;
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finaliser (counter RNG)
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+// lowest `n` set bits of `w`
+__device__ __forceinline__ uint32_t lowest_bits(uint32_t w, uint32_t n) {
+    uint32_t m = 0;
+    for (uint32_t i = 0; i < n && w; ++i) {
+        uint32_t b = w & (0u - w);
+        m |= b;
+        w ^= b;
+    }
+    return m;
+}
+
+// ---------------------------------------------------------------- CTA state
+struct CtaState {
+    uint32_t lid, M, gen, level, in_sel;
+    uint32_t action, last, entry, block, consumed;
+    uint64_t deadline;
+    unsigned long long edges, frontier, reached;   // per-CTA stats, flushed at body exit
+    uint32_t bar_M, bar_naive;                     // barrier: M of the episode, killed on entry (NAIVE)
+    uint32_t app_u32[8];                           // app broadcast scratch
+};
+
+__device__ __forceinline__ bool set_abort(const KParams &p, uint32_t code) {
+    atomicCAS(&p.ctl->err, DERR_NONE, code);
+    st_release32(&p.ctl->done, 1);
+    return true;
+}
+// watchdog for spin loops (thread-level); true => abort
+__device__ __forceinline__ bool spin_check(const KParams &p, const CtaState &cs, uint32_t &spins) {
+    if ((++spins & 127u) != 0) return false;
+    if (ld_relaxed32(&p.ctl->err) != DERR_NONE) return true;
+    if (globaltimer() > cs.deadline) return set_abort(p, DERR_TIMEOUT);
+    return false;
+}
+
+__device__ __forceinline__ uint32_t mhist_get(const KParams &p, uint32_t gen);
+
+// ---------------------------------------------------------------- forks
+// Warp-collective: claim up to k idle parked CTAs from the pool and assign
+// them logical ids M, M+1, ... with the transmit state of WG 0.
+// With `wait`, keeps trying until k are found (killed CTAs park promptly).
+__device__ uint32_t fork_from_pool(const KParams &p, const CtaState &cs, uint32_t gnext, uint32_t M,
+                                   uint32_t k, uint32_t entry, const Transmit &tx0, bool wait) {
+    const uint32_t lane = threadIdx.x & 31;
+    Ctl *c = p.ctl;
+    const uint32_t nwords = (p.P + 31) / 32;
+    uint32_t got = 0, spins = 0;
+    while (got < k) {
+        for (uint32_t w0 = 0; w0 < nwords && got < k; w0 += 32) {
+            const uint32_t wi = w0 + lane;
+            uint32_t word = wi < nwords ? ld_relaxed32(&c->pool[wi]) : 0u;
+            uint32_t cnt = __popc(word);
+            uint32_t incl = warp_incl_scan(cnt), excl = incl - cnt;
+            uint32_t need = k - got;
+            uint32_t want = need > excl ? min(cnt, need - excl) : 0u;
+            uint32_t mask = lowest_bits(word, want);
+            uint32_t claimed = mask ? (atomicAnd(&c->pool[wi], ~mask) & mask) : 0u;
+            uint32_t nc = __popc(claimed);
+            uint32_t cincl = warp_incl_scan(nc), cexcl = cincl - nc;
+            uint32_t ctot = __shfl_sync(FULL, cincl, 31);
+            uint32_t r = 0;
+            while (claimed) {
+                uint32_t b = __ffs(claimed) - 1;
+                claimed &= claimed - 1;
+                uint32_t phys = wi * 32 + b;
+                Mailbox *mb = p.mb + phys;
+                Transmit t = tx0;
+                t.gen = gnext;
+                t.lid = M + got + cexcl + r++;
+                t.entry = entry;
+                mb->tx = t;
+                __threadfence();
+                st_release32(&mb->flag, gnext);
+            }
+            got += ctot;
+        }
+        if (!wait || got >= k) break;
+        uint32_t abort = 0;
+        if (lane == 0) abort = spin_check(p, cs, spins) ? 1u : 0u;
+        if (__shfl_sync(FULL, abort, 0)) break;
+        __nanosleep(256);
+    }
+    return got;
+}
+
+// ---------------------------------------------------------------- barrier
+template <class App>
+__device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_t g, uint32_t M,
+                               bool resizing, uint32_t entry, uint32_t *out_mp) {
+    const uint32_t lane = threadIdx.x & 31;
+    Ctl *c = p.ctl;
+    uint32_t Mp = M, ep = 0, take = 0;
+    bool sched_fork = false, wait_fork = false;
+    if (lane == 0) {
+        ep = c->episode;
+        if (resizing && p.barrier_mode != COOP_BARRIER_PLAIN) {
+            if (p.policy == COOP_POLICY_SCRIPTED) {
+                uint32_t s = ep < p.script_len ? p.script[ep] : 0u;
+                if (s) Mp = s;
+                wait_fork = true;
+            } else if (p.policy == COOP_POLICY_RANDOM) {
+                uint64_t h = mix64(p.seed * 0x2545F4914F6CDD1Dull + ep);
+                if ((uint32_t)h < p.resize_thresh) Mp = 1 + (uint32_t)((h >> 32) % p.P);
+                wait_fork = true;
+            } else if (p.policy == COOP_POLICY_SCHEDULER) {
+                if (p.barrier_mode == COOP_BARRIER_QUERY) {
+                    // query(): W = demand, satisfied up to M-1 in this episode (reading R5)
+                    uint32_t d = ld_relaxed32(&c->demand);
+                    while (d > 0 && M > 1) {
+                        uint32_t t = min(d, M - 1);
+                        uint32_t old = atomicCAS(&c->demand, d, d - t);
+                        if (old == d) { take = t; break; }
+                        d = old;
+                    }
+                }
+                if (take > 0) {
+                    Mp = M - take;
+                } else {
+                    uint32_t gr = ld_relaxed32(&c->grant);
+                    if (gr > 0 && M < p.P) { Mp = M + min(gr, p.P - M); sched_fork = true; }
+                }
+            }
+            Mp = max(1u, min(Mp, p.P));
+        }
+    }
+    Mp = __shfl_sync(FULL, Mp, 0);
+    wait_fork = __shfl_sync(FULL, (uint32_t)wait_fork, 0) != 0;
+    uint32_t got = 0;
+    if (Mp > M) {
+        Transmit tx0 = c->tx0;   // WG 0's transmit state published at its arrival
+        got = fork_from_pool(p, cs, g + 1, M, Mp - M, entry, tx0, wait_fork);
+        Mp = M + got;
+    }
+    if (lane == 0) {
+        const uint64_t now = globaltimer();
+        if (sched_fork && got) atomicSub(&c->grant, got);
+        if (take > 0) {   // gather bookkeeping of the task instance in flight
+            uint32_t cur = c->cur_task;
+            if (cur && cur - 1 < p.events_cap) {
+                TaskEventDev *e = p.events + (cur - 1);
+                const uint32_t before = atomicAdd(&e->surrendered, take);
+                if (before == 0) e->t_first_surrender = now;
+                if (before + take >= e->demanded) e->t_last_surrender = now;
+            }
+        }
+        app.serial(p, cs, entry, resizing);
+        if (resizing) {
+            if (ep < p.m_trace_cap) p.m_trace[ep] = Mp;
+            c->episode = ep + 1;
+        }
+        if (Mp < M) atomicAdd(&c->kills, M - Mp);
+        c->forks += got;
+        c->min_m = min(c->min_m, Mp);
+        c->max_m = max(c->max_m, Mp);
+        if (p.flags & COOP_FLAG_CHECK) {
+            // every active WG arrived exactly once and ids were exactly [0, M)
+            uint32_t a = atomicExch(&c->chk_arr[g & 1], 0u);
+            bool bad = a != M;
+            const uint32_t nw = (p.P + 31) / 32;
+            for (uint32_t w = 0; w < nw; ++w) {
+                uint32_t bits = atomicExch(&c->idmap[g & 1][w], 0u);
+                uint32_t lo = w * 32;
+                uint32_t expect = M >= lo + 32 ? 0xffffffffu : (M > lo ? ((1u << (M - lo)) - 1u) : 0u);
+                bad |= bits != expect;
+            }
+            if (bad) { atomicAdd(&c->violations, 1u); atomicCAS(&c->err, DERR_NONE, DERR_INVARIANT); }
+        }
+        // M' of generation g+1, read by survivors and forked CTAs (never by W.M, which
+        // NAIVE kills may lower during g+1)
+        st_relaxed32(&c->mhist[(g + 1) & 7], Mp);
+        __threadfence();
+        st_release64(&c->W, pack_w(g + 1, Mp, 0));
+    }
+    *out_mp = Mp;
+}
+
+__device__ __forceinline__ uint32_t mhist_get(const KParams &p, uint32_t gen) {
+    return ld_relaxed32(&p.ctl->mhist[gen & 7]);
+}
+
+// Resizing (or plain, resizing=false) global barrier for the whole CTA.
+// Returns ACT_CONT (survived; cs.M / cs.gen updated), ACT_KILLED or ACT_ABORT.
+template <class App>
+__device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resizing, uint32_t entry) {
+    __syncthreads();
+    Ctl *c = p.ctl;
+    if (threadIdx.x == 0) {
+        const uint32_t g = cs.gen;
+        if (cs.lid == 0) {  // publish WG 0's transmit-annotated state
+            c->tx0.level = cs.level;
+            c->tx0.in_sel = cs.in_sel;
+        }
+        if (p.flags & COOP_FLAG_CHECK) {
+            atomicAdd(&c->chk_arr[g & 1], 1u);
+            atomicOr(&c->idmap[g & 1][cs.lid >> 5], 1u << (cs.lid & 31));
+        }
+        __threadfence();
+        uint32_t action = ACT_CONT, last = 0, killed_naive = 0;
+        unsigned long long old;
+        if (resizing && p.barrier_mode == COOP_BARRIER_NAIVE && p.policy == COOP_POLICY_SCHEDULER &&
+            cs.lid != 0) {
+            // naive barrier: the slave offers kill on entry; only id M-1 can go
+            old = ld_relaxed64(&c->W);
+            for (;;) {
+                uint32_t Mw = w_M(old);
+                if (cs.lid != Mw - 1 || Mw <= 1) break;
+                uint32_t d = ld_relaxed32(&c->demand);
+                if (d == 0) break;
+                if (atomicCAS(&c->demand, d, d - 1) != d) continue;
+                // W: {g, M, a} -> {g, M-1, a}; retry on concurrent arrivals
+                for (;;) {
+                    unsigned long long nw = pack_w(g, Mw - 1, w_arr(old));
+                    unsigned long long prev = atomicCAS(&c->W, old, nw);
+                    if (prev == old) break;
+                    old = prev;
+                    Mw = w_M(old);
+                }
+                killed_naive = 1;
+                atomicAdd(&c->kills, 1u);
+                uint32_t cur = c->cur_task;
+                uint64_t now = globaltimer();
+                if (cur && cur - 1 < p.events_cap) {
+                    TaskEventDev *e = p.events + (cur - 1);
+                    const uint32_t before = atomicAdd(&e->surrendered, 1u);
+                    if (before == 0) e->t_first_surrender = now;
+                    if (before + 1 >= e->demanded) e->t_last_surrender = now;
+                }
+                if (p.flags & COOP_FLAG_CHECK) {  // withdraw from the arrival check
+                    atomicSub(&c->chk_arr[g & 1], 1u);
+                    atomicAnd(&c->idmap[g & 1][cs.lid >> 5], ~(1u << (cs.lid & 31)));
+                }
+                if (w_arr(old) == Mw - 1) last = 1;   // everybody else already waits: complete on their behalf
+                break;
+            }
+            if (!killed_naive) {
+                old = atomicAdd(&c->W, 1ull);
+                last = (w_arr(old) + 1 == w_M(old)) ? 1u : 0u;
+            }
+        } else {
+            old = atomicAdd(&c->W, 1ull);
+            last = (w_arr(old) + 1 == w_M(old)) ? 1u : 0u;
+        }
+        if (w_gen(old) != g) { atomicCAS(&c->err, DERR_NONE, DERR_INVARIANT); set_abort(p, DERR_INVARIANT); }
+        cs.last = last;
+        cs.bar_M = killed_naive ? w_M(old) - 1 : w_M(old);   // M of the episode for the serial section
+        cs.bar_naive = killed_naive;
+        if (!last) {
+            if (killed_naive) {
+                action = ACT_KILLED;
+            } else {
+                uint32_t spins = 0;
+                unsigned long long w;
+                for (;;) {
+                    w = ld_acquire64(&c->W);
+                    if (w_gen(w) != g) break;
+                    if (spin_check(p, cs, spins)) { action = ACT_ABORT; break; }
+                }
+                if (action != ACT_ABORT) {
+                    if (w_gen(w) != g + 1) {
+                        action = ACT_KILLED;               // W moved on without us => we were killed at g
+                    } else {
+                        uint32_t Mn = mhist_get(p, g + 1);
+                        if (cs.lid >= Mn) action = ACT_KILLED;
+                        else { cs.M = Mn; cs.gen = g + 1; }
+                    }
+                }
+            }
+            __threadfence();
+        }
+        cs.action = action;
+    }
+    __syncthreads();
+    if (cs.last) {  // uniform
+        if (threadIdx.x < 32) {
+            uint32_t Mp;
+            serial_section(p, cs, app, cs.gen, cs.bar_M, resizing, entry, &Mp);
+            if (threadIdx.x == 0) {
+                if (cs.bar_naive || cs.lid >= Mp) cs.action = ACT_KILLED;
+                else { cs.M = Mp; cs.gen = cs.gen + 1; cs.action = ACT_CONT; }
+                if (ld_relaxed32(&c->err) != DERR_NONE) cs.action = ACT_ABORT;
+            }
+        }
+        __syncthreads();
+    }
+    return cs.action;
+}
+
+// ---------------------------------------------------------------- body
+// Fig. 4 with the app's process_node; entry points are the
+// program points after each resizing barrier (forked CTAs start there).
+template <class App, int BLOCK>
+__device__ uint32_t run_body(const KParams &p, CtaState &cs, App &app, uint32_t entry) {
+    uint32_t r;
+    app.enter(p, cs);
+    if (entry == ENTRY_START) {
+        app.template init<BLOCK>(p, cs);
+        r = barrier(p, cs, app, /*resizing=*/false, ENTRY_AFTER_RB2);   // global_barrier
+        if (r != ACT_CONT) return r;
+        entry = ENTRY_AFTER_RB2;
+    }
+    bool skip_to_rb1 = entry == ENTRY_AFTER_RB1;
+    for (;;) {
+        if (!skip_to_rb1) {
+            if (app.empty(p, cs)) return ACT_DONE;            // while (in_nodes.size > 0)
+            app.template expand<BLOCK>(p, cs);                 // for (i = tid; ...) process_node
+            if (threadIdx.x == 0) cs.in_sel ^= 1u;            // swap(&in_nodes, &out_nodes)
+            r = barrier(p, cs, app, true, ENTRY_AFTER_RB1);   // resizing_global_barrier() #1
+            if (r != ACT_CONT) return r;
+        }
+        skip_to_rb1 = false;
+        if (threadIdx.x == 0) cs.level += 1;                  // reset(out_nodes) done in serial; level++
+        if (p.bpl == 2) {
+            r = barrier(p, cs, app, true, ENTRY_AFTER_RB2);   // resizing_global_barrier() #2
+            if (r != ACT_CONT) return r;
+        } else {
+            __syncthreads();
+        }
+    }
+}
+
+__device__ __forceinline__ void flush_stats(const KParams &p, CtaState &cs) {
+    if (threadIdx.x == 0) {
+        if (cs.edges) atomicAdd(&p.ctl->edges_scanned, cs.edges);
+        if (cs.frontier) atomicAdd(&p.ctl->frontier_total, cs.frontier);
+        if (cs.reached) atomicAdd(&p.ctl->reached, cs.reached);
+        cs.edges = cs.frontier = cs.reached = 0;
+    }
+}
+
+// ---------------------------------------------------------------- tasks
+// One block of the synthetic non-cooperative task (K11: occupies a workgroup
+// for a fixed time).  Thread 0 spins on %globaltimer.
+__device__ void run_task_block(const KParams &p, CtaState &cs) {
+    if (threadIdx.x == 0) {
+        Ctl *c = p.ctl;
+        uint64_t t0 = globaltimer();
+        uint32_t cur = ld_relaxed32(&c->cur_task);
+        if (cur && cur - 1 < p.events_cap) atomicCAS(&p.events[cur - 1].t_first_start, 0ull, (unsigned long long)t0);
+        unsigned long long ns = ld_relaxed64(&c->task_block_ns);
+        uint32_t spins = 0;
+        while (globaltimer() - t0 < ns) {
+            if (spin_check(p, cs, spins)) break;
+            __nanosleep(100);
+        }
+        __threadfence();
+        uint32_t total = ld_relaxed32(&c->task_total);
+        if (atomicAdd(&c->task_done, 1u) + 1 == total && cur && cur - 1 < p.events_cap)
+            p.events[cur - 1].t_end = globaltimer();
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------- scheduler CTA
+__device__ void scheduler_loop(const KParams &p, CtaState &cs) {
+    if (threadIdx.x != 0) return;
+    Ctl *c = p.ctl;
+    const uint64_t t0 = globaltimer();
+    uint64_t next = t0 + p.task_first_ns;
+    uint32_t posted = 0, inflight = 0, cur = 0, spins = 0;
+    uint32_t pend_task = 0, pend_wgs = 0, pend_blocks = 0;
+    unsigned long long pend_ns = 0;
+    for (;;) {
+        if (ld_relaxed32(&c->err) != DERR_NONE) break;
+        const uint64_t now = globaltimer();
+        const uint32_t done = ld_acquire32(&c->done);
+        if (p.host) {  // host packets (SVM-style channel)
+            uint32_t s = ld_sys32(&p.host->seq);
+            if (s != c->host_seq_seen) {
+                uint32_t kind = ld_sys32(&p.host->kind);
+                if (kind == 1) { pend_task = 1; pend_wgs = p.host->a; pend_blocks = p.host->b; pend_ns = p.host->c; }
+                else if (kind == 2) atomicAdd(&c->demand, (uint32_t)p.host->a);
+                else if (kind == 3) atomicAdd(&c->grant, (uint32_t)p.host->a);
+                c->host_seq_seen = s;
+                __threadfence_system();
+                p.host->ack = s;
+            }
+            p.host->cur_m = w_M(ld_relaxed64(&c->W));
+            p.host->demand_mirror = ld_relaxed32(&c->demand);
+        }
+        if (inflight) {
+            if (ld_acquire32(&c->task_done) >= c->task_total) {
+                st_relaxed32(&c->task_next, 0xFFFFFFFFu);
+                uint32_t rem = atomicExch(&c->demand, 0u);
+                TaskEventDev *e = cur < p.events_cap ? p.events + cur : nullptr;
+                uint32_t surrendered = e ? e->surrendered : (c->task_wgs - min(rem, c->task_wgs));
+                if (surrendered) atomicAdd(&c->grant, surrendered);   // fork them back
+                c->tasks_completed += 1;
+                c->cur_task = 0;
+                inflight = 0;
+            }
+        } else if (!done) {
+            bool periodic = p.task_period_ns && (p.task_max == 0 || posted < p.task_max) && now >= next;
+            if (periodic || pend_task) {
+                uint32_t q = pend_task ? pend_wgs : p.task_wgs;
+                uint32_t b = pend_task ? pend_blocks : p.task_blocks;
+                unsigned long long ns = pend_task ? pend_ns : p.task_block_ns;
+                pend_task = 0;
+                cur = posted++;
+                if (cur < p.events_cap) {
+                    TaskEventDev *e = p.events + cur;
+                    e->t_arrive = now;
+                    e->demanded = q;
+                }
+                c->task_total = b;
+                c->task_done = 0;
+                c->task_block_ns = ns;
+                c->task_wgs = q;
+                c->cur_task = cur + 1;
+                c->tasks_posted = posted;
+                c->n_events = min(posted, p.events_cap);
+                __threadfence();
+                st_release32(&c->task_next, 0u);       // blocks become claimable
+                atomicAdd(&c->demand, q);               // resource message: surrender q WGs
+                inflight = 1;
+                if (periodic) next += p.task_period_ns;
+            }
+        }
+        if (done && !inflight) break;
+        if (spin_check(p, cs, spins)) break;
+        __nanosleep(400);
+    }
+    if (p.host) p.host->done_mirror = 1;
+}
+
+// ---------------------------------------------------------------- park loop
+// The megakernel worker pool: wait for a fork assignment,
+// otherwise run blocks of the competing task; exit at termination.
+template <class App, int BLOCK>
+__device__ void park_loop(const KParams &p, CtaState &cs, App &app) {
+    Ctl *c = p.ctl;
+    const uint32_t phys = blockIdx.x;
+    const uint32_t wi = phys >> 5, bit = 1u << (phys & 31);
+    for (;;) {
+        if (threadIdx.x == 0) {
+            uint32_t action = ACT_IDLE, spins = 0;
+            Mailbox *mb = p.mb + phys;
+            for (;;) {
+                uint32_t f = ld_acquire32(&mb->flag);
+                if (f != cs.consumed) {
+                    cs.consumed = f;
+                    Transmit t = mb->tx;
+                    cs.lid = t.lid; cs.gen = t.gen; cs.level = t.level; cs.in_sel = t.in_sel; cs.entry = t.entry;
+                    action = ACT_RUN_BODY;
+                    break;
+                }
+                if (ld_acquire32(&c->done)) {
+                    if (ld_acquire32(&mb->flag) != cs.consumed) continue;   // a final fork happened-before done
+                    if (ld_relaxed32(&c->task_next) >= c->task_total) { action = ACT_EXIT; break; }
+                }
+                if (ld_relaxed32(&c->err) != DERR_NONE) { action = ACT_EXIT; break; }
+                if (ld_relaxed32(&c->task_next) < ld_relaxed32(&c->task_total)) {
+                    uint32_t old = atomicAnd(&c->pool[wi], ~bit);     // leave the forkable set
+                    if (old & bit) {
+                        uint32_t b = atomicAdd(&c->task_next, 1u);
+                        if (b < c->task_total) { cs.block = b; action = ACT_RUN_TASK; break; }
+                        atomicOr(&c->pool[wi], bit);
+                    }
+                }
+                if (spin_check(p, cs, spins)) { action = ACT_EXIT; break; }
+                __nanosleep(128);
+            }
+            cs.action = action;
+        }
+        __syncthreads();
+        const uint32_t act = cs.action;
+        if (act == ACT_EXIT) return;
+        if (act == ACT_RUN_TASK) {
+            run_task_block(p, cs);
+            if (threadIdx.x == 0) { __threadfence(); atomicOr(&c->pool[wi], bit); }
+            continue;
+        }
+        // forked: join generation cs.gen once W reaches it (the release of the fork episode)
+        if (threadIdx.x == 0) {
+            uint32_t spins = 0;
+            cs.action = ACT_CONT;
+            while (w_gen(ld_acquire64(&c->W)) != cs.gen) {
+                if (spin_check(p, cs, spins)) { cs.action = ACT_ABORT; break; }
+            }
+            cs.M = mhist_get(p, cs.gen);
+            __threadfence();
+        }
+        __syncthreads();
+        if (cs.action == ACT_ABORT) return;
+        uint32_t r = run_body<App, BLOCK>(p, cs, app, cs.entry);
+        flush_stats(p, cs);
+        if (r == ACT_DONE) {
+            if (threadIdx.x == 0 && cs.lid == 0) {
+                c->t_end = globaltimer();
+                st_release32(&c->done, 1);
+            }
+        }
+        if (r == ACT_ABORT) return;
+        // killed (offer_kill accepted) or finished: back to the worker pool, where the
+        // CTA can run task blocks and be forked again
+        if (threadIdx.x == 0) { __threadfence(); atomicOr(&c->pool[wi], bit); }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- kernel
+template <class App, int BLOCK, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(KParams p) {
+    __shared__ CtaState cs;
+    App app;
+    if (threadIdx.x == 0) {
+        const uint64_t t0 = globaltimer();
+        cs.deadline = t0 + p.timeout_ns;
+        cs.edges = cs.frontier = cs.reached = 0;
+        cs.consumed = 0;
+        cs.lid = blockIdx.x; cs.M = p.M0; cs.gen = 0; cs.level = 0; cs.in_sel = 0;
+        if (blockIdx.x == 0) p.ctl->t_start = t0;
+    }
+    __syncthreads();
+    if (p.has_sched && blockIdx.x == p.P) { scheduler_loop(p, cs); return; }
+    if (blockIdx.x < p.M0) {
+        uint32_t r = run_body<App, BLOCK>(p, cs, app, ENTRY_START);
+        flush_stats(p, cs);
+        if (r == ACT_DONE) {
+            if (threadIdx.x == 0 && cs.lid == 0) {
+                p.ctl->t_end = globaltimer();
+                st_release32(&p.ctl->done, 1);
+            }
+            if (p.barrier_mode == COOP_BARRIER_PLAIN) return;
+        }
+        if (r == ACT_ABORT) return;
+        if (threadIdx.x == 0) {   // killed or finished: join the worker pool
+            __threadfence();
+            atomicOr(&p.ctl->pool[blockIdx.x >> 5], 1u << (blockIdx.x & 31));
+        }
+        __syncthreads();
+    }
+    if (p.barrier_mode == COOP_BARRIER_PLAIN) return;
+    park_loop<App, BLOCK>(p, cs, app);
+}
+
+}  // namespace coop
