@@ -103,6 +103,16 @@ def dist_env():
     return ws, rank, local
 
 
+def alg_bytes_bfs(st, V):
+    """Algorithmic HBM bytes of one cooperative BFS launch:
+    4 B per column index examined (top-down scans + bottom-up checks), 20 B per
+    reached vertex (frontier entry read 4 + row offsets 8 + level write 4 +
+    append 4), the level init 4V + V/8 bitmap, and per bottom-up level the
+    sequential row-offset read 4V plus the visited and frontier bitmaps 3V/8."""
+    return (4 * st.edges_scanned + 20 * st.reached + 4 * V + V // 8
+            + st.bottom_up_levels * (4 * V + 3 * V // 8))
+
+
 def make_graph(scale, device):
     import graphgen as gg
     t = time.time()
@@ -206,42 +216,42 @@ def run_ours(args, ws, rank, local):
         return e0.elapsed_time(e1), k0.elapsed_time(k1), st
 
     # ---- main: standalone cooperative BFS (NeverResize)
+    flags = 0 if args.topdown else coop.FLAG_DIROPT
     for i in range(args.warmup):
-        one(i)
+        one(i, flags=flags)
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
-    times, ktimes, edges, reached, scanned = [], [], [], [], []
+    times, ktimes, stats = [], [], []
     with ClockSampler(local) as clk:
         for i in range(args.warmup, n_steps):
-            t, kt, st = one(i)
+            t, kt, st = one(i, flags=flags)
             times.append(t)
             ktimes.append(kt)
-            edges.append(st.edges_scanned // 2)
-            scanned.append(st.edges_scanned)
-            reached.append(st.reached)
+            stats.append(st)
+            # Graph500 edge count of this traversal, from the result (untimed)
+            st.teps_edges = int(deg[out >= 0].sum().item()) // 2
     torch.cuda.synchronize(dev)
     tot_ms = sum(times)
     if ws > 1:
         t = torch.tensor([tot_ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         tot_ms = float(t.item())
-        ed = torch.tensor([float(sum(edges))], device=dev)
+        ed = torch.tensor([float(sum(s.teps_edges for s in stats))], device=dev)
         torch.distributed.all_reduce(ed)
         all_edges = float(ed.item())
     else:
-        all_edges = float(sum(edges))
+        all_edges = float(sum(s.teps_edges for s in stats))
     gteps = all_edges / (tot_ms * 1e-3) / 1e9
-    # roofline of the persistent kernel: algorithmic bytes per launch / kernel time
     peak, peak_src = _peaks()
-    s_o = 4
-    alg_bytes = [4 * sc + (12 + 2 * s_o) * r + 4 * V + V // 8 for sc, r in zip(scanned, reached)]
+    alg_bytes = [alg_bytes_bfs(st, V) for st in stats]
     achieved = sum(alg_bytes) / (sum(ktimes) * 1e-3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("bfs_rmat24", {}).get("dram_bytes_per_launch")
+            key = "bfs_rmat%d_%s" % (args.scale, "topdown" if args.topdown else "diropt")
+            traffic = json.load(open(prof)).get(key, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
@@ -256,15 +266,16 @@ def run_ours(args, ws, rank, local):
         col_h = g.col_idx.cpu().pin_memory()
         lv_h = torch.empty(V, dtype=torch.int32).pin_memory()
         et, ee = [], []
+        deg_h = deg.cpu()
         for i in range(1 + 3):
             s = srcs[i]
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
-            _, st = coop.bfs_host(ro_h, col_h, s, lv_h, threads_per_wg=args.threads)
+            coop.bfs_host(ro_h, col_h, s, lv_h, threads_per_wg=args.threads, flags=flags)
             dt = time.perf_counter() - t0
             if i >= 1:
                 et.append(dt)
-                ee.append(st.edges_scanned // 2)
+                ee.append(int(deg_h[lv_h >= 0].sum()) // 2)
         e2e = {"value": sum(ee) / sum(et) / 1e9, "unit": "GTEPS",
                "h2d_bytes_per_step": int(ro_h.numel() * 4 + col_h.numel() * 4),
                "d2h_bytes_per_step": int(V * 4), "steps": len(et)}
@@ -284,13 +295,15 @@ def run_ours(args, ws, rank, local):
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (RMAT, Graph500 parameters a,b,c=.57,.19,.19, edgefactor 16, seed 1, relabelled)",
-            "config": {"workload": f"BFS RMAT-{args.scale} (configs[2]), standalone cooperative, NeverResize",
+            "config": {"workload": f"BFS RMAT-{args.scale} (configs[2]), standalone cooperative, NeverResize, "
+                                   + ("top-down" if args.topdown else "direction-optimising (top-down + bottom-up levels)"),
                        "scale": args.scale, "vertices": V, "directed_edges": E, "sources": args.steps,
                        "wgs": info["max_coresident"], "threads_per_wg": args.threads,
                        "l2": "flushed (256 MB write) before every step; CSR 2.2 GB > L2",
                        "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
                        "graph_gen_s": round(gen_s, 2)},
             "kernel_ms_per_step": sum(ktimes) / len(ktimes),
+            "levels": stats[-1].levels, "bottom_up_levels": stats[-1].bottom_up_levels,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "coop_kernel<BfsApp<uint32_t>,%d>" % args.threads,
@@ -397,6 +410,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scale", type=int, default=24)
     ap.add_argument("--threads", type=int, default=512)
+    ap.add_argument("--topdown", action="store_true", help="main line without direction optimisation")
     ap.add_argument("--quick", action="store_true", help="skip the extra objects")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)

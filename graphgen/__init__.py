@@ -259,3 +259,92 @@ def graph_hash(g: CSR) -> str:
     if g.weights is not None:
         h.update(g.weights.cpu().numpy().tobytes())
     return h.hexdigest()[:16]
+
+
+# ---------------------------------------------------------------- 1-D partition (configs[4])
+@dataclasses.dataclass
+class PartCSR:
+    """Rank `rank`'s share of a 1-D vertex partition: every edge (u, v) whose
+    destination v lies in [v_begin, v_end), indexed by the GLOBAL source u
+    (row_offsets has V+1 entries), destinations stored rank-local (v - v_begin)."""
+    num_vertices: int
+    v_begin: int
+    v_end: int
+    rank: int
+    nranks: int
+    row_offsets: torch.Tensor
+    col_local: torch.Tensor
+
+    @property
+    def num_edges(self) -> int:
+        return int(self.col_local.numel())
+
+    def local_degrees(self) -> torch.Tensor:
+        return self.row_offsets[1:] - self.row_offsets[:-1]
+
+
+def part_bounds(V: int, P: int) -> list[int]:
+    """Owned-range boundaries, multiples of 32 (whole bitmap words per rank)."""
+    nw = (V + 31) // 32
+    b = [min(V, (p * nw // P) * 32) for p in range(P)]
+    return b + [V]
+
+
+def partition(g: CSR, P: int, rank: int) -> PartCSR:
+    b = part_bounds(g.num_vertices, P)
+    vb, ve = b[rank], b[rank + 1]
+    col = g.col_idx
+    keep = (col >= vb) & (col < ve)
+    cm = torch.zeros(col.numel() + 1, dtype=torch.int64, device=col.device)
+    cm[1:] = torch.cumsum(keep.to(torch.int64), 0)
+    ro = cm[g.row_offsets]
+    return PartCSR(g.num_vertices, vb, ve, rank, P, ro, (col[keep] - vb).to(torch.int32))
+
+
+def rmat_partition(scale: int, P: int, rank: int, edgefactor: int = 16, seed: int = 1, device="cpu",
+                   chunk: int = 1 << 25) -> PartCSR:
+    """Rank `rank`'s share of rmat(scale, ...) built without materialising the
+    whole graph: the same tuples are drawn, but only the directed entries whose
+    destination this rank owns are kept (equals partition(rmat(...), P, rank))."""
+    V = 1 << scale
+    ntup = edgefactor * V
+    a, bq, c = 0.57, 0.19, 0.19
+    t1, t2, t3 = int(a * (1 << 53)), int((a + bq) * (1 << 53)), int((a + bq + c) * (1 << 53))
+    smix = _s64(splitmix64_int(seed & _M64))
+    perm_keys = splitmix64(torch.arange(V, dtype=torch.int64, device=device) ^ _s64(splitmix64_int((seed + 0x5EED) & _M64)))
+    order = torch.argsort(perm_keys, stable=True)
+    pi = torch.empty_like(order)
+    pi[order] = torch.arange(V, dtype=torch.int64, device=device)
+    del perm_keys, order
+    bnd = part_bounds(V, P)
+    vb, ve = bnd[rank], bnd[rank + 1]
+    keys = []
+    for start in range(0, ntup, chunk):
+        i = torch.arange(start, min(ntup, start + chunk), dtype=torch.int64, device=device)
+        u = torch.zeros_like(i)
+        v = torch.zeros_like(i)
+        base = (i << 6) ^ smix
+        del i
+        for k in range(scale):
+            x = uniform_u53(splitmix64(base ^ k))
+            u = (u << 1) | (x >= t2).to(torch.int64)
+            v = (v << 1) | (((x >= t1) & (x < t2)) | (x >= t3)).to(torch.int64)
+            del x
+        del base
+        u = pi[u]
+        v = pi[v]
+        src = torch.cat([u, v])
+        dst = torch.cat([v, u])
+        del u, v
+        keep = (src != dst) & (dst >= vb) & (dst < ve)
+        keys.append(torch.unique(src[keep] * V + dst[keep]))
+        del src, dst, keep
+    key = torch.unique(torch.cat(keys)) if keys else torch.zeros(0, dtype=torch.int64, device=device)
+    del keys
+    s = key // V
+    d = (key - s * V - vb).to(torch.int32)
+    del key
+    counts = torch.bincount(s, minlength=V)
+    ro = torch.zeros(V + 1, dtype=torch.int64, device=device)
+    ro[1:] = torch.cumsum(counts, 0)
+    return PartCSR(V, vb, ve, rank, P, ro, d)

@@ -69,6 +69,8 @@ typedef enum {
 } coop_policy;
 
 #define COOP_FLAG_CHECK 0x1u   /* per-episode arrival / contiguity / message-passing checks -> COOP_ERR_INVARIANT */
+#define COOP_FLAG_DIROPT 0x2u  /* BFS: direction-optimising levels (bottom-up on large frontiers, Beamer's
+                                  alpha=14 / beta=24 switch); results are identical, only the work differs */
 
 /* CSR graph, device memory, neighbour lists of vertex v at [row_offsets[v], row_offsets[v+1]). */
 typedef struct {
@@ -104,6 +106,7 @@ typedef struct {
     void *stream;               /* cudaStream_t (NULL = legacy default stream) */
     void *ev_kernel_start;      /* optional cudaEvent_t recorded on `stream` right before the persistent kernel */
     void *ev_kernel_end;        /* optional cudaEvent_t recorded on `stream` right after it (kernel-only timing) */
+    uint32_t workspace;         /* scratch set on the device (0..7): concurrent calls on one device need distinct ones */
 } coop_opts;
 
 /* One competing-task instance, all times from %globaltimer (ns). */
@@ -129,6 +132,7 @@ typedef struct {
     uint32_t n_wgs;             /* N launched */
     uint32_t threads_per_wg;
     uint32_t tasks_posted, tasks_completed;
+    uint32_t bottom_up_levels;  /* COOP_FLAG_DIROPT: levels run bottom-up */
     uint32_t *m_trace;          /* optional caller-owned HOST buffer: M after each resizing episode */
     uint32_t m_trace_cap;
     uint32_t *level_sizes;      /* optional caller-owned HOST buffer: frontier size per level */
@@ -209,9 +213,50 @@ coop_status coop_barrier_bench(uint32_t n_ctas, uint32_t threads, uint64_t iters
  */
 coop_status coop_l2_atomic_rtt(uint64_t iters, double *ns_per_atomic);
 
-/* ---- asynchronous handle API (host <-> GPU channel, P:870-903) ---- */
 typedef struct coop_handle coop_handle;
 
+/* ---- 1-D vertex-partitioned BFS across the GPUs of one node (BASELINE.json configs[4]) ----
+ * Not in the paper (single iGPU).  One call per rank; every rank runs the
+ * cooperative BFS kernel over its partition and the per-level frontier is
+ * all-gathered INSIDE the kernel: each rank stores its slice of the next
+ * frontier bitmap into every peer's copy (NVLink peer memory) and the
+ * resizing barrier's serial section doubles as the cross-GPU barrier
+ * (release/acquire flags at system scope).  Pointers to peer buffers come
+ * from coop_ipc_* (or are plain device pointers when all ranks share a GPU). */
+#define COOP_MAX_RANKS 8
+typedef struct {
+    int64_t num_vertices;       /* global V */
+    int64_t v_begin, v_end;     /* owned vertices [v_begin, v_end); v_begin % 32 == 0 */
+    int32_t rank, nranks;       /* 1 <= nranks <= COOP_MAX_RANKS */
+    uint32_t seq;               /* call sequence number: identical on all ranks, new for every call */
+    const void *row_offsets;    /* device, V+1 offsets of the local edges (destination owned), by global source */
+    int32_t offset_bits;        /* 32 or 64 */
+    const int32_t *col_local;   /* device, destination - v_begin */
+    int64_t num_edges;          /* local edges */
+    const uint32_t *hub_ids;    /* device, ascending vertices with local degree >= hub_degree (NULL if none) */
+    const uint64_t *hub_prefix; /* device, num_hubs + 1 prefix sums of the hubs' local degrees */
+    uint32_t num_hubs, hub_degree;
+    uint32_t *frontier[COOP_MAX_RANKS][2]; /* rank q's two frontier bitmaps, ceil(V/32) words each, device-visible */
+    uint64_t *flags[COOP_MAX_RANKS];       /* rank q's flag block, 2*COOP_MAX_RANKS uint64, zeroed once when allocated */
+} coop_part;
+
+/* Blocking partitioned BFS of this rank.  levels_owned_out: device int32[v_end - v_begin];
+ * on COOP_OK entry i = hop distance of vertex v_begin + i, -1 if unreachable. */
+coop_status coop_bfs_part(const coop_part *part, int64_t source, int32_t *levels_owned_out,
+                          const coop_opts *opts, coop_stats *stats);
+/* Asynchronous variant (finish with coop_wait); several ranks may share one GPU
+ * when each uses its own opts->workspace and stream. */
+coop_status coop_bfs_part_launch(const coop_part *part, int64_t source, int32_t *levels_owned_out,
+                                 const coop_opts *opts, coop_handle **handle);
+/* Exchange buffers: cudaMalloc'd (so they can be shared by IPC) and zeroed; and
+ * CUDA IPC helpers for the peer frontier buffers (64-byte opaque handles). */
+coop_status coop_exchange_alloc(uint64_t bytes, void **dptr);
+coop_status coop_exchange_free(void *dptr);
+coop_status coop_ipc_get_handle(const void *dptr, void *handle64);
+coop_status coop_ipc_open(const void *handle64, void **dptr);
+coop_status coop_ipc_close(void *dptr);
+
+/* ---- asynchronous handle API (host <-> GPU channel, P:870-903) ---- */
 /* Launch cooperative BFS (kind 0) or SSSP (kind 1) asynchronously; opts->policy
  * must be COOP_POLICY_SCHEDULER.  Resource messages and tasks then come from the
  * host through a host-mapped mailbox polled by the scheduler CTA (the paper's

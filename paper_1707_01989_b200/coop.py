@@ -23,6 +23,7 @@ STATUS_NAMES = {0: "COOP_OK", 1: "COOP_ERR_INVALID_ARG", 2: "COOP_ERR_CUDA", 3: 
 BARRIER_QUERY, BARRIER_PLAIN, BARRIER_NAIVE = 0, 1, 2
 POLICY_NEVER, POLICY_SCRIPTED, POLICY_RANDOM, POLICY_SCHEDULER = 0, 1, 2, 3
 FLAG_CHECK = 0x1
+FLAG_DIROPT = 0x2
 
 
 class CoopError(RuntimeError):
@@ -48,7 +49,8 @@ class Opts(ctypes.Structure):
                 ("task_block_ns", ctypes.c_uint64), ("task_period_ns", ctypes.c_uint64),
                 ("task_first_ns", ctypes.c_uint64), ("task_max", ctypes.c_uint32),
                 ("timeout_ns", ctypes.c_uint64), ("stream", ctypes.c_void_p),
-                ("ev_kernel_start", ctypes.c_void_p), ("ev_kernel_end", ctypes.c_void_p)]
+                ("ev_kernel_start", ctypes.c_void_p), ("ev_kernel_end", ctypes.c_void_p),
+                ("workspace", ctypes.c_uint32)]
 
 
 class TaskEvent(ctypes.Structure):
@@ -65,6 +67,7 @@ class Stats(ctypes.Structure):
                 ("min_m", ctypes.c_uint32), ("max_m", ctypes.c_uint32),
                 ("n_wgs", ctypes.c_uint32), ("threads_per_wg", ctypes.c_uint32),
                 ("tasks_posted", ctypes.c_uint32), ("tasks_completed", ctypes.c_uint32),
+                ("bottom_up_levels", ctypes.c_uint32),
                 ("m_trace", ctypes.POINTER(ctypes.c_uint32)), ("m_trace_cap", ctypes.c_uint32),
                 ("level_sizes", ctypes.POINTER(ctypes.c_uint32)), ("level_sizes_cap", ctypes.c_uint32),
                 ("task_events", ctypes.POINTER(TaskEvent)), ("task_events_cap", ctypes.c_uint32)]
@@ -79,6 +82,17 @@ class DeviceInfo(ctypes.Structure):
 class BarrierStats(ctypes.Structure):
     _fields_ = [("iters", ctypes.c_uint64), ("ns_per_barrier", ctypes.c_double), ("kernel_ns", ctypes.c_uint64),
                 ("kills", ctypes.c_uint32), ("forks", ctypes.c_uint32), ("violations", ctypes.c_uint32)]
+
+
+class CoopPart(ctypes.Structure):
+    """coop_part (1-D partitioned BFS, one rank)."""
+    _fields_ = [("num_vertices", ctypes.c_int64), ("v_begin", ctypes.c_int64), ("v_end", ctypes.c_int64),
+                ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("seq", ctypes.c_uint32),
+                ("row_offsets", ctypes.c_void_p), ("offset_bits", ctypes.c_int32),
+                ("col_local", ctypes.c_void_p), ("num_edges", ctypes.c_int64),
+                ("hub_ids", ctypes.c_void_p), ("hub_prefix", ctypes.c_void_p),
+                ("num_hubs", ctypes.c_uint32), ("hub_degree", ctypes.c_uint32),
+                ("frontier", (ctypes.c_void_p * 2) * 8), ("flags", ctypes.c_void_p * 8)]
 
 
 # every function declared in include/coop.h: name -> (restype, argtypes)
@@ -110,6 +124,15 @@ SIGNATURES = {
     "coop_current_m": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint32)]),
     "coop_wait": (ctypes.c_int, [_P, ctypes.POINTER(Stats)]),
     "coop_destroy": (None, [_P]),
+    "coop_bfs_part": (ctypes.c_int, [ctypes.POINTER(CoopPart), ctypes.c_int64, _P, ctypes.POINTER(Opts),
+                                     ctypes.POINTER(Stats)]),
+    "coop_bfs_part_launch": (ctypes.c_int, [ctypes.POINTER(CoopPart), ctypes.c_int64, _P, ctypes.POINTER(Opts),
+                                            ctypes.POINTER(_P)]),
+    "coop_exchange_alloc": (ctypes.c_int, [ctypes.c_uint64, ctypes.POINTER(_P)]),
+    "coop_exchange_free": (ctypes.c_int, [_P]),
+    "coop_ipc_get_handle": (ctypes.c_int, [_P, _P]),
+    "coop_ipc_open": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
+    "coop_ipc_close": (ctypes.c_int, [_P]),
 }
 
 _lib = None
@@ -153,6 +176,7 @@ class RunStats:
     threads_per_wg: int = 0
     tasks_posted: int = 0
     tasks_completed: int = 0
+    bottom_up_levels: int = 0
     m_trace: list = field(default_factory=list)
     level_sizes: list = field(default_factory=list)
     task_events: list = field(default_factory=list)
@@ -193,7 +217,7 @@ def _device_csr(g, need_weights: bool):
 def make_opts(*, max_wgs=0, init_wgs=0, threads_per_wg=0, barrier_mode=BARRIER_QUERY, barriers_per_level=1,
               policy=POLICY_NEVER, script: Optional[Sequence[int]] = None, flags=0, seed=0, resize_prob=0.0,
               task_wgs=0, task_blocks=0, task_block_ns=0, task_period_ns=0, task_first_ns=0, task_max=0,
-              timeout_ns=0, stream=None, ev_kernel_start=None, ev_kernel_end=None):
+              timeout_ns=0, stream=None, ev_kernel_start=None, ev_kernel_end=None, workspace=0):
     import torch
     o = Opts()
     o.max_wgs, o.init_wgs, o.threads_per_wg = max_wgs, init_wgs, threads_per_wg
@@ -210,6 +234,7 @@ def make_opts(*, max_wgs=0, init_wgs=0, threads_per_wg=0, barrier_mode=BARRIER_Q
     if stream is None and torch.cuda.is_available():
         stream = torch.cuda.current_stream().cuda_stream
     o.stream = stream
+    o.workspace = workspace
     if ev_kernel_start is not None:   # torch.cuda.Event(enable_timing=True)
         o.ev_kernel_start = ev_kernel_start.cuda_event
         o.ev_kernel_end = ev_kernel_end.cuda_event
@@ -234,7 +259,8 @@ def _stats_struct(trace_cap=0, level_cap=0, event_cap=0):
 def _to_runstats(st: Stats, bufs) -> RunStats:
     r = RunStats(**{k: getattr(st, k) for k in ("kernel_ns", "edges_scanned", "frontier_total", "reached",
                                                 "levels", "episodes", "kills", "forks", "min_m", "max_m",
-                                                "n_wgs", "threads_per_wg", "tasks_posted", "tasks_completed")})
+                                                "n_wgs", "threads_per_wg", "tasks_posted", "tasks_completed",
+                                                "bottom_up_levels")})
     if "m" in bufs:
         r.m_trace = list(bufs["m"][: min(st.episodes, st.m_trace_cap)])
     if "l" in bufs:

@@ -23,11 +23,21 @@ template <typename T>
 __device__ __forceinline__ T ldcg(const T *p) { return __ldcg(p); }
 
 // ============================================================== BFS
+// Level L reads frontier parity in = L & 1 (the transmitted in_sel) and fills
+// parity out.  Modes (chosen by the serial section at the end of each level):
+//   TDQ  top-down over the light/heavy frontier queues (process_node of Fig. 4)
+//   TDB  top-down over the frontier bitmap (the level after a bottom-up level)
+//   BU   bottom-up: every unvisited vertex looks for a parent in the frontier
+//        bitmap (direction optimisation; only with COOP_FLAG_DIROPT)
+// Every mode produces the same level values (BFS levels are unique).
 template <typename OffT>
 struct BfsApp {
     using LE = typename std::conditional<sizeof(OffT) == 4, LightEntry, LightEntry64>::type;
+    static constexpr int KB = 4;   // 32-edge windows per warp iteration (32*KB <= kHeavyDeg)
 
     __device__ void enter(const KParams &, CtaState &) {}
+    template <int BLOCK>
+    __device__ void between(const KParams &, CtaState &) {}
 
     template <int BLOCK>
     __device__ void init(const KParams &p, CtaState &cs) {
@@ -51,7 +61,15 @@ struct BfsApp {
         }
         for (uint64_t i = h + 4 * nvec + tid; i < (uint64_t)V; i += nth) lv[i] = (int64_t)i == s ? 0 : -1;
         const uint64_t nw = ((uint64_t)V + 31) / 32;
-        for (uint64_t i = tid; i < nw; i += nth) p.visited[i] = i == (uint64_t)(s >> 5) ? (1u << (s & 31)) : 0u;
+        const uint32_t sw = (uint32_t)(s >> 5), sb = 1u << (s & 31);
+        for (uint64_t i = tid; i < nw; i += nth) {
+            p.visited[i] = i == sw ? sb : 0u;
+            if (p.dopt) {
+                p.fbits[0][i] = i == sw ? sb : 0u;
+                p.fbits[1][i] = 0u;
+                p.fbits[2][i] = 0u;
+            }
+        }
         if (cs.lid == 0 && threadIdx.x == 0) {
             const OffT *ro = static_cast<const OffT *>(p.ro);
             const OffT b = ro[s], e = ro[s + 1];
@@ -66,6 +84,10 @@ struct BfsApp {
                 static_cast<LE *>(p.qlight[0])[0] = le;
                 p.ctl->qsize[0] = 1;
             }
+            p.ctl->nf[0] = 1;
+            p.ctl->mf[0] = deg;
+            p.ctl->vis_edges = deg;
+            p.ctl->bmode[0] = BFS_TDQ;
             cs.reached += 1;
             if (p.level_cap) p.level_sizes[0] = 1;
             p.ctl->frontier_total = 1;
@@ -76,92 +98,105 @@ struct BfsApp {
     __device__ bool empty(const KParams &p, CtaState &cs) {
         if (threadIdx.x == 0) {
             const uint32_t in = cs.in_sel;
-            const uint32_t nl = ld_relaxed32(&p.ctl->qsize[in]);
             const unsigned long long hv = ld_relaxed64(&p.ctl->heavy[in]);
-            cs.app_u32[0] = nl;
-            cs.app_u32[1] = (uint32_t)(hv >> 40);
             const uint64_t Eh = hv & kMask40;
+            cs.app_u32[0] = ld_relaxed32(&p.ctl->qsize[in]);
+            cs.app_u32[1] = (uint32_t)(hv >> 40);
             cs.app_u32[2] = (uint32_t)Eh;
             cs.app_u32[3] = (uint32_t)(Eh >> 32);
+            cs.app_u32[4] = ld_relaxed64(&p.ctl->nf[in]) ? 1u : 0u;
+            cs.app_u32[5] = ld_relaxed32(&p.ctl->bmode[in]);
         }
         __syncthreads();
-        return cs.app_u32[0] == 0 && cs.app_u32[1] == 0;
+        return cs.app_u32[4] == 0;
     }
 
-    // claim u at level L1 (atomic on the visited bitmap, reading R8) and push it
-    // to the next frontier; warp-collective (every lane calls, u < 0 = nothing)
-    __device__ __forceinline__ void visit(const KParams &p, int32_t u, uint32_t L1, uint32_t out,
-                                          uint32_t &reached) {
+    // ---------------------------------------------------------- top-down claim
+    // Claim a batch of K candidates per lane at level L1 and push the winners to
+    // the next frontier (warp-collective; u < 0 = no candidate).  The K probes,
+    // the K atomics and the K offset reads are independent, so each warp keeps
+    // K memory operations of each kind in flight.
+    template <int K>
+    __device__ __forceinline__ void visit_batch(const KParams &p, const int32_t (&u)[K], uint32_t L1,
+                                                uint32_t out, uint32_t *fnext, uint32_t &reached,
+                                                uint64_t &mfsum) {
         const uint32_t lane = threadIdx.x & 31;
-        bool win = false;
-        OffT nb = 0;
-        uint32_t nd = 0;
-        if (u >= 0) {
-            const uint32_t wd = (uint32_t)u >> 5, bit = 1u << (u & 31);
-            const uint32_t cur = p.visited[wd];                 // non-atomic pre-check (stale 0 is safe)
-            if (!(cur & bit)) {
-                const uint32_t old = atomicOr(&p.visited[wd], bit);
-                if (!(old & bit)) {
-                    win = true;
-                    p.level_out[u] = (int32_t)L1;
-                    const OffT *ro = static_cast<const OffT *>(p.ro);
-                    nb = __ldg(ro + u);
-                    nd = (uint32_t)(__ldg(ro + u + 1) - nb);
+        uint32_t *vis = p.visited;
+        uint32_t cur[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) cur[k] = u[k] >= 0 ? vis[(uint32_t)u[k] >> 5] : 0xFFFFFFFFu;  // pre-check
+        bool win[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            win[k] = false;
+            if (u[k] >= 0) {
+                const uint32_t bit = 1u << (u[k] & 31);
+                if (!(cur[k] & bit)) win[k] = !(atomicOr(vis + ((uint32_t)u[k] >> 5), bit) & bit);   // claim
+            }
+        }
+        const OffT *ro = static_cast<const OffT *>(p.ro);
+        OffT nb[K];
+        uint32_t nd[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            nb[k] = 0;
+            nd[k] = 0;
+            if (win[k]) {
+                p.level_out[u[k]] = (int32_t)L1;
+                nb[k] = __ldg(ro + u[k]);
+                nd[k] = (uint32_t)(__ldg(ro + u[k] + 1) - nb[k]);
+                mfsum += nd[k];
+                if (fnext) atomicOr(fnext + ((uint32_t)u[k] >> 5), 1u << (u[k] & 31));
+            }
+        }
+        // contract: warp ballots, one queue atomic per warp for the whole batch
+        uint32_t m[K], off[K], tot = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            reached += __popc(__ballot_sync(FULL, win[k]));
+            m[k] = __ballot_sync(FULL, win[k] && nd[k] > 0 && nd[k] < kHeavyDeg);
+            off[k] = tot;
+            tot += __popc(m[k]);
+        }
+        if (tot) {
+            uint32_t pos = 0;
+            if (lane == 0) pos = atomicAdd(&p.ctl->qsize[out], tot);
+            pos = __shfl_sync(FULL, pos, 0);
+            LE *q = static_cast<LE *>(p.qlight[out]);
+            const uint32_t lt = lanemask_lt();
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if ((m[k] >> lane) & 1u) {
+                    LE le;
+                    le.beg = nb[k];
+                    le.deg = nd[k];
+                    q[pos + off[k] + __popc(m[k] & lt)] = le;
                 }
             }
         }
-        const uint32_t wins = __ballot_sync(FULL, win);
-        reached += __popc(wins);
-        const bool lw = win && nd > 0 && nd < kHeavyDeg;
-        const uint32_t m = __ballot_sync(FULL, lw);
-        if (m) {   // warp-aggregated append: one atomic per warp (ballot + popc)
-            const uint32_t leader = __ffs(m) - 1;
-            uint32_t pos = 0;
-            if (lane == leader) pos = atomicAdd(&p.ctl->qsize[out], (uint32_t)__popc(m));
-            pos = __shfl_sync(FULL, pos, leader);
-            if (lw) {
-                LE le;
-                le.beg = nb;
-                le.deg = nd;
-                static_cast<LE *>(p.qlight[out])[pos + __popc(m & lanemask_lt())] = le;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (win[k] && nd[k] >= kHeavyDeg) {
+                const unsigned long long old = atomicAdd(&p.ctl->heavy[out], (1ull << 40) | nd[k]);
+                p.qheavy[out][old >> 40] = HeavyEntry{(uint64_t)nb[k], old & kMask40, nd[k], 0u};
             }
-        }
-        if (win && nd >= kHeavyDeg) {
-            const unsigned long long old = atomicAdd(&p.ctl->heavy[out], (1ull << 40) | nd);
-            p.qheavy[out][old >> 40] = HeavyEntry{(uint64_t)nb, old & kMask40, nd, 0u};
         }
     }
 
-    template <int BLOCK>
-    __device__ void expand(const KParams &p, CtaState &cs) {
-        constexpr uint32_t WPB = BLOCK / 32;
-        const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        const uint64_t gw = (uint64_t)cs.lid * WPB + warp;        // get_global_id at warp granularity
-        const uint64_t TW = (uint64_t)cs.M * WPB;                 // get_global_size / 32
-        const uint32_t nl = cs.app_u32[0], nh = cs.app_u32[1];
-        const uint64_t Eh = ((uint64_t)cs.app_u32[3] << 32) | cs.app_u32[2];
-        const uint32_t in = cs.in_sel, out = in ^ 1u;
-        const uint32_t L1 = cs.level + 1;
-        const LE *inq = static_cast<const LE *>(p.qlight[in]);
+    // warp-wide neighbour gather over up to 32 lists (one per lane): prefix sum
+    // of the degrees, then 32*KB edges per iteration, owner found by a shuffle
+    // binary search (warp-level load balancing of short lists)
+    __device__ __forceinline__ uint32_t gather(const KParams &p, OffT beg, uint32_t deg, uint32_t L1, uint32_t out,
+                                               uint32_t *fnext, uint32_t &reached, uint64_t &mfsum) {
+        const uint32_t lane = threadIdx.x & 31;
         const int32_t *__restrict__ col = p.col;
-        uint64_t edges = 0;
-        uint32_t reached = 0;
-
-        // ---- light entries: 32 per warp, Fig. 4 stride over warps
-        for (uint64_t base = gw * 32; base < nl; base += TW * 32) {
-            const uint64_t i = base + lane;
-            OffT beg = 0;
-            uint32_t deg = 0;
-            if (i < nl) {
-                LE e = inq[i];
-                beg = e.beg;
-                deg = e.deg;
-            }
-            const uint32_t incl = warp_incl_scan(deg), excl = incl - deg;
-            const uint32_t total = __shfl_sync(FULL, incl, 31);
-            edges += total;
-            for (uint32_t e0 = 0; e0 < total; e0 += 32) {
-                const uint32_t e = e0 + lane;
+        const uint32_t incl = warp_incl_scan(deg), excl = incl - deg;
+        const uint32_t total = __shfl_sync(FULL, incl, 31);
+        for (uint32_t e0 = 0; e0 < total; e0 += 32 * KB) {
+            int32_t u[KB];
+#pragma unroll
+            for (int k = 0; k < KB; ++k) {
+                const uint32_t e = e0 + 32 * k + lane;
                 uint32_t j = 0;   // owner lane: largest j with excl_j <= e
 #pragma unroll
                 for (uint32_t s = 16; s >= 1; s >>= 1) {
@@ -171,12 +206,36 @@ struct BfsApp {
                 }
                 const OffT b = __shfl_sync(FULL, beg, j);
                 const uint32_t ex = __shfl_sync(FULL, excl, j);
-                const int32_t u = e < total ? __ldg(col + b + (e - ex)) : -1;
-                visit(p, u, L1, out, reached);
+                u[k] = e < total ? __ldg(col + b + (e - ex)) : -1;
             }
+            visit_batch<KB>(p, u, L1, out, fnext, reached, mfsum);
         }
+        return total;
+    }
 
-        // ---- heavy entries: the edge range [0, Eh) split evenly over the M*WPB warps
+    // ---------------------------------------------------------- top-down, queue input
+    __device__ void expand_tdq(const KParams &p, CtaState &cs, uint64_t gw, uint64_t TW, uint32_t *fnext,
+                               uint64_t &edges, uint32_t &reached, uint64_t &mfsum) {
+        const uint32_t lane = threadIdx.x & 31;
+        const uint32_t nl = cs.app_u32[0], nh = cs.app_u32[1];
+        const uint64_t Eh = ((uint64_t)cs.app_u32[3] << 32) | cs.app_u32[2];
+        const uint32_t in = cs.in_sel, out = in ^ 1u;
+        const uint32_t L1 = cs.level + 1;
+        const LE *inq = static_cast<const LE *>(p.qlight[in]);
+        const int32_t *__restrict__ col = p.col;
+        // light entries: 32 per warp, Fig. 4 stride over warps
+        for (uint64_t base = gw * 32; base < nl; base += TW * 32) {
+            const uint64_t i = base + lane;
+            OffT beg = 0;
+            uint32_t deg = 0;
+            if (i < nl) {
+                LE e = inq[i];
+                beg = e.beg;
+                deg = e.deg;
+            }
+            edges += gather(p, beg, deg, L1, out, fnext, reached, mfsum);
+        }
+        // heavy entries: the edge range [0, Eh) split evenly over the M*W warps
         if (nh) {
             const HeavyEntry *hq = p.qheavy[in];
             const uint64_t s0 = Eh * gw / TW, s1 = Eh * (gw + 1) / TW;
@@ -189,40 +248,172 @@ struct BfsApp {
                 uint32_t j = lo;
                 uint64_t hb = ldcg(&hq[j].beg), hp = ldcg(&hq[j].prefix);
                 uint32_t hd = ldcg(&hq[j].deg);
-                for (uint64_t ws = s0; ws < s1; ws += 32) {
+                constexpr uint32_t WIN = 32 * KB;   // <= kHeavyDeg: a window crosses at most one entry end
+                for (uint64_t ws = s0; ws < s1; ws += WIN) {
                     const uint64_t hend = hp + hd;
                     uint64_t hb2 = hb, hp2 = hp;
                     uint32_t hd2 = hd;
-                    if (ws + 32 >= hend && j + 1 < nh) {   // window reaches the next entry
+                    if (ws + WIN >= hend && j + 1 < nh) {   // window reaches the next entry
                         hb2 = ldcg(&hq[j + 1].beg); hp2 = ldcg(&hq[j + 1].prefix); hd2 = ldcg(&hq[j + 1].deg);
                     }
-                    const uint64_t e = ws + lane;
-                    int32_t u = -1;
-                    if (e < s1) u = __ldg(col + (e < hend ? hb + (e - hp) : hb2 + (e - hp2)));
-                    visit(p, u, L1, out, reached);
-                    if (ws + 32 >= hend) { ++j; hb = hb2; hp = hp2; hd = hd2; }
+                    int32_t u[KB];
+#pragma unroll
+                    for (int k = 0; k < KB; ++k) {
+                        const uint64_t e = ws + 32 * k + lane;
+                        u[k] = e < s1 ? __ldg(col + (e < hend ? hb + (e - hp) : hb2 + (e - hp2))) : -1;
+                    }
+                    visit_batch<KB>(p, u, L1, out, fnext, reached, mfsum);
+                    if (ws + WIN >= hend) { ++j; hb = hb2; hp = hp2; hd = hd2; }
                 }
                 edges += s1 - s0;
             }
         }
-        if (lane == 0) {
-            if (edges) atomicAdd(&cs.edges, (unsigned long long)edges);
-            if (reached) atomicAdd(&cs.reached, (unsigned long long)reached);
+    }
+
+    // ---------------------------------------------------------- top-down, bitmap input
+    // lane l owns frontier word base+l and pops one vertex per round
+    __device__ void expand_tdb(const KParams &p, CtaState &cs, uint64_t gw, uint64_t TW, uint32_t *fnext,
+                               uint64_t &edges, uint32_t &reached, uint64_t &mfsum) {
+        const uint32_t lane = threadIdx.x & 31;
+        const uint32_t in = cs.in_sel, out = in ^ 1u;
+        const uint32_t L1 = cs.level + 1;
+        const uint32_t *fcur = p.fbits[cs.level % 3];
+        const OffT *ro = static_cast<const OffT *>(p.ro);
+        const uint64_t nw = ((uint64_t)p.V + 31) / 32;
+        for (uint64_t base = gw * 32; base < nw; base += TW * 32) {
+            const uint64_t wi = base + lane;
+            uint32_t word = wi < nw ? ldcg(fcur + wi) : 0u;
+            while (__any_sync(FULL, word != 0)) {
+                OffT beg = 0;
+                uint32_t deg = 0;
+                if (word) {
+                    const uint32_t b = __ffs(word) - 1;
+                    word &= word - 1;
+                    const uint64_t v = wi * 32 + b;
+                    beg = __ldg(ro + v);
+                    deg = (uint32_t)(__ldg(ro + v + 1) - beg);
+                }
+                edges += gather(p, beg, deg, L1, out, fnext, reached, mfsum);
+            }
         }
     }
 
-    // Fig. 4 between the barriers: reset(out_nodes); per-level statistics
+    // ---------------------------------------------------------- bottom-up
+    // warp per 32-vertex word: each unvisited vertex scans its list (4 per
+    // step) for a parent in the frontier bitmap and stops at the first hit.
+    // The warp owns the visited / next-frontier words, so no atomics.
+    __device__ void expand_bu(const KParams &p, CtaState &cs, uint64_t gw, uint64_t TW, uint64_t &edges,
+                              uint32_t &reached, uint64_t &mfsum) {
+        const uint32_t lane = threadIdx.x & 31;
+        const uint32_t L1 = cs.level + 1;
+        const uint32_t *fcur = p.fbits[cs.level % 3];
+        uint32_t *fnext = p.fbits[L1 % 3];
+        const OffT *ro = static_cast<const OffT *>(p.ro);
+        const int32_t *__restrict__ col = p.col;
+        const uint64_t V = (uint64_t)p.V;
+        const uint64_t nw = (V + 31) / 32;
+        for (uint64_t w = gw; w < nw; w += TW) {
+            const uint32_t vw = ldcg(p.visited + w);
+            if (vw == 0xFFFFFFFFu) continue;
+            const uint64_t v = w * 32 + lane;
+            bool open = v < V && !((vw >> lane) & 1u);
+            OffT b = 0, e = 0;
+            if (open) {
+                b = __ldg(ro + v);
+                e = __ldg(ro + v + 1);
+            }
+            const uint32_t deg = (uint32_t)(e - b);
+            bool found = false;
+            uint32_t scanned = 0;
+            while (open && b < e && !found) {
+                int32_t u[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) u[k] = b + k < e ? __ldg(col + b + k) : -1;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (u[k] >= 0 && ((ldcg(fcur + ((uint32_t)u[k] >> 5)) >> (u[k] & 31)) & 1u)) found = true;
+                const uint32_t n = (uint32_t)min((OffT)4, (OffT)(e - b));
+                scanned += n;
+                b += n;
+            }
+            const uint32_t wins = __ballot_sync(FULL, found);
+            if (found) {
+                p.level_out[v] = (int32_t)L1;
+                mfsum += deg;
+            }
+            edges += scanned;
+            if (wins) {
+                if (lane == 0) {
+                    p.visited[w] = vw | wins;
+                    fnext[w] = wins;
+                }
+                reached += __popc(wins);
+            }
+        }
+    }
+
+    template <int BLOCK>
+    __device__ void expand(const KParams &p, CtaState &cs) {
+        constexpr uint32_t WPB = BLOCK / 32;
+        const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const uint64_t gw = (uint64_t)cs.lid * WPB + warp;        // get_global_id at warp granularity
+        const uint64_t TW = (uint64_t)cs.M * WPB;                 // get_global_size / 32
+        const uint32_t out = cs.in_sel ^ 1u;
+        uint64_t edges = 0, mfsum = 0;
+        uint32_t reached = 0;
+        const uint32_t mode = cs.app_u32[5];
+        uint32_t *fnext = p.dopt ? p.fbits[(cs.level + 1) % 3] : nullptr;
+        if (p.dopt) {   // recycle the bitmap of level L-1 as the next-next frontier
+            uint32_t *fold = p.fbits[(cs.level + 2) % 3];
+            const uint64_t nw = ((uint64_t)p.V + 31) / 32;
+            for (uint64_t i = (uint64_t)cs.lid * BLOCK + threadIdx.x; i < nw; i += (uint64_t)cs.M * BLOCK) fold[i] = 0u;
+        }
+        if (mode == BFS_BU) expand_bu(p, cs, gw, TW, edges, reached, mfsum);
+        else if (mode == BFS_TDB) expand_tdb(p, cs, gw, TW, fnext, edges, reached, mfsum);
+        else expand_tdq(p, cs, gw, TW, fnext, edges, reached, mfsum);
+        // per-warp totals: lane-level partial sums of edges / degrees, warp-uniform reached
+#pragma unroll
+        for (int s = 16; s; s >>= 1) {
+            edges += __shfl_xor_sync(FULL, edges, s);
+            mfsum += __shfl_xor_sync(FULL, mfsum, s);
+        }
+        if (mode != BFS_BU) edges /= 32;   // top-down edge counts are warp-uniform (counted 32x)
+        if (lane == 0) {
+            if (edges) atomicAdd(&cs.edges, (unsigned long long)edges);
+            if (reached) {
+                atomicAdd(&cs.reached, (unsigned long long)reached);
+                atomicAdd(&p.ctl->nf[out], (unsigned long long)reached);
+            }
+            if (mfsum) atomicAdd(&p.ctl->mf[out], (unsigned long long)mfsum);
+        }
+    }
+
+    // Fig. 4 between the barriers: reset(out_nodes); per-level statistics; the
+    // direction of the next level (Beamer: TD->BU if m_f > m_u/alpha, BU->TD if
+    // n_f < V/beta)
     __device__ void serial(const KParams &p, CtaState &cs, uint32_t entry, bool resizing) {
         if (!resizing || entry != ENTRY_AFTER_RB1) return;
         Ctl *c = p.ctl;
         const uint32_t in = cs.in_sel, out = in ^ 1u;        // post-swap selectors
+        const uint32_t prev = c->bmode[out];
         c->qsize[out] = 0;
         c->heavy[out] = 0;
-        const uint32_t n = ld_relaxed32(&c->qsize[in]) + (uint32_t)(ld_relaxed64(&c->heavy[in]) >> 40);
-        if (n) {
+        c->nf[out] = 0;
+        c->mf[out] = 0;
+        const unsigned long long nf = c->nf[in], mf = c->mf[in];
+        c->vis_edges += mf;
+        uint32_t mode = BFS_TDQ;
+        if (p.dopt) {
+            const unsigned long long mu = (unsigned long long)p.E - min((unsigned long long)p.E, c->vis_edges);
+            if (prev == BFS_BU) mode = nf * p.beta < (unsigned long long)p.V ? BFS_TDB : BFS_BU;
+            else mode = mf * p.alpha > mu ? BFS_BU : BFS_TDQ;
+            if (mode == BFS_BU) c->n_bu_levels += 1;
+        }
+        c->bmode[in] = mode;
+        if (nf) {
             const uint32_t L = cs.level + 1;
-            if (L < p.level_cap) p.level_sizes[L] = n;
-            c->frontier_total += n;
+            if (L < p.level_cap) p.level_sizes[L] = (uint32_t)nf;
+            c->frontier_total += nf;
             c->levels += 1;
         }
     }
@@ -232,6 +423,8 @@ struct BfsApp {
 template <typename OffT>
 struct SsspApp {
     __device__ void enter(const KParams &, CtaState &) {}
+    template <int BLOCK>
+    __device__ void between(const KParams &, CtaState &) {}
 
     template <int BLOCK>
     __device__ void init(const KParams &p, CtaState &cs) {
@@ -346,6 +539,8 @@ struct BarrierApp {
     }
     template <int BLOCK>
     __device__ void init(const KParams &, CtaState &) {}
+    template <int BLOCK>
+    __device__ void between(const KParams &, CtaState &) {}
     __device__ bool empty(const KParams &p, CtaState &cs) {
         return (uint64_t)cs.level >= p.iters;
     }

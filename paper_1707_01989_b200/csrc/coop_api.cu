@@ -18,6 +18,7 @@
 
 #include "../../include/coop.h"
 #include "apps.cuh"
+#include "part_app.cuh"
 
 using namespace coop;
 
@@ -80,6 +81,7 @@ static void *pick_block(uint32_t threads) {
 }
 
 static void *select_kernel(uint32_t app, int off64, uint32_t threads) {
+    if (app == APP_PBFS) return off64 ? pick_block<PartBfsApp<int64_t>>(threads) : pick_block<PartBfsApp<uint32_t>>(threads);
     if (app == APP_BFS) return off64 ? pick_block<BfsApp<int64_t>>(threads) : pick_block<BfsApp<uint32_t>>(threads);
     if (app == APP_SSSP) return off64 ? pick_block<SsspApp<int64_t>>(threads) : pick_block<SsspApp<uint32_t>>(threads);
     switch (threads) {
@@ -126,19 +128,21 @@ struct DevBuf {
 
 struct Scratch {
     int device = -1;
-    DevBuf ctl, mb, visited, qlev, ql0, ql1, qh0, qh1, stamp, mtrace, lsizes, events, script, wmax;
+    DevBuf ctl, mb, visited, qlev, ql0, ql1, qh0, qh1, stamp, mtrace, lsizes, events, script, wmax, fb0, fb1, fb2;
     DevBuf h_ro, h_col, h_w, h_out;   // end-to-end (host-pointer) calls
     Ctl *host_ctl = nullptr;          // pinned staging
     std::mutex mu;
 };
 
-static Scratch g_scratch[16];
+constexpr uint32_t kWorkspaces = 8;
+static Scratch g_scratch[16][kWorkspaces];
 
-static coop_status get_scratch(Scratch **out) {
+static coop_status get_scratch(Scratch **out, uint32_t ws) {
     int dev = 0;
     CUDA_TRY(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 16) return fail(COOP_ERR_INVALID_ARG, "device %d out of range", dev);
-    Scratch *s = &g_scratch[dev];
+    if (ws >= kWorkspaces) return fail(COOP_ERR_INVALID_ARG, "workspace %u out of range [0, %u)", ws, kWorkspaces);
+    Scratch *s = &g_scratch[dev][ws];
     if (!s->host_ctl) CUDA_TRY(cudaHostAlloc((void **)&s->host_ctl, sizeof(Ctl), cudaHostAllocDefault));
     s->device = dev;
     *out = s;
@@ -184,6 +188,7 @@ extern "C" coop_status coop_device_query(int device, uint32_t threads_per_wg, co
 struct RunReq {
     uint32_t app;
     const coop_csr *g;
+    const coop_part *part;      // APP_PBFS
     int64_t source;
     void *out;
     const coop_opts *opts;
@@ -208,6 +213,7 @@ static coop_status fill_stats(const Ctl &c, const KParams &kp, coop_stats *st, c
     st->n_wgs = kp.P;
     st->tasks_posted = c.tasks_posted;
     st->tasks_completed = c.tasks_completed;
+    st->bottom_up_levels = c.n_bu_levels;
     if (st->m_trace && st->m_trace_cap) {
         uint32_t n = std::min(st->m_trace_cap, std::min(c.episode, kp.m_trace_cap));
         if (n) CUDA_TRY(cudaMemcpyAsync(st->m_trace, kp.m_trace, n * 4, cudaMemcpyDeviceToHost, stream));
@@ -260,14 +266,56 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
     static const coop_opts kDefault = {};
     const coop_opts &o = r.opts ? *r.opts : kDefault;
     Scratch *s = nullptr;
-    coop_status st = get_scratch(&s);
+    coop_status st = get_scratch(&s, o.workspace);
     if (st != COOP_OK) return st;
     KParams kp;
     memset(&kp, 0, sizeof kp);
     kp.app = r.app;
     const uint32_t threads = o.threads_per_wg ? o.threads_per_wg : (r.app == APP_BARRIER ? 128u : 512u);
     int off64 = 0;
-    if (r.app != APP_BARRIER) {
+    if (r.app == APP_PBFS) {
+        const coop_part *pt = r.part;
+        if (!pt) return fail(COOP_ERR_INVALID_ARG, "part is NULL");
+        if (pt->num_vertices < 1 || pt->num_vertices > (int64_t)INT32_MAX)
+            return fail(COOP_ERR_INVALID_ARG, "num_vertices out of range");
+        if (pt->nranks < 1 || pt->nranks > COOP_MAX_RANKS || pt->rank < 0 || pt->rank >= pt->nranks)
+            return fail(COOP_ERR_INVALID_ARG, "rank %d / nranks %d invalid", pt->rank, pt->nranks);
+        if (pt->v_begin < 0 || pt->v_end > pt->num_vertices || pt->v_begin > pt->v_end || (pt->v_begin & 31))
+            return fail(COOP_ERR_INVALID_ARG, "owned range [%lld, %lld) invalid (v_begin %% 32 == 0 required)",
+                        (long long)pt->v_begin, (long long)pt->v_end);
+        if (pt->offset_bits != 32 && pt->offset_bits != 64) return fail(COOP_ERR_INVALID_ARG, "offset_bits");
+        if (!pt->row_offsets || (!pt->col_local && pt->num_edges > 0)) return fail(COOP_ERR_INVALID_ARG, "CSR NULL");
+        if (pt->num_hubs && (!pt->hub_ids || !pt->hub_prefix || !pt->hub_degree))
+            return fail(COOP_ERR_INVALID_ARG, "hub arrays NULL");
+        for (int q = 0; q < pt->nranks; ++q)
+            if (!pt->frontier[q][0] || !pt->frontier[q][1] || !pt->flags[q])
+                return fail(COOP_ERR_INVALID_ARG, "exchange buffers of rank %d NULL", q);
+        if (r.source < 0 || r.source >= pt->num_vertices) return fail(COOP_ERR_INVALID_ARG, "source out of range");
+        if (!r.out) return fail(COOP_ERR_INVALID_ARG, "output buffer is NULL");
+        off64 = pt->offset_bits == 64;
+        kp.V = pt->num_vertices;
+        kp.ro = pt->row_offsets;
+        kp.off64 = off64;
+        kp.col = pt->col_local;
+        kp.source = r.source;
+        kp.E = pt->num_edges;
+        kp.level_out = static_cast<int32_t *>(r.out);
+        PartParams &pp = kp.part;
+        pp.vb = pt->v_begin;
+        pp.ve = pt->v_end;
+        pp.rank = pt->rank;
+        pp.nranks = pt->nranks;
+        pp.seq = pt->seq;
+        pp.nhub = pt->num_hubs;
+        pp.hub_deg = pt->hub_degree;
+        pp.hub_ids = pt->hub_ids;
+        pp.hub_prefix = reinterpret_cast<const unsigned long long *>(pt->hub_prefix);
+        for (int q = 0; q < pt->nranks; ++q) {
+            pp.F[q][0] = pt->frontier[q][0];
+            pp.F[q][1] = pt->frontier[q][1];
+            pp.flags[q] = reinterpret_cast<unsigned long long *>(pt->flags[q]);
+        }
+    } else if (r.app != APP_BARRIER) {
         const coop_csr *g = r.g;
         if (!g) return fail(COOP_ERR_INVALID_ARG, "graph is NULL");
         if (g->num_vertices < 1 || g->num_vertices > (int64_t)INT32_MAX)
@@ -289,6 +337,7 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
         kp.col = g->col_idx;
         kp.w = g->weights;
         kp.source = r.source;
+        kp.E = g->num_edges;
         if (r.app == APP_BFS) kp.level_out = static_cast<int32_t *>(r.out);
         else kp.dist_out = static_cast<uint32_t *>(r.out);
     }
@@ -310,7 +359,7 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
     uint32_t M0 = o.init_wgs ? o.init_wgs : P;
     if (M0 < 1 || M0 > P) return fail(COOP_ERR_INVALID_ARG, "init_wgs %u not in [1, %u]", M0, P);
     if (plain) M0 = P;
-    const uint32_t bpl = o.barriers_per_level ? o.barriers_per_level : 1;
+    const uint32_t bpl = r.app == APP_PBFS ? 2u : (o.barriers_per_level ? o.barriers_per_level : 1);
     if (bpl != 1 && bpl != 2) return fail(COOP_ERR_INVALID_ARG, "barriers_per_level must be 1 or 2");
     if (o.policy == COOP_POLICY_SCRIPTED && o.script_len && !o.script) return fail(COOP_ERR_INVALID_ARG, "script NULL");
     if (o.resize_prob < 0 || o.resize_prob > 1) return fail(COOP_ERR_INVALID_ARG, "resize_prob not in [0,1]");
@@ -335,7 +384,7 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
 
     // ---- scratch
     const uint64_t V = r.app == APP_BARRIER ? 0 : (uint64_t)kp.V;
-    const uint64_t E = r.app == APP_BARRIER ? 0 : (uint64_t)r.g->num_edges;
+    const uint64_t E = (r.app == APP_BARRIER || r.app == APP_PBFS) ? 0 : (uint64_t)r.g->num_edges;
     CUDA_TRY(s->ctl.ensure(sizeof(Ctl)));
     CUDA_TRY(s->mb.ensure(sizeof(Mailbox) * P));
     CUDA_TRY(s->stamp.ensure(4ull * kMaxCtas));
@@ -352,8 +401,24 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
         CUDA_TRY(s->qh0.ensure(sizeof(HeavyEntry) * nh));
         CUDA_TRY(s->qh1.ensure(sizeof(HeavyEntry) * nh));
         kp.visited = static_cast<uint32_t *>(s->visited.p);
+        if (o.flags & COOP_FLAG_DIROPT) {
+            const size_t fbytes = 4 * ((V + 31) / 32);
+            CUDA_TRY(s->fb0.ensure(fbytes));
+            CUDA_TRY(s->fb1.ensure(fbytes));
+            CUDA_TRY(s->fb2.ensure(fbytes));
+            kp.fbits[0] = static_cast<uint32_t *>(s->fb0.p);
+            kp.fbits[1] = static_cast<uint32_t *>(s->fb1.p);
+            kp.fbits[2] = static_cast<uint32_t *>(s->fb2.p);
+            kp.dopt = 1;
+        }
+        kp.alpha = 14;
+        kp.beta = 24;
         kp.qheavy[0] = static_cast<HeavyEntry *>(s->qh0.p);
         kp.qheavy[1] = static_cast<HeavyEntry *>(s->qh1.p);
+    } else if (r.app == APP_PBFS) {
+        const uint64_t nown = (uint64_t)(kp.part.ve - kp.part.vb);
+        CUDA_TRY(s->visited.ensure(4 * ((nown + 31) / 32) + 4));
+        kp.visited = static_cast<uint32_t *>(s->visited.p);
     } else if (r.app == APP_SSSP) {
         CUDA_TRY(s->qlev.ensure(4 * V));
         CUDA_TRY(s->ql0.ensure(4 * V));
@@ -462,7 +527,7 @@ static coop_status finish(Prepared &pr, coop_stats *stats) {
 static coop_status run_blocking(const RunReq &r) {
     Prepared pr;
     Scratch *s = nullptr;
-    coop_status st = get_scratch(&s);
+    coop_status st = get_scratch(&s, r.opts ? r.opts->workspace : 0);
     if (st != COOP_OK) return st;
     SCRATCH_LOCK(s);
     st = prepare(r, &pr);
@@ -474,13 +539,13 @@ static coop_status run_blocking(const RunReq &r) {
 
 extern "C" coop_status coop_bfs(const coop_csr *g, int64_t source, int32_t *levels_out, const coop_opts *opts,
                                 coop_stats *stats) {
-    RunReq r = {APP_BFS, g, source, levels_out, opts, stats, 0, nullptr, false};
+    RunReq r = {APP_BFS, g, nullptr, source, levels_out, opts, stats, 0, nullptr, false};
     return run_blocking(r);
 }
 
 extern "C" coop_status coop_sssp(const coop_csr *g, int64_t source, uint32_t *dist_out, const coop_opts *opts,
                                  coop_stats *stats) {
-    RunReq r = {APP_SSSP, g, source, dist_out, opts, stats, 0, nullptr, false};
+    RunReq r = {APP_SSSP, g, nullptr, source, dist_out, opts, stats, 0, nullptr, false};
     return run_blocking(r);
 }
 
@@ -491,7 +556,7 @@ static coop_status run_host(uint32_t app, int64_t V, const void *ro, int32_t off
     if (V < 1 || !ro || !out) return fail(COOP_ERR_INVALID_ARG, "bad host arguments");
     if (offset_bits != 32 && offset_bits != 64) return fail(COOP_ERR_INVALID_ARG, "offset_bits must be 32 or 64");
     Scratch *s = nullptr;
-    coop_status st = get_scratch(&s);
+    coop_status st = get_scratch(&s, opts ? opts->workspace : 0);
     if (st != COOP_OK) return st;
     const size_t ob = offset_bits / 8;
     uint64_t E = 0;
@@ -512,7 +577,7 @@ static coop_status run_host(uint32_t app, int64_t V, const void *ro, int32_t off
     }
     coop_csr g = {V, (int64_t)E, s->h_ro.p, offset_bits, static_cast<const int32_t *>(s->h_col.p),
                   app == APP_SSSP ? static_cast<const uint32_t *>(s->h_w.p) : nullptr, max_weight};
-    RunReq r = {app, &g, source, s->h_out.p, opts, stats, 0, nullptr, false};
+    RunReq r = {app, &g, nullptr, source, s->h_out.p, opts, stats, 0, nullptr, false};
     st = run_blocking(r);
     if (st != COOP_OK) return st;
     CUDA_TRY(cudaMemcpyAsync(out, s->h_out.p, 4 * V, cudaMemcpyDeviceToHost, stream));
@@ -553,10 +618,10 @@ extern "C" coop_status coop_barrier_bench(uint32_t n_ctas, uint32_t threads, uin
     o.timeout_ns = 60000000000ull;
     coop_stats st = {};
     Scratch *s = nullptr;
-    coop_status rc = get_scratch(&s);
+    coop_status rc = get_scratch(&s, 0);
     if (rc != COOP_OK) return rc;
     SCRATCH_LOCK(s);
-    RunReq r = {APP_BARRIER, nullptr, 0, nullptr, &o, &st, iters, nullptr, false};
+    RunReq r = {APP_BARRIER, nullptr, nullptr, 0, nullptr, &o, &st, iters, nullptr, false};
     Prepared pr;
     rc = prepare(r, &pr);
     if (rc != COOP_OK) return rc;
@@ -605,40 +670,102 @@ struct coop_handle {
     uint64_t next_task_id = 0;
 };
 
+static coop_status launch_handle(const RunReq &r0, const coop_opts *opts, bool channel, coop_handle **handle) {
+    coop_handle *h = new (std::nothrow) coop_handle();
+    if (!h) return fail(COOP_ERR_INVALID_ARG, "out of host memory");
+    if (channel) {
+        cudaError_t e = cudaHostAlloc((void **)&h->hc, sizeof(HostChannel), cudaHostAllocMapped);
+        if (e != cudaSuccess) { delete h; return fail(COOP_ERR_CUDA, "cudaHostAlloc: %s", cudaGetErrorString(e)); }
+        memset((void *)h->hc, 0, sizeof(HostChannel));
+        e = cudaHostGetDevicePointer((void **)&h->dc, h->hc, 0);
+        if (e != cudaSuccess) { cudaFreeHost(h->hc); delete h; return fail(COOP_ERR_CUDA, "cudaHostGetDevicePointer"); }
+    }
+    RunReq r = r0;
+    r.host = h->dc;
+    Scratch *s = nullptr;
+    coop_status st = get_scratch(&s, opts ? opts->workspace : 0);
+    if (st == COOP_OK) {
+        if (!s->mu.try_lock()) {   // held until coop_wait/destroy: the scratch belongs to this launch
+            st = fail(COOP_ERR_BUSY, "device scratch in use by another call or an un-waited handle");
+        } else {
+            st = prepare(r, &h->pr);
+            if (st == COOP_OK) st = launch(h->pr);
+            if (st != COOP_OK) s->mu.unlock();
+        }
+    }
+    if (st != COOP_OK) {
+        if (h->hc) cudaFreeHost(h->hc);
+        delete h;
+        return st;
+    }
+    *handle = h;
+    return COOP_OK;
+}
+
 extern "C" coop_status coop_launch(int kind, const coop_csr *g, int64_t source, void *out, const coop_opts *opts,
                                    coop_handle **handle) {
     if (!handle || !opts) return fail(COOP_ERR_INVALID_ARG, "handle/opts NULL");
     if (kind != 0 && kind != 1) return fail(COOP_ERR_INVALID_ARG, "kind must be 0 (BFS) or 1 (SSSP)");
     if (opts->policy != COOP_POLICY_SCHEDULER || opts->barrier_mode == COOP_BARRIER_PLAIN)
         return fail(COOP_ERR_INVALID_ARG, "coop_launch needs policy SCHEDULER and a cooperative barrier");
-    coop_handle *h = new (std::nothrow) coop_handle();
-    if (!h) return fail(COOP_ERR_INVALID_ARG, "out of host memory");
-    cudaError_t e = cudaHostAlloc((void **)&h->hc, sizeof(HostChannel), cudaHostAllocMapped);
-    if (e != cudaSuccess) { delete h; return fail(COOP_ERR_CUDA, "cudaHostAlloc: %s", cudaGetErrorString(e)); }
-    memset((void *)h->hc, 0, sizeof(HostChannel));
-    e = cudaHostGetDevicePointer((void **)&h->dc, h->hc, 0);
-    if (e != cudaSuccess) { cudaFreeHost(h->hc); delete h; return fail(COOP_ERR_CUDA, "cudaHostGetDevicePointer"); }
-    RunReq r = {kind == 0 ? APP_BFS : APP_SSSP, g, source, out, opts, nullptr, 0, h->dc, true};
-    Scratch *s = nullptr;
-    coop_status st = get_scratch(&s);
-    if (st == COOP_OK) {
-        if (!s->mu.try_lock()) {   // held until coop_wait/destroy: the scratch belongs to this launch
-            st = fail(COOP_ERR_BUSY, "device scratch in use by another call or an un-waited handle");
-            cudaFreeHost(h->hc);
-            delete h;
-            return st;
-        }
-        st = prepare(r, &h->pr);
-        if (st == COOP_OK) st = launch(h->pr);
-        if (st != COOP_OK) s->mu.unlock();
-    }
-    if (st != COOP_OK) { cudaFreeHost(h->hc); delete h; return st; }
-    *handle = h;
+    RunReq r = {kind == 0 ? APP_BFS : APP_SSSP, g, nullptr, source, out, opts, nullptr, 0, nullptr, true};
+    return launch_handle(r, opts, true, handle);
+}
+
+// ------------------------------------------------------------------ partitioned BFS
+extern "C" coop_status coop_bfs_part(const coop_part *part, int64_t source, int32_t *levels_owned_out,
+                                     const coop_opts *opts, coop_stats *stats) {
+    RunReq r = {APP_PBFS, nullptr, part, source, levels_owned_out, opts, stats, 0, nullptr, false};
+    return run_blocking(r);
+}
+
+extern "C" coop_status coop_bfs_part_launch(const coop_part *part, int64_t source, int32_t *levels_owned_out,
+                                            const coop_opts *opts, coop_handle **handle) {
+    if (!handle) return fail(COOP_ERR_INVALID_ARG, "handle NULL");
+    RunReq r = {APP_PBFS, nullptr, part, source, levels_owned_out, opts, nullptr, 0, nullptr, true};
+    const bool chan = opts && opts->policy == COOP_POLICY_SCHEDULER;
+    return launch_handle(r, opts, chan, handle);
+}
+
+extern "C" coop_status coop_exchange_alloc(uint64_t bytes, void **dptr) {
+    if (!dptr || !bytes) return fail(COOP_ERR_INVALID_ARG, "bad arguments");
+    CUDA_TRY(cudaMalloc(dptr, bytes));
+    CUDA_TRY(cudaMemset(*dptr, 0, bytes));
+    return COOP_OK;
+}
+
+extern "C" coop_status coop_exchange_free(void *dptr) {
+    if (!dptr) return fail(COOP_ERR_INVALID_ARG, "NULL argument");
+    CUDA_TRY(cudaFree(dptr));
+    return COOP_OK;
+}
+
+extern "C" coop_status coop_ipc_get_handle(const void *dptr, void *handle64) {
+    if (!dptr || !handle64) return fail(COOP_ERR_INVALID_ARG, "NULL argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, const_cast<void *>(dptr)));
+    memcpy(handle64, &h, sizeof h);
+    return COOP_OK;
+}
+
+extern "C" coop_status coop_ipc_open(const void *handle64, void **dptr) {
+    if (!dptr || !handle64) return fail(COOP_ERR_INVALID_ARG, "NULL argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof h);
+    CUDA_TRY(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return COOP_OK;
+}
+
+extern "C" coop_status coop_ipc_close(void *dptr) {
+    if (!dptr) return fail(COOP_ERR_INVALID_ARG, "NULL argument");
+    CUDA_TRY(cudaIpcCloseMemHandle(dptr));
     return COOP_OK;
 }
 
 static coop_status post(coop_handle *h, uint32_t kind, uint32_t a, uint32_t b, uint64_t c) {
     if (h->waited) return fail(COOP_ERR_BUSY, "handle already waited");
+    if (!h->hc) return fail(COOP_ERR_BUSY, "handle has no host channel (policy is not SCHEDULER)");
     // single-slot channel: wait until the scheduler CTA consumed the previous packet
     for (long spins = 0; h->hc->ack != h->seq; ++spins) {
         if (h->hc->done_mirror) return fail(COOP_ERR_BUSY, "kernel already terminated");
@@ -678,12 +805,14 @@ extern "C" coop_status coop_grant(coop_handle *h, uint32_t forks) {
 
 extern "C" coop_status coop_query(coop_handle *h, uint32_t *W) {
     if (!h || !W) return fail(COOP_ERR_INVALID_ARG, "NULL argument");
+    if (!h->hc) return fail(COOP_ERR_BUSY, "handle has no host channel");
     *W = h->hc->demand_mirror;
     return COOP_OK;
 }
 
 extern "C" coop_status coop_current_m(coop_handle *h, uint32_t *M) {
     if (!h || !M) return fail(COOP_ERR_INVALID_ARG, "NULL argument");
+    if (!h->hc) return fail(COOP_ERR_BUSY, "handle has no host channel");
     *M = h->hc->cur_m;
     return COOP_OK;
 }
@@ -703,6 +832,6 @@ extern "C" void coop_destroy(coop_handle *h) {
         cudaStreamSynchronize(h->pr.stream);
         h->pr.s->mu.unlock();
     }
-    cudaFreeHost(h->hc);
+    if (h->hc) cudaFreeHost(h->hc);
     delete h;
 }

@@ -17,7 +17,11 @@ enum : uint32_t { ACT_CONT = 0, ACT_KILLED = 1, ACT_DONE = 2, ACT_ABORT = 3, ACT
 enum : uint32_t { ENTRY_START = 0, ENTRY_AFTER_RB1 = 1, ENTRY_AFTER_RB2 = 2 };
 // error codes written to Ctl::err (host maps to coop_status)
 enum : uint32_t { DERR_NONE = 0, DERR_TIMEOUT = 1, DERR_INVARIANT = 2, DERR_OVERFLOW = 3 };
-enum : uint32_t { APP_BFS = 0, APP_SSSP = 1, APP_BARRIER = 2 };
+enum : uint32_t { APP_BFS = 0, APP_SSSP = 1, APP_BARRIER = 2, APP_PBFS = 3 };
+constexpr int kMaxRanks = 8;                         // partitioned BFS: GPUs of one NVSwitch node
+// BFS level modes (direction optimisation): top-down over the frontier queue,
+// top-down over the frontier bitmap (after a bottom-up level), bottom-up
+enum : uint32_t { BFS_TDQ = 0, BFS_TDB = 1, BFS_BU = 2 };
 
 // Transmit struct: the transmit-annotated state of Fig. 4 (level, in_nodes,
 // out_nodes) plus what a forked CTA needs to join (reading R7).
@@ -88,6 +92,33 @@ struct __align__(128) Ctl {
     // host-mapped channel mirror: last host sequence numbers consumed
     uint32_t host_seq_seen;
     uint32_t pad_h[31];
+    // BFS frontier accounting per level parity (next frontier of the level being expanded)
+    unsigned long long nf[2];          // vertices discovered
+    unsigned long long mf[2];          // sum of their degrees
+    unsigned long long vis_edges;      // sum of degrees of every vertex discovered so far
+    uint32_t bmode[2];                 // BFS_* mode of the level that reads parity p
+    uint32_t n_bu_levels;              // statistics: bottom-up levels executed
+    uint32_t pad_b[19];
+    // partitioned BFS
+    unsigned long long pcount[2];      // owned vertices discovered per level parity (this rank)
+    unsigned long long gcount;         // vertices in the global frontier of the current level (all ranks)
+    unsigned long long xwait_ns;       // time spent in the cross-GPU flag exchange
+    uint32_t pad_p[24];
+};
+
+// Partitioned BFS (1-D vertex partition).  Frontier bitmaps and
+// flag blocks of every rank are device-visible here (own memory, or peer
+// memory mapped through CUDA IPC over NVLink).
+struct PartParams {
+    int64_t vb, ve;                    // owned vertices [vb, ve), vb % 32 == 0
+    int32_t rank, nranks;
+    uint32_t seq;                      // call sequence number, identical on every rank
+    uint32_t nhub;                     // static hubs (local degree >= hub_deg)
+    uint32_t hub_deg;
+    const uint32_t *hub_ids;
+    const unsigned long long *hub_prefix;        // nhub + 1 local-edge prefix over the hubs
+    uint32_t *F[kMaxRanks][2];         // F[q][b]: rank q's copy of global frontier bitmap b
+    unsigned long long *flags[kMaxRanks];        // rank q's flag block [kMaxRanks][2]
 };
 
 // Host -> GPU packet channel (host-mapped pinned memory; the paper's SVM atomics).
@@ -121,6 +152,7 @@ struct KParams {
     void *qlight[2];            // BFS light entries / SSSP vertex ids
     HeavyEntry *qheavy[2];
     uint32_t *stamp;            // barrier bench message passing [kMaxCtas]
+    uint32_t *fbits[3];         // BFS direction optimisation: frontier bitmaps of levels L, L+1, L+2 (mod 3)
     uint32_t *m_trace; uint32_t m_trace_cap;
     uint32_t *level_sizes; uint32_t level_cap;
     TaskEventDev *events; uint32_t events_cap;
@@ -139,6 +171,10 @@ struct KParams {
     uint32_t resize_thresh;     // resize_prob * 2^32
     uint64_t timeout_ns;
     uint64_t iters;             // barrier bench
+    int64_t E;                  // directed edges
+    uint32_t dopt;              // BFS: direction-optimising (COOP_FLAG_DIROPT)
+    PartParams part;            // APP_PBFS
+    uint32_t alpha, beta;       // Beamer's switch thresholds (m_f > m_u/alpha -> BU; n_f < V/beta -> TD)
     // periodic task generator
     uint32_t task_wgs, task_blocks, task_max;
     uint64_t task_block_ns, task_period_ns, task_first_ns;

@@ -62,6 +62,14 @@ __device__ __forceinline__ void st_release64(unsigned long long *p, unsigned lon
 __device__ __forceinline__ void st_relaxed32(uint32_t *p, uint32_t v) {
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long ld_acquire_sys64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t ld_sys32(const volatile uint32_t *p) {
     uint32_t v;
     asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -401,6 +409,7 @@ __device__ uint32_t run_body(const KParams &p, CtaState &cs, App &app, uint32_t 
             if (r != ACT_CONT) return r;
         }
         skip_to_rb1 = false;
+        app.template between<BLOCK>(p, cs);                   // CTA work between Fig. 4's two barriers
         if (threadIdx.x == 0) cs.level += 1;                  // reset(out_nodes) done in serial; level++
         if (p.bpl == 2) {
             r = barrier(p, cs, app, true, ENTRY_AFTER_RB2);   // resizing_global_barrier() #2

@@ -1,0 +1,254 @@
+// part_app.cuh -- 1-D vertex-partitioned cooperative BFS (BASELINE.json
+// configs[4]).  Not in the paper (single iGPU): the paper's
+// cooperative kernel runs unchanged on every GPU, and the per-level frontier
+// exchange is fused into it as a direct NVLink peer-memory all-gather.
+//
+// Rank p owns vertices [vb, ve) (vb a multiple of 32) and stores every edge
+// (u, v) with v owned, indexed by the global source u (row_offsets over all V,
+// col = v - vb).  Per level L (two resizing barriers, Fig. 4):
+//   expand : read the global frontier bitmap F[L&1] (own copy), scan the
+//            local rows of its vertices, claim owned targets in the local
+//            visited bitmap, write level L+1 and set their bit in the own
+//            slice of F[(L+1)&1]
+//   RB1    : resizing barrier
+//   between: clear the consumed F[L&1]; store the own slice of F[(L+1)&1]
+//            into every peer's copy (NVLink stores, 16 B each)
+//   RB2    : resizing barrier whose serial section is also the cross-GPU
+//            barrier: fence.sys, then publish (epoch, discovered count) into
+//            every peer's flag block and wait for every peer's; the sum is
+//            the size of the next global frontier (0 = terminate everywhere)
+// Static hubs (local degree >= hub_deg) are processed edge-balanced over
+// all warps so one hub cannot stall a level.
+#pragma once
+#include "apps.cuh"
+
+namespace coop {
+
+template <typename OffT>
+struct PartBfsApp {
+    static constexpr int KB = 4;
+
+    __device__ void enter(const KParams &, CtaState &) {}
+
+    template <int BLOCK>
+    __device__ void init(const KParams &p, CtaState &cs) {
+        const PartParams &pp = p.part;
+        const uint64_t tid = (uint64_t)cs.lid * BLOCK + threadIdx.x;
+        const uint64_t nth = (uint64_t)cs.M * BLOCK;
+        const int64_t s = p.source;
+        const uint64_t nown = (uint64_t)(pp.ve - pp.vb);
+        for (uint64_t i = tid; i < nown; i += nth) p.level_out[i] = (int64_t)i + pp.vb == s ? 0 : -1;
+        const uint64_t nlw = (nown + 31) / 32;
+        const bool own_s = s >= pp.vb && s < pp.ve;
+        for (uint64_t i = tid; i < nlw; i += nth)
+            p.visited[i] = (own_s && i == (uint64_t)((s - pp.vb) >> 5)) ? (1u << ((s - pp.vb) & 31)) : 0u;
+        const uint64_t nw = ((uint64_t)p.V + 31) / 32;
+        uint32_t *F0 = pp.F[pp.rank][0], *F1 = pp.F[pp.rank][1];
+        for (uint64_t i = tid; i < nw; i += nth) {     // every rank knows the source (level 0 frontier)
+            F0[i] = i == (uint64_t)(s >> 5) ? (1u << (s & 31)) : 0u;
+            F1[i] = 0u;
+        }
+        if (cs.lid == 0 && threadIdx.x == 0) {
+            p.ctl->gcount = 1;
+            p.ctl->frontier_total = 1;
+            p.ctl->levels = 1;
+            if (p.level_cap) p.level_sizes[0] = 1;
+            if (own_s) cs.reached += 1;
+        }
+    }
+
+    __device__ bool empty(const KParams &p, CtaState &cs) {
+        if (threadIdx.x == 0) cs.app_u32[0] = ld_relaxed64(&p.ctl->gcount) ? 1u : 0u;
+        __syncthreads();
+        return cs.app_u32[0] == 0;
+    }
+
+    // claim owned targets t (local ids) -- warp-collective, batch of K per lane
+    __device__ __forceinline__ void claim(const KParams &p, const int32_t (&t)[KB], uint32_t L1, uint32_t *fnext,
+                                          uint32_t &won) {
+        uint32_t *vis = p.visited;
+        uint32_t cur[KB];
+#pragma unroll
+        for (int k = 0; k < KB; ++k) cur[k] = t[k] >= 0 ? vis[(uint32_t)t[k] >> 5] : 0xFFFFFFFFu;
+#pragma unroll
+        for (int k = 0; k < KB; ++k) {
+            if (t[k] < 0) continue;
+            const uint32_t bit = 1u << (t[k] & 31);
+            if ((cur[k] & bit) || (atomicOr(vis + ((uint32_t)t[k] >> 5), bit) & bit)) continue;
+            p.level_out[t[k]] = (int32_t)L1;
+            const uint64_t g = (uint64_t)p.part.vb + (uint32_t)t[k];
+            atomicOr(fnext + (g >> 5), 1u << (g & 31));
+            ++won;
+        }
+    }
+
+    template <int BLOCK>
+    __device__ void expand(const KParams &p, CtaState &cs) {
+        constexpr uint32_t WPB = BLOCK / 32;
+        const PartParams &pp = p.part;
+        const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const uint64_t gw = (uint64_t)cs.lid * WPB + warp, TW = (uint64_t)cs.M * WPB;
+        const uint32_t L = cs.level, L1 = L + 1;
+        const uint32_t *fcur = pp.F[pp.rank][L & 1];
+        uint32_t *fnext = pp.F[pp.rank][L1 & 1];
+        const OffT *ro = static_cast<const OffT *>(p.ro);
+        const int32_t *__restrict__ col = p.col;
+        const uint64_t nw = ((uint64_t)p.V + 31) / 32;
+        uint64_t edges = 0;
+        uint32_t won = 0;
+        // ---- frontier vertices from the bitmap, lane l owns word base+l
+        for (uint64_t base = gw * 32; base < nw; base += TW * 32) {
+            const uint64_t wi = base + lane;
+            uint32_t word = wi < nw ? ldcg(fcur + wi) : 0u;
+            while (__any_sync(FULL, word != 0)) {
+                OffT beg = 0;
+                uint32_t deg = 0;
+                if (word) {
+                    const uint32_t b = __ffs(word) - 1;
+                    word &= word - 1;
+                    const uint64_t u = wi * 32 + b;
+                    beg = __ldg(ro + u);
+                    deg = (uint32_t)(__ldg(ro + u + 1) - beg);
+                    if (pp.nhub && deg >= pp.hub_deg) deg = 0;   // static hub: edge-balanced pass below
+                }
+                const uint32_t incl = warp_incl_scan(deg), excl = incl - deg;
+                const uint32_t total = __shfl_sync(FULL, incl, 31);
+                edges += total;
+                for (uint32_t e0 = 0; e0 < total; e0 += 32 * KB) {
+                    int32_t t[KB];
+#pragma unroll
+                    for (int k = 0; k < KB; ++k) {
+                        const uint32_t e = e0 + 32 * k + lane;
+                        uint32_t j = 0;
+#pragma unroll
+                        for (uint32_t s = 16; s >= 1; s >>= 1) {
+                            const uint32_t c = j + s;
+                            const uint32_t ex = __shfl_sync(FULL, excl, c);
+                            if (ex <= e) j = c;
+                        }
+                        const OffT b = __shfl_sync(FULL, beg, j);
+                        const uint32_t ex = __shfl_sync(FULL, excl, j);
+                        t[k] = e < total ? __ldg(col + b + (e - ex)) : -1;
+                    }
+                    claim(p, t, L1, fnext, won);
+                }
+            }
+        }
+        // ---- static hubs: hub edge space [0, Eh) split evenly over the warps;
+        //      a hub segment is read only if the hub is in the frontier
+        if (pp.nhub) {
+            const uint64_t Eh = pp.hub_prefix[pp.nhub];
+            const uint64_t s0 = Eh * gw / TW, s1 = Eh * (gw + 1) / TW;
+            if (s0 < s1) {
+                uint32_t lo = 0, hi = pp.nhub - 1;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi + 1) >> 1;
+                    if (__ldg(pp.hub_prefix + mid) <= s0) lo = mid; else hi = mid - 1;
+                }
+                for (uint32_t h = lo; h < pp.nhub; ++h) {
+                    const uint64_t hp = __ldg(pp.hub_prefix + h), hq = __ldg(pp.hub_prefix + h + 1);
+                    if (hp >= s1) break;
+                    const uint32_t hub = __ldg(pp.hub_ids + h);
+                    if (!((ldcg(fcur + (hub >> 5)) >> (hub & 31)) & 1u)) continue;
+                    const uint64_t a = hp > s0 ? hp : s0, z = hq < s1 ? hq : s1;
+                    const OffT rb = __ldg(ro + hub);
+                    edges += z - a;
+                    for (uint64_t ws = a; ws < z; ws += 32 * KB) {
+                        int32_t t[KB];
+#pragma unroll
+                        for (int k = 0; k < KB; ++k) {
+                            const uint64_t e = ws + 32 * k + lane;
+                            t[k] = e < z ? __ldg(col + rb + (e - hp)) : -1;
+                        }
+                        claim(p, t, L1, fnext, won);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int s = 16; s; s >>= 1) won += __shfl_xor_sync(FULL, won, s);
+        if (lane == 0) {   // edges is warp-uniform, won was per lane
+            if (edges) atomicAdd(&cs.edges, (unsigned long long)edges);
+            if (won) {
+                atomicAdd(&cs.reached, (unsigned long long)won);
+                atomicAdd(&p.ctl->pcount[L1 & 1], (unsigned long long)won);
+            }
+        }
+    }
+
+    // between RB1 and RB2: recycle F[L&1], push the own slice of F[(L+1)&1]
+    // to every peer (all-gather over NVLink stores)
+    template <int BLOCK>
+    __device__ void between(const KParams &p, CtaState &cs) {
+        const PartParams &pp = p.part;
+        const uint64_t tid = (uint64_t)cs.lid * BLOCK + threadIdx.x, nth = (uint64_t)cs.M * BLOCK;
+        const uint32_t L = cs.level;
+        const uint64_t nw = ((uint64_t)p.V + 31) / 32;
+        uint32_t *fcur = pp.F[pp.rank][L & 1];
+        for (uint64_t i = tid; i < nw; i += nth) fcur[i] = 0u;
+        const uint32_t nb = (L + 1) & 1;
+        const uint32_t *mine = pp.F[pp.rank][nb];
+        const uint64_t w0 = (uint64_t)pp.vb / 32, w1 = ((uint64_t)pp.ve + 31) / 32;
+        const uint64_t n = w1 - w0;
+        // 16-B stores over the 4-word-aligned body, word stores at the edges
+        const uint64_t a = min(n, (4 - (w0 & 3)) & 3);
+        const uint64_t n4 = (n - a) / 4;
+        for (int q = 0; q < pp.nranks; ++q) {
+            if (q == pp.rank) continue;
+            uint32_t *dst = pp.F[q][nb];
+            for (uint64_t i = tid; i < a; i += nth) dst[w0 + i] = ldcg(mine + w0 + i);
+            const uint4 *src4 = reinterpret_cast<const uint4 *>(mine + w0 + a);
+            uint4 *dst4 = reinterpret_cast<uint4 *>(dst + w0 + a);
+            for (uint64_t i = tid; i < n4; i += nth) dst4[i] = __ldcg(src4 + i);
+            for (uint64_t i = a + 4 * n4 + tid; i < n; i += nth) dst[w0 + i] = ldcg(mine + w0 + i);
+        }
+        __threadfence_system();
+    }
+
+    __device__ __forceinline__ bool exchange(const KParams &p, const CtaState &cs, uint32_t epoch,
+                                             unsigned long long count, unsigned long long *total) {
+        const PartParams &pp = p.part;
+        __threadfence_system();
+        const unsigned long long word = ((unsigned long long)epoch << 32) | (count & 0xFFFFFFFFull);
+        for (int q = 0; q < pp.nranks; ++q) st_release_sys64(pp.flags[q] + pp.rank * 2 + (epoch & 1), word);
+        unsigned long long sum = 0;
+        const unsigned long long *mine = pp.flags[pp.rank];
+        uint32_t spins = 0;
+        for (int q = 0; q < pp.nranks; ++q) {
+            unsigned long long v;
+            while (((v = ld_acquire_sys64(mine + q * 2 + (epoch & 1))) >> 32) != epoch) {
+                if (spin_check(p, cs, spins)) return false;
+            }
+            sum += v & 0xFFFFFFFFull;
+        }
+        *total = sum;
+        return true;
+    }
+
+    __device__ void serial(const KParams &p, CtaState &cs, uint32_t entry, bool resizing) {
+        Ctl *c = p.ctl;
+        const uint32_t base = p.part.seq << 16;
+        const uint64_t t0 = globaltimer();
+        if (!resizing) {   // the init global barrier: every rank cleared its bitmaps before any peer writes
+            unsigned long long tot;
+            exchange(p, cs, base | 1u, 0, &tot);
+            c->xwait_ns += globaltimer() - t0;
+            return;
+        }
+        if (entry != ENTRY_AFTER_RB2) return;
+        const uint32_t L = cs.level;                 // level++ already done before RB2
+        const unsigned long long mine = c->pcount[L & 1];
+        unsigned long long tot = 0;
+        if (!exchange(p, cs, base | (L + 1), mine, &tot)) return;
+        c->pcount[L & 1] = 0;
+        c->gcount = tot;
+        c->xwait_ns += globaltimer() - t0;
+        if (tot) {
+            if (L < p.level_cap) p.level_sizes[L] = (uint32_t)tot;
+            c->frontier_total += tot;
+            c->levels += 1;
+        }
+    }
+};
+
+}  // namespace coop

@@ -30,7 +30,7 @@ def test_header_declares_the_north_star_entry_points():
     for n in ["coop_bfs", "coop_sssp", "coop_launch", "coop_submit_task", "coop_demand", "coop_grant",
               "coop_query", "coop_wait", "coop_barrier_bench", "coop_bfs_host", "coop_sssp_host"]:
         assert n in names
-    assert len(names) == 18
+    assert len(names) == 25
 
 
 def test_library_exports_every_declared_symbol(lib_path):
@@ -58,8 +58,8 @@ def test_struct_layouts_match_header(lib_path):
 #include <stdio.h>
 #include <stddef.h>
 #include "coop.h"
-int main(void){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(coop_csr), sizeof(coop_opts), sizeof(coop_stats),
- sizeof(coop_task_event), sizeof(coop_device_info), sizeof(coop_barrier_stats)); return 0;}
+int main(void){printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(coop_csr), sizeof(coop_opts), sizeof(coop_stats),
+ sizeof(coop_task_event), sizeof(coop_device_info), sizeof(coop_barrier_stats), sizeof(coop_part)); return 0;}
 """
     import tempfile
     with tempfile.TemporaryDirectory() as d:
@@ -69,7 +69,7 @@ int main(void){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(coop_csr), sizeof(coo
         subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", exe, c])
         sizes = [int(x) for x in subprocess.check_output([exe]).split()]
     assert sizes == [ctypes.sizeof(t) for t in (coop.CooperativeCSR, coop.Opts, coop.Stats, coop.TaskEvent,
-                                                coop.DeviceInfo, coop.BarrierStats)]
+                                                coop.DeviceInfo, coop.BarrierStats, coop.CoopPart)]
 
 
 def test_sass_targets_sm100a(lib_path):

@@ -263,3 +263,35 @@ def test_end_to_end_host_pointers(coop):
     outd = torch.empty(gw.num_vertices, dtype=torch.int32)
     coop.sssp_host(gw.row_offsets, gw.col_idx, gw.weights, 1000, 0, outd)
     np.testing.assert_array_equal(outd.numpy().view(np.uint32), tb.dijkstra(gw, 0))
+
+
+# ---------------------------------------------------------------- direction optimisation
+@pytest.mark.parametrize("name", ["rmat12", "rmat16", "disconnected", "grid_ragged", "star5000", "btree10"])
+def test_bfs_direction_optimising(coop, name):
+    g = GRAPHS[name]()
+    gd = _dev(g)
+    for s in [0] + gg.sample_sources(g, 3):
+        ref = tb.bfs(g, s)
+        lv, st = coop.bfs(gd, s, flags=coop.FLAG_DIROPT, level_cap=4096)
+        np.testing.assert_array_equal(lv.cpu().numpy(), ref)
+        assert st.level_sizes == tb.level_sizes(ref)
+        assert st.reached == int((ref >= 0).sum())
+    if name.startswith("rmat"):
+        assert st.bottom_up_levels >= 1          # R-MAT's giant frontier triggers bottom-up
+
+
+def test_bfs_direction_optimising_under_resizes(coop):
+    g = gg.rmat(15, seed=2)
+    gd = _dev(g)
+    s = gg.sample_sources(g, 1)[0]
+    ref = tb.bfs(g, s)
+    for seed in range(3):
+        lv, st = coop.bfs(gd, s, flags=coop.FLAG_DIROPT | coop.FLAG_CHECK, max_wgs=50, threads_per_wg=256,
+                          policy=coop.POLICY_RANDOM, resize_prob=0.8, seed=seed, barriers_per_level=1 + seed % 2)
+        np.testing.assert_array_equal(lv.cpu().numpy(), ref)
+        assert st.kills + st.forks > 0 and st.bottom_up_levels >= 1
+    info = coop.device_query(0, 256)
+    lv, st = coop.bfs(gd, s, flags=coop.FLAG_DIROPT, threads_per_wg=256, policy=coop.POLICY_SCHEDULER,
+                      task_wgs=(info["max_coresident"] - 1) // 2, task_blocks=64, task_block_ns=5_000,
+                      task_period_ns=20_000, event_cap=64)
+    np.testing.assert_array_equal(lv.cpu().numpy(), ref)
