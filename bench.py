@@ -257,7 +257,7 @@ def run_ours(args, ws, rank, local):
 
     extras = {}
     if rank == 0 and not args.quick:
-        extras = run_extras(args, g, srcs, out, flush, stream, dev, info, times)
+        extras = run_extras(args, g, srcs, out, flush, stream, dev, info, times, flags)
 
     # ---- end to end through the C ABI with HOST buffers (H2D graph + D2H levels inside)
     e2e = None
@@ -319,7 +319,7 @@ def run_ours(args, ws, rank, local):
         torch.distributed.destroy_process_group()
 
 
-def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times):
+def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags):
     import torch
     import graphgen as gg
     from paper_1707_01989_b200 import coop
@@ -340,8 +340,8 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times):
     t_plain, t_coop = [], []
     for i in range(k + 1):
         tp, (_, stp) = timed(lambda: coop.bfs(g, srcs[i], out, threads_per_wg=args.threads,
-                                                barrier_mode=coop.BARRIER_PLAIN))
-        tc, (_, stc) = timed(lambda: coop.bfs(g, srcs[i], out, threads_per_wg=args.threads))
+                                                barrier_mode=coop.BARRIER_PLAIN, flags=flags))
+        tc, (_, stc) = timed(lambda: coop.bfs(g, srcs[i], out, threads_per_wg=args.threads, flags=flags))
         if i:
             t_plain.append(tp)
             t_coop.append(tc)
@@ -355,7 +355,7 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times):
         block_ns = int(E_us * 1000 * (N - 1) / blocks)
         tt, lat, gat, tasks = [], [], [], 0
         for i in range(k + 1):
-            t, (_, st) = timed(lambda: coop.bfs(g, srcs[i], out, threads_per_wg=args.threads,
+            t, (_, st) = timed(lambda: coop.bfs(g, srcs[i], out, threads_per_wg=args.threads, flags=flags,
                                                 policy=coop.POLICY_SCHEDULER, task_wgs=q, task_blocks=blocks,
                                                 task_block_ns=block_ns, task_period_ns=P_us * 1000,
                                                 task_first_ns=0, event_cap=4096))

@@ -107,6 +107,7 @@ typedef struct {
     void *ev_kernel_start;      /* optional cudaEvent_t recorded on `stream` right before the persistent kernel */
     void *ev_kernel_end;        /* optional cudaEvent_t recorded on `stream` right after it (kernel-only timing) */
     uint32_t workspace;         /* scratch set on the device (0..7): concurrent calls on one device need distinct ones */
+    uint32_t sssp_delta;        /* SSSP near-far band width (0 = plain worklist Bellman-Ford); results identical */
 } coop_opts;
 
 /* One competing-task instance, all times from %globaltimer (ns). */

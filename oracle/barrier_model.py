@@ -7,16 +7,18 @@ one episode on a packed word, in the spirit of the paper's efficient
 and modelled here, independently of the CUDA source, at the granularity of
 single atomic operations by thread 0 of each CTA:
 
-  W = (gen, M, arrived)                 one 64-bit word
+  W = (gen, M, arrived)                 arrival word (one 64-bit word)
+  R = (gen, M)                          release word (its own cache line)
   arrive:    old = atomicAdd(W.arrived, 1); last iff old.arrived + 1 == old.M
   serial:    (last arriver only; all M CTAs are waiting)
              M' = policy(gen); for each new id in [M, M'): CAS an IDLE slot
              to CLAIMED, write its mailbox {id, gen+1, M', transmit of WG 0},
-             store ASSIGNED; then W := (gen+1, M', 0)            (release)
-  waiters:   spin until W.gen != gen; killed iff W.gen != gen+1 or id >= W.M
+             store ASSIGNED; then W := (gen+1, M', 0)         (reset arrivals)
+             and R := (gen+1, M')                              (release)
+  waiters:   spin until R.gen != gen; killed iff R.gen != gen+1 or id >= R.M
   killed:    slot := IDLE, back to the park loop
   park loop: on ASSIGNED read mailbox, slot := ACTIVE, wait until
-             W.gen == mailbox.gen, then run the body after the barrier
+             R.gen == mailbox.gen, then run the body after the barrier
 
 Every reachable state under every interleaving (and every scripted target
 sequence) is explored; properties checked on every transition:
@@ -38,7 +40,7 @@ from dataclasses import dataclass
 IDLE, CLAIMED, ASSIGNED, ACTIVE = 0, 1, 2, 3
 
 # CTA program counters
-PARKED, WAIT_GEN, WORK, ARRIVE, SPIN, SERIAL, RELEASE, KILLED, EXITED = range(9)
+PARKED, WAIT_GEN, WORK, ARRIVE, SPIN, SERIAL, RELEASE, KILLED, EXITED, RELEASE_R = range(10)
 
 
 class ProtocolViolation(AssertionError):
@@ -59,7 +61,7 @@ def _initial(P, M0):
     ctas = tuple(Cta(WORK, p, 0, M0) if p < M0 else Cta(PARKED) for p in range(P))
     slots = tuple(ACTIVE if p < M0 else IDLE for p in range(P))
     mail = tuple((-1, -1, -1, -1) for _ in range(P))
-    W = (0, M0, 0)
+    W = ((0, M0, 0), (0, M0))      # (arrival word, release word)
     worked = ((),)            # per gen: tuple of lids that worked
     arrivals = (0,)           # per gen: arrivals
     m_at = (M0,)              # per gen: M of that interval
@@ -89,12 +91,13 @@ def _successors(state, targets, P, E, bugs=frozenset()):
                 put(Cta(EXITED))
             # else: spinning -- a self loop, no new state
         elif c.pc == WAIT_GEN:
-            if W[0] == c.gen:
+            R = W[1]
+            if R[0] == c.gen:
                 if c.gen >= E:      # forked at the final barrier: termination check first
                     put(Cta(EXITED), slots=slots[:p] + (IDLE,) + slots[p + 1:])
                 else:
                     put(Cta(WORK, c.lid, c.gen, c.M))
-            elif W[0] > c.gen:
+            elif R[0] > c.gen:
                 raise ProtocolViolation("forked CTA missed its generation")
         elif c.pc == WORK:
             g = c.gen
@@ -108,17 +111,17 @@ def _successors(state, targets, P, E, bugs=frozenset()):
             ntpub = g if c.lid == 0 else tpub        # WG 0 publishes its transmit state
             put(Cta(ARRIVE, c.lid, g, c.M), worked=nworked, tpub=ntpub)
         elif c.pc == ARRIVE:
-            gen, M, arr = W
+            gen, M, arr = W[0]
             if gen != c.gen:
                 raise ProtocolViolation("arrived on a stale generation")
             narr = arrivals[:gen] + (arrivals[gen] + 1,) + arrivals[gen + 1:]
             if arr + 1 == M:
                 mp = max(1, min(P, targets[gen] if gen < len(targets) and targets[gen] else M))
-                put(Cta(SERIAL, c.lid, c.gen, c.M, 0, mp), W=(gen, M, arr + 1), arrivals=narr)
+                put(Cta(SERIAL, c.lid, c.gen, c.M, 0, mp), W=((gen, M, arr + 1), W[1]), arrivals=narr)
             else:
-                put(Cta(SPIN, c.lid, c.gen, c.M), W=(gen, M, arr + 1), arrivals=narr)
+                put(Cta(SPIN, c.lid, c.gen, c.M), W=((gen, M, arr + 1), W[1]), arrivals=narr)
         elif c.pc == SPIN:
-            gen, M, _ = W
+            gen, M = W[1]
             if gen == c.gen:
                 continue                                  # spin
             killed = (c.lid >= M) if "kill_by_M_only" in bugs else (gen != c.gen + 1 or c.lid >= M)
@@ -133,7 +136,7 @@ def _successors(state, targets, P, E, bugs=frozenset()):
                 else:
                     put(Cta(WORK, c.lid, gen, M))
         elif c.pc == SERIAL:
-            M, mp = W[1], c.mprime
+            M, mp = W[0][1], c.mprime
             nid = M + c.claim_next
             if nid < mp:
                 # claim one IDLE slot by CAS (each slot a separate atomic => each choice a transition)
@@ -145,10 +148,12 @@ def _successors(state, targets, P, E, bugs=frozenset()):
                 # no IDLE slot: wait (scripted policy waits for killed CTAs to park)
             else:
                 put(Cta(RELEASE, c.lid, c.gen, c.M, c.claim_next, mp))
-        elif c.pc == RELEASE:
+        elif c.pc == RELEASE:       # reset the arrival word for generation g+1
+            put(Cta(RELEASE_R, c.lid, c.gen, c.M, c.claim_next, c.mprime), W=((c.gen + 1, c.mprime, 0), W[1]))
+        elif c.pc == RELEASE_R:     # release: publish (g+1, M') on R
             g = c.gen
             ng = g + 1
-            nW = (ng, c.mprime, 0)
+            nW = (W[0], (ng, c.mprime))
             nworked = worked + ((),) if len(worked) <= ng else worked
             narr = arrivals + (0,) if len(arrivals) <= ng else arrivals
             nm_at = m_at + (c.mprime,) if len(m_at) <= ng else m_at
@@ -171,8 +176,8 @@ def explore(P: int, M0: int, targets: list[int], episodes: int, max_states: int 
 
     ``bugs`` injects known-wrong protocol variants (used by the tests to show
     the model is not vacuous): "kill_by_M_only" decides a waiter's fate from
-    W.M alone, ignoring that W may already be a later generation;
-    "no_wait_gen" lets a forked CTA start before the release of W."""
+    R.M alone, ignoring that R may already be a later generation;
+    "no_wait_gen" lets a forked CTA start before the release of R."""
     init = _initial(P, M0)
     seen = {init}
     q = deque([init])

@@ -420,6 +420,16 @@ struct BfsApp {
 };
 
 // ============================================================== SSSP
+// Worklist SSSP (l-sssp of Table 1, reading R8): each interval relaxes the
+// out-edges of the current worklist with atomicMin and appends every improved
+// vertex once per round (atomicMax stamp).  With delta > 0 the worklist is
+// split near/far (Davidson et al.'s near-far pile, a Delta-stepping variant):
+// a relaxation with new distance < T goes to the next near worklist, others to
+// the far pile; when the near worklist runs dry a DRAIN interval moves far
+// entries with dist < T + delta to near (T += delta) and compacts the rest.
+// The fixpoint -- and so every distance -- is the same as plain Bellman-Ford.
+enum : uint32_t { SSSP_RELAX = 0, SSSP_DRAIN = 1, SSSP_DONE = 2 };
+
 template <typename OffT>
 struct SsspApp {
     __device__ void enter(const KParams &, CtaState &) {}
@@ -436,18 +446,64 @@ struct SsspApp {
             p.qlev[i] = 0u;
         }
         if (cs.lid == 0 && threadIdx.x == 0) {
+            Ctl *c = p.ctl;
             static_cast<uint32_t *>(p.qlight[0])[0] = (uint32_t)s;
-            p.ctl->qsize[0] = 1;
+            c->qsize[0] = 1;
+            c->smode[0] = SSSP_RELAX;
+            c->T = p.delta ? p.delta : 0xFFFFFFFFull;
             if (p.level_cap) p.level_sizes[0] = 1;
-            p.ctl->frontier_total = 1;
-            p.ctl->levels = 1;
+            c->frontier_total = 1;
+            c->levels = 1;
         }
     }
 
     __device__ bool empty(const KParams &p, CtaState &cs) {
-        if (threadIdx.x == 0) cs.app_u32[0] = ld_relaxed32(&p.ctl->qsize[cs.in_sel]);
+        if (threadIdx.x == 0) {
+            const Ctl *c = p.ctl;
+            cs.app_u32[0] = ld_relaxed32(&c->qsize[cs.in_sel]);
+            cs.app_u32[5] = ld_relaxed32(&c->smode[cs.in_sel]);
+            cs.app_u32[1] = ld_relaxed32(&c->far_sel);
+            cs.app_u32[2] = min(ld_relaxed32(&c->far_size[cs.app_u32[1]]), p.far_cap);
+            const unsigned long long T = ld_relaxed64(&c->T), Tlo = ld_relaxed64(&c->T_lo);
+            cs.app_u32[3] = (uint32_t)T;
+            cs.app_u32[4] = (uint32_t)(T >> 32);
+            cs.app_u32[6] = (uint32_t)Tlo;
+            cs.app_u32[7] = (uint32_t)(Tlo >> 32);
+        }
         __syncthreads();
-        return cs.app_u32[0] == 0;
+        return cs.app_u32[5] == SSSP_DONE;
+    }
+
+    uint32_t r1_cur;
+    __device__ __forceinline__ uint32_t r1_of(const KParams &) const { return r1_cur; }
+
+    // push v into the next near worklist (once per round) or into the far pile;
+    // warp-collective, `who` = lane pushes somewhere, `near` selects the pile
+    __device__ __forceinline__ void push(const KParams &p, bool who, bool near, uint32_t v, uint32_t out,
+                                         uint32_t fout) {
+        const uint32_t lane = threadIdx.x & 31;
+        const uint32_t lt = lanemask_lt();
+        const uint32_t mn = __ballot_sync(FULL, who && near);
+        if (mn) {
+            uint32_t pos = 0;
+            if (lane == __ffs(mn) - 1) pos = atomicAdd(&p.ctl->qsize[out], (uint32_t)__popc(mn));
+            pos = __shfl_sync(FULL, pos, __ffs(mn) - 1);
+            if (who && near) static_cast<uint32_t *>(p.qlight[out])[pos + __popc(mn & lt)] = v;
+        }
+        const uint32_t mf = __ballot_sync(FULL, who && !near);
+        if (mf) {
+            uint32_t pos = 0;
+            if (lane == __ffs(mf) - 1) pos = atomicAdd(&p.ctl->far_size[fout], (uint32_t)__popc(mf));
+            pos = __shfl_sync(FULL, pos, __ffs(mf) - 1);
+            if (who && !near) {
+                const uint32_t slot = pos + __popc(mf & lt);
+                if (slot < p.far_cap) {
+                    p.far[fout][slot] = v;
+                } else if (atomicMax(p.qlev + v, r1_of(p)) < r1_of(p)) {   // far pile full: relax it early
+                    static_cast<uint32_t *>(p.qlight[out])[atomicAdd(&p.ctl->qsize[out], 1u)] = v;
+                }
+            }
+        }
     }
 
     template <int BLOCK>
@@ -456,15 +512,42 @@ struct SsspApp {
         const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         const uint64_t gw = (uint64_t)cs.lid * WPB + warp;
         const uint64_t TW = (uint64_t)cs.M * WPB;
-        const uint32_t n = cs.app_u32[0];
         const uint32_t in = cs.in_sel, out = in ^ 1u;
         const uint32_t r1 = cs.level + 1;                         // round counter (transmitted "level")
+        r1_cur = r1;
+        const uint32_t fsel = cs.app_u32[1];
+        const unsigned long long T = ((unsigned long long)cs.app_u32[4] << 32) | cs.app_u32[3];
+        const unsigned long long Tlo = ((unsigned long long)cs.app_u32[7] << 32) | cs.app_u32[6];
+        uint64_t edges = 0;
+        if (cs.app_u32[5] == SSSP_DRAIN) {
+            // far pile -> near worklist for Tlo <= dist < T (the serial section raised T from
+            // Tlo); dist < Tlo means the vertex already went through a near worklist after
+            // its last improvement (stale copy: dropped); the rest is compacted into the
+            // other far buffer
+            const uint32_t nf = cs.app_u32[2];
+            const uint32_t *fin = p.far[fsel];
+            for (uint64_t base = gw * 32; base < nf; base += TW * 32) {
+                const uint64_t i = base + lane;
+                uint32_t v = 0, d = 0xFFFFFFFFu;
+                bool have = i < nf;
+                if (have) {
+                    v = ldcg(fin + i);
+                    d = ldcg(p.dist_out + v);
+                }
+                have = have && d >= Tlo;
+                const bool near = have && d < T;
+                bool who = have && !near;
+                if (near) who = atomicMax(p.qlev + v, r1) < r1;    // once per round
+                if (have && !near) atomicMin(&p.ctl->far_min, d);
+                push(p, who, near, v, out, fsel ^ 1u);
+            }
+            return;
+        }
+        const uint32_t n = cs.app_u32[0];
         const uint32_t *inq = static_cast<const uint32_t *>(p.qlight[in]);
-        uint32_t *outq = static_cast<uint32_t *>(p.qlight[out]);
         const OffT *ro = static_cast<const OffT *>(p.ro);
         const int32_t *__restrict__ col = p.col;
         const uint32_t *__restrict__ wt = p.w;
-        uint64_t edges = 0;
         for (uint64_t base = gw * 32; base < n; base += TW * 32) {
             const uint64_t i = base + lane;
             OffT beg = 0;
@@ -490,7 +573,7 @@ struct SsspApp {
                 const OffT b = __shfl_sync(FULL, beg, j);
                 const uint32_t ex = __shfl_sync(FULL, excl, j);
                 const uint32_t dsrc = __shfl_sync(FULL, du, j);
-                bool push = false;
+                bool who = false, near = true;
                 int32_t v = -1;
                 if (e < total) {
                     const OffT k = b + (e - ex);
@@ -498,28 +581,49 @@ struct SsspApp {
                     const uint32_t nd = dsrc + __ldg(wt + k);
                     if (nd < ldcg(p.dist_out + v)) {                      // pre-check
                         const uint32_t old = atomicMin(p.dist_out + v, nd);   // relax
-                        if (nd < old) push = atomicMax(p.qlev + v, r1) < r1;  // once per round
+                        if (nd < old) {
+                            near = nd < T;
+                            who = near ? atomicMax(p.qlev + v, r1) < r1 : true;
+                        }
                     }
                 }
-                const uint32_t m = __ballot_sync(FULL, push);
-                if (m) {
-                    const uint32_t leader = __ffs(m) - 1;
-                    uint32_t pos = 0;
-                    if (lane == leader) pos = atomicAdd(&p.ctl->qsize[out], (uint32_t)__popc(m));
-                    pos = __shfl_sync(FULL, pos, leader);
-                    if (push) outq[pos + __popc(m & lanemask_lt())] = (uint32_t)v;
-                }
+                push(p, who, near, (uint32_t)v, out, fsel);
             }
         }
         if (lane == 0 && edges) atomicAdd(&cs.edges, (unsigned long long)edges);
     }
 
+    // between the barriers: reset(out); choose the next interval (relax, drain, done)
     __device__ void serial(const KParams &p, CtaState &cs, uint32_t entry, bool resizing) {
         if (!resizing || entry != ENTRY_AFTER_RB1) return;
         Ctl *c = p.ctl;
-        const uint32_t in = cs.in_sel, out = in ^ 1u;
+        const uint32_t in = cs.in_sel, out = in ^ 1u;        // post-swap selectors
+        const uint32_t done_mode = c->smode[out];
         c->qsize[out] = 0;
-        const uint32_t n = ld_relaxed32(&c->qsize[in]);
+        uint32_t fsel = c->far_sel;
+        if (done_mode == SSSP_DRAIN) {                        // kept entries now live in the other buffer
+            c->far_size[fsel] = 0;
+            fsel ^= 1u;
+            c->far_sel = fsel;
+        }
+        const uint32_t n = c->qsize[in];
+        const uint32_t nfar = min(c->far_size[fsel], p.far_cap);
+        uint32_t mode = SSSP_RELAX;
+        if (n == 0) {
+            if (nfar == 0) {
+                mode = SSSP_DONE;
+            } else {
+                // raise the threshold; skip empty bands using the smallest kept distance
+                unsigned long long T = c->T + p.delta;
+                if (done_mode == SSSP_DRAIN && c->far_min != 0xFFFFFFFFu && c->far_min >= T)
+                    T = (unsigned long long)c->far_min + 1;
+                c->T_lo = c->T;
+                c->T = T;
+                c->far_min = 0xFFFFFFFFu;
+                mode = SSSP_DRAIN;
+            }
+        }
+        c->smode[in] = mode;
         if (n) {
             const uint32_t L = cs.level + 1;
             if (L < p.level_cap) p.level_sizes[L] = n;

@@ -104,23 +104,28 @@ __global__ void max_u32_kernel(const uint32_t *w, int64_t n, uint32_t *out) {
 __global__ void l2_rtt_kernel(unsigned long long *word, uint64_t iters, unsigned long long *out_ns) {
     unsigned long long v = 0;
     const uint64_t t0 = globaltimer();
-    for (uint64_t i = 0; i < iters; ++i) v = atomicAdd(word + (v & 0), 1ull);   // dependent chain
+    for (uint64_t i = 0; i < iters; ++i) v = atomicAdd(word + (v >> 63), 1ull);   // dependent chain (v < 2^63)
     const uint64_t t1 = globaltimer();
     out_ns[0] = t1 - t0;
     out_ns[1] = v;
 }
 
 // ------------------------------------------------------------------ scratch
+// Scratch grows with stream-ordered allocations on the call's stream: a
+// cudaFree/cudaMalloc would synchronise the device and deadlock against a
+// running persistent kernel of another rank sharing the GPU (tests).
+static thread_local cudaStream_t g_alloc_stream = nullptr;
+
 struct DevBuf {
     void *p = nullptr;
     size_t cap = 0;
     cudaError_t ensure(size_t n) {
         if (n <= cap) return cudaSuccess;
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, g_alloc_stream);
         p = nullptr;
         cap = 0;
         size_t want = std::max<size_t>(n, 256);
-        cudaError_t e = cudaMalloc(&p, want);
+        cudaError_t e = cudaMallocAsync(&p, want, g_alloc_stream);
         if (e == cudaSuccess) cap = want;
         return e;
     }
@@ -128,7 +133,8 @@ struct DevBuf {
 
 struct Scratch {
     int device = -1;
-    DevBuf ctl, mb, visited, qlev, ql0, ql1, qh0, qh1, stamp, mtrace, lsizes, events, script, wmax, fb0, fb1, fb2;
+    DevBuf ctl, mb, visited, qlev, ql0, ql1, qh0, qh1, stamp, mtrace, lsizes, events, script, wmax, fb0, fb1, fb2,
+        far0, far1;
     DevBuf h_ro, h_col, h_w, h_out;   // end-to-end (host-pointer) calls
     Ctl *host_ctl = nullptr;          // pinned staging
     std::mutex mu;
@@ -143,7 +149,11 @@ static coop_status get_scratch(Scratch **out, uint32_t ws) {
     if (dev < 0 || dev >= 16) return fail(COOP_ERR_INVALID_ARG, "device %d out of range", dev);
     if (ws >= kWorkspaces) return fail(COOP_ERR_INVALID_ARG, "workspace %u out of range [0, %u)", ws, kWorkspaces);
     Scratch *s = &g_scratch[dev][ws];
-    if (!s->host_ctl) CUDA_TRY(cudaHostAlloc((void **)&s->host_ctl, sizeof(Ctl), cudaHostAllocDefault));
+    if (!s->host_ctl) {   // all workspaces of the device at once (no allocation while a kernel runs)
+        for (uint32_t k = 0; k < kWorkspaces; ++k)
+            if (!g_scratch[dev][k].host_ctl)
+                CUDA_TRY(cudaHostAlloc((void **)&g_scratch[dev][k].host_ctl, sizeof(Ctl), cudaHostAllocDefault));
+    }
     s->device = dev;
     *out = s;
     return COOP_OK;
@@ -265,6 +275,7 @@ struct Prepared {
 static coop_status prepare(const RunReq &r, Prepared *pr) {
     static const coop_opts kDefault = {};
     const coop_opts &o = r.opts ? *r.opts : kDefault;
+    g_alloc_stream = static_cast<cudaStream_t>(o.stream);
     Scratch *s = nullptr;
     coop_status st = get_scratch(&s, o.workspace);
     if (st != COOP_OK) return st;
@@ -424,6 +435,14 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
         CUDA_TRY(s->ql0.ensure(4 * V));
         CUDA_TRY(s->ql1.ensure(4 * V));
         kp.qlev = static_cast<uint32_t *>(s->qlev.p);
+        if (o.sssp_delta) {   // far piles: every entry is one distance improvement, so <= E + V
+            CUDA_TRY(s->far0.ensure(4 * (E + V)));
+            CUDA_TRY(s->far1.ensure(4 * (E + V)));
+            kp.far[0] = static_cast<uint32_t *>(s->far0.p);
+            kp.far[1] = static_cast<uint32_t *>(s->far1.p);
+            kp.delta = o.sssp_delta;
+            kp.far_cap = (uint32_t)std::min<uint64_t>(E + V, 0xFFFFFFFFull);
+        }
     }
     kp.qlight[0] = s->ql0.p;
     kp.qlight[1] = s->ql1.p;
@@ -466,6 +485,7 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
     Ctl *h = s->host_ctl;
     memset(h, 0, sizeof(Ctl));
     h->W = pack_w(0, M0, 0);
+    h->R = pack_w(0, M0, 0);
     h->mhist[0] = M0;
     h->min_m = M0;
     h->max_m = M0;
@@ -565,6 +585,7 @@ static coop_status run_host(uint32_t app, int64_t V, const void *ro, int32_t off
     if (E && !col) return fail(COOP_ERR_INVALID_ARG, "col_idx NULL");
     if (app == APP_SSSP && E && !w) return fail(COOP_ERR_INVALID_ARG, "SSSP needs weights");
     cudaStream_t stream = opts ? static_cast<cudaStream_t>(opts->stream) : nullptr;
+    g_alloc_stream = stream;
     {
         SCRATCH_LOCK(s);
         CUDA_TRY(s->h_ro.ensure(ob * (V + 1)));

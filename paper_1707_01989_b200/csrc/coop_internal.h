@@ -52,8 +52,10 @@ struct TaskEventDev {
 
 // Control block in device memory.  Hot words sit on their own 128-B lines.
 struct __align__(128) Ctl {
-    unsigned long long W;              // barrier word {gen:32 | M:16 | arrived:16}
+    unsigned long long W;              // barrier word {gen:32 | M:16 | arrived:16} (arrivals)
     unsigned long long pad_w[15];
+    unsigned long long R;              // release word {gen:32 | M':16 | 0} (waiters poll it)
+    unsigned long long pad_r[15];
     // line: scheduler channel (resource messages)
     uint32_t demand;                   // WGs the scheduler wants back (query() = min(demand, M-1))
     uint32_t grant;                    // WGs the scheduler offers at the next fork point
@@ -104,6 +106,14 @@ struct __align__(128) Ctl {
     unsigned long long gcount;         // vertices in the global frontier of the current level (all ranks)
     unsigned long long xwait_ns;       // time spent in the cross-GPU flag exchange
     uint32_t pad_p[24];
+    // SSSP near-far
+    unsigned long long T;              // near threshold
+    unsigned long long T_lo;           // previous threshold (far entries below it are stale)
+    uint32_t smode[2];                 // SSSP_* mode of the interval reading parity p
+    uint32_t far_size[2];              // far pile sizes
+    uint32_t far_sel;                  // far pile holding the live entries
+    uint32_t far_min;                  // min distance among kept far entries (drain)
+    uint32_t pad_f[24];
 };
 
 // Partitioned BFS (1-D vertex partition).  Frontier bitmaps and
@@ -153,6 +163,9 @@ struct KParams {
     HeavyEntry *qheavy[2];
     uint32_t *stamp;            // barrier bench message passing [kMaxCtas]
     uint32_t *fbits[3];         // BFS direction optimisation: frontier bitmaps of levels L, L+1, L+2 (mod 3)
+    uint32_t *far[2];           // SSSP near-far: far piles
+    uint32_t delta;             // SSSP near-far band width (0 = plain worklist Bellman-Ford)
+    uint32_t far_cap;           // entries per far pile
     uint32_t *m_trace; uint32_t m_trace_cap;
     uint32_t *level_sizes; uint32_t level_cap;
     TaskEventDev *events; uint32_t events_cap;

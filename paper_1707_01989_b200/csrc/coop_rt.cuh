@@ -14,14 +14,35 @@
 //            ids [M, M') onto idle parked CTAs (mailbox + transmit of WG 0,
 //            P:892-903), run the app's serial work (Fig. 4 reset(out)),
 //            record M' in mhist[gen+1], then release W := {gen+1, M', 0}.
-//   waiters: spin until W.gen != gen; killed iff W.gen != gen+1 or id >= M'
-//            (ids >= M' leave: the query barrier's "ids >= M-W").
+//   waiters: spin on the release word R until R.gen != gen; killed iff
+//            R.gen != gen+1 or id >= M' (ids >= M' leave: the query barrier's
+//            "ids >= M-W").  R sits on its own line so the polls do
+//            not queue behind the arrival atomics on W.
 // NAIVE mode: on entry the top WG (id M-1 > 0) offers kill; if the
 // scheduler has demand it leaves by CAS W {g,M,a} -> {g,M-1,a}.
 #pragma once
 #include <stdint.h>
 #include "coop_internal.h"
 #include "../../include/coop.h"
+
+// Barrier implementation switches (A/B measured with tools/barrier_variants.sh;
+// the defaults are the measured best that keeps the acquire/release pairing):
+//   COOP_POLL_ACQUIRE : 1 = poll with ld.acquire; 0 = poll relaxed, one fence after
+//   COOP_POST_FENCE   : extra __threadfence() after the poll (L1 invalidation)
+//   COOP_ERR_RELOAD   : re-read the error word after the serial section
+//   COOP_ARRIVE_ACQREL: 1 = atom.acq_rel arrival; 0 = fence + relaxed atom (+ fence if last)
+#ifndef COOP_POLL_ACQUIRE
+#define COOP_POLL_ACQUIRE 1
+#endif
+#ifndef COOP_POST_FENCE
+#define COOP_POST_FENCE 1
+#endif
+#ifndef COOP_ERR_RELOAD
+#define COOP_ERR_RELOAD 1
+#endif
+#ifndef COOP_ARRIVE_ACQREL
+#define COOP_ARRIVE_ACQREL 1
+#endif
 
 namespace coop {
 
@@ -59,8 +80,16 @@ __device__ __forceinline__ void st_release32(uint32_t *p, uint32_t v) {
 __device__ __forceinline__ void st_release64(unsigned long long *p, unsigned long long v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void st_relaxed32(uint32_t *p, uint32_t v) {
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long atom_add_acq_rel64(unsigned long long *p, unsigned long long v) {
+    unsigned long long old;
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+    return old;
 }
 __device__ __forceinline__ unsigned long long ld_acquire_sys64(const unsigned long long *p) {
     unsigned long long v;
@@ -190,10 +219,12 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
                                bool resizing, uint32_t entry, uint32_t *out_mp) {
     const uint32_t lane = threadIdx.x & 31;
     Ctl *c = p.ctl;
-    uint32_t Mp = M, ep = 0, take = 0;
+    // every app passes exactly one non-resizing barrier (the init global_barrier at
+    // generation 0), so the resizing episode of generation g is g - 1 (no load)
+    const uint32_t ep = g - 1;
+    uint32_t Mp = M, take = 0;
     bool sched_fork = false, wait_fork = false;
     if (lane == 0) {
-        ep = c->episode;
         if (resizing && p.barrier_mode != COOP_BARRIER_PLAIN) {
             if (p.policy == COOP_POLICY_SCRIPTED) {
                 uint32_t s = ep < p.script_len ? p.script[ep] : 0u;
@@ -247,12 +278,15 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
         app.serial(p, cs, entry, resizing);
         if (resizing) {
             if (ep < p.m_trace_cap) p.m_trace[ep] = Mp;
-            c->episode = ep + 1;
+            c->episode = ep + 1;                       // plain store: statistics only
         }
+        // statistics as fire-and-forget reductions (no round trip on the critical path)
         if (Mp < M) atomicAdd(&c->kills, M - Mp);
-        c->forks += got;
-        c->min_m = min(c->min_m, Mp);
-        c->max_m = max(c->max_m, Mp);
+        if (got) atomicAdd(&c->forks, got);
+        if (Mp != M) {
+            atomicMin(&c->min_m, Mp);
+            atomicMax(&c->max_m, Mp);
+        }
         if (p.flags & COOP_FLAG_CHECK) {
             // every active WG arrived exactly once and ids were exactly [0, M)
             uint32_t a = atomicExch(&c->chk_arr[g & 1], 0u);
@@ -266,11 +300,14 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
             }
             if (bad) { atomicAdd(&c->violations, 1u); atomicCAS(&c->err, DERR_NONE, DERR_INVARIANT); }
         }
-        // M' of generation g+1, read by survivors and forked CTAs (never by W.M, which
-        // NAIVE kills may lower during g+1)
+        // M' of generation g+1 for NAIVE mode and forked CTAs (NAIVE kills may lower
+        // W.M during g+1); the release store publishes it with everything above
         st_relaxed32(&c->mhist[(g + 1) & 7], Mp);
-        __threadfence();
-        st_release64(&c->W, pack_w(g + 1, Mp, 0));
+        // reset the arrival word for generation g+1, then release on the separate
+        // release line R (waiters poll R, arrivals hit W: no polling traffic on the
+        // line the arrival atomics serialise on)
+        st_relaxed64(&c->W, pack_w(g + 1, Mp, 0));
+        st_release64(&c->R, pack_w(g + 1, Mp, 0));
     }
     *out_mp = Mp;
 }
@@ -295,12 +332,12 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
             atomicAdd(&c->chk_arr[g & 1], 1u);
             atomicOr(&c->idmap[g & 1][cs.lid >> 5], 1u << (cs.lid & 31));
         }
-        __threadfence();
         uint32_t action = ACT_CONT, last = 0, killed_naive = 0;
         unsigned long long old;
         if (resizing && p.barrier_mode == COOP_BARRIER_NAIVE && p.policy == COOP_POLICY_SCHEDULER &&
             cs.lid != 0) {
             // naive barrier: the slave offers kill on entry; only id M-1 can go
+            __threadfence();
             old = ld_relaxed64(&c->W);
             for (;;) {
                 uint32_t Mw = w_M(old);
@@ -334,12 +371,21 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
                 break;
             }
             if (!killed_naive) {
-                old = atomicAdd(&c->W, 1ull);
+                old = atom_add_acq_rel64(&c->W, 1ull);
                 last = (w_arr(old) + 1 == w_M(old)) ? 1u : 0u;
             }
         } else {
+            // arrive: release the CTA's writes of this interval (bar.sync + cumulative
+            // release) and, for the last arriver, acquire everybody else's
+#if COOP_ARRIVE_ACQREL
+            old = atom_add_acq_rel64(&c->W, 1ull);
+            last = (w_arr(old) + 1 == w_M(old)) ? 1u : 0u;
+#else
+            __threadfence();
             old = atomicAdd(&c->W, 1ull);
             last = (w_arr(old) + 1 == w_M(old)) ? 1u : 0u;
+            if (last) __threadfence();
+#endif
         }
         if (w_gen(old) != g) { atomicCAS(&c->err, DERR_NONE, DERR_INVARIANT); set_abort(p, DERR_INVARIANT); }
         cs.last = last;
@@ -352,21 +398,31 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
                 uint32_t spins = 0;
                 unsigned long long w;
                 for (;;) {
-                    w = ld_acquire64(&c->W);
+#if COOP_POLL_ACQUIRE
+                    w = ld_acquire64(&c->R);
+#else
+                    w = ld_relaxed64(&c->R);
+#endif
                     if (w_gen(w) != g) break;
                     if (spin_check(p, cs, spins)) { action = ACT_ABORT; break; }
                 }
+#if !COOP_POLL_ACQUIRE
+                __threadfence();
+#endif
                 if (action != ACT_ABORT) {
                     if (w_gen(w) != g + 1) {
                         action = ACT_KILLED;               // W moved on without us => we were killed at g
                     } else {
-                        uint32_t Mn = mhist_get(p, g + 1);
+                        // W.M is M' unless NAIVE kills of generation g+1 already lowered it
+                        const uint32_t Mn = p.barrier_mode == COOP_BARRIER_NAIVE ? mhist_get(p, g + 1) : w_M(w);
                         if (cs.lid >= Mn) action = ACT_KILLED;
                         else { cs.M = Mn; cs.gen = g + 1; }
                     }
                 }
             }
+#if COOP_POST_FENCE
             __threadfence();
+#endif
         }
         cs.action = action;
     }
@@ -378,7 +434,9 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
             if (threadIdx.x == 0) {
                 if (cs.bar_naive || cs.lid >= Mp) cs.action = ACT_KILLED;
                 else { cs.M = Mp; cs.gen = cs.gen + 1; cs.action = ACT_CONT; }
+#if COOP_ERR_RELOAD
                 if (ld_relaxed32(&c->err) != DERR_NONE) cs.action = ACT_ABORT;
+#endif
             }
         }
         __syncthreads();
@@ -575,7 +633,7 @@ __device__ void park_loop(const KParams &p, CtaState &cs, App &app) {
         if (threadIdx.x == 0) {
             uint32_t spins = 0;
             cs.action = ACT_CONT;
-            while (w_gen(ld_acquire64(&c->W)) != cs.gen) {
+            while (w_gen(ld_acquire64(&c->R)) != cs.gen) {
                 if (spin_check(p, cs, spins)) { cs.action = ACT_ABORT; break; }
             }
             cs.M = mhist_get(p, cs.gen);

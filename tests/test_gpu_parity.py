@@ -295,3 +295,24 @@ def test_bfs_direction_optimising_under_resizes(coop):
                       task_wgs=(info["max_coresident"] - 1) // 2, task_blocks=64, task_block_ns=5_000,
                       task_period_ns=20_000, event_cap=64)
     np.testing.assert_array_equal(lv.cpu().numpy(), ref)
+
+
+# ---------------------------------------------------------------- SSSP near-far
+@pytest.mark.parametrize("delta", [1, 50, 700, 5000, 1 << 30])
+def test_sssp_near_far_matches_dijkstra(coop, delta):
+    for name in ["grid_w", "rmat_w", "disc_w", "path_w"]:
+        g = SSSP_GRAPHS[name]()
+        gd = _dev(g)
+        s = gg.sample_sources(g, 1)[0]
+        d, st = coop.sssp(gd, s, sssp_delta=delta)
+        np.testing.assert_array_equal(_u32(d), tb.dijkstra(g, s))
+
+
+def test_sssp_near_far_under_resizes(coop):
+    g = SSSP_GRAPHS["grid_w"]()
+    gd = _dev(g)
+    ref = tb.dijkstra(g, 0)
+    for seed in range(3):
+        d, st = coop.sssp(gd, 0, sssp_delta=300, max_wgs=24, threads_per_wg=256, policy=coop.POLICY_RANDOM,
+                          resize_prob=0.5, seed=seed, flags=coop.FLAG_CHECK, barriers_per_level=1 + seed % 2)
+        np.testing.assert_array_equal(_u32(d), ref)

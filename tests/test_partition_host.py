@@ -1,0 +1,97 @@
+"""CPU tests of the partitioned path's host logic: partition layout, per-rank
+generation, hub selection, and the IPC-handle all-gather over torch.distributed
+(gloo, world_size 2, 127.0.0.1)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+import graphgen as gg
+from oracle import partition_sim as ps
+from oracle import textbook as tb
+
+
+def test_part_bounds_are_word_aligned_and_cover():
+    for V, P in [(1, 1), (31, 2), (1000, 3), (1 << 16, 8), (100, 8)]:
+        b = gg.part_bounds(V, P)
+        assert b[0] == 0 and b[-1] == V and len(b) == P + 1
+        assert all(x % 32 == 0 for x in b[:-1])
+        assert all(b[i] <= b[i + 1] for i in range(P))
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_partition_keeps_exactly_owned_destinations(P):
+    g = gg.rmat(10, seed=5)
+    ro, col = g.row_offsets.numpy(), g.col_idx.numpy()
+    total = 0
+    for r in range(P):
+        p = gg.partition(g, P, r)
+        lro, lcol = p.row_offsets.numpy(), p.col_local.numpy()
+        for u in range(0, g.num_vertices, 37):
+            full = col[ro[u]:ro[u + 1]]
+            own = full[(full >= p.v_begin) & (full < p.v_end)] - p.v_begin
+            np.testing.assert_array_equal(lcol[lro[u]:lro[u + 1]], own)
+        total += p.num_edges
+    assert total == g.num_edges
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_rmat_partition_equals_partition_of_rmat(P):
+    g = gg.rmat(10, seed=7)
+    for r in range(P):
+        a = gg.partition(g, P, r)
+        b = gg.rmat_partition(10, P, r, seed=7, chunk=3000)
+        assert torch.equal(a.row_offsets, b.row_offsets) and torch.equal(a.col_local, b.col_local)
+
+
+def test_hubs_of():
+    from paper_1707_01989_b200 import partitioned as pt
+    g = gg.disjoint_union(gg.star(5000), gg.path(10))
+    p = gg.partition(g, 2, 0)
+    ids, pref = pt.hubs_of(p, hub_degree=1000)
+    ld = p.local_degrees()
+    assert ids.tolist() == torch.nonzero(ld >= 1000).flatten().tolist()
+    assert pref[-1].item() == int(ld[ld >= 1000].sum())
+
+
+def test_partition_sim_uses_any_boundaries():
+    """BFS levels do not depend on the partition boundaries (oracle O5 vs O1)."""
+    g = gg.rmat(9, seed=1)
+    s = gg.sample_sources(g, 1)[0]
+    lv, _ = ps.bfs_partitioned(g.row_offsets.numpy(), g.col_idx.numpy().astype(np.int64), g.num_vertices, s, 5)
+    np.testing.assert_array_equal(lv, tb.bfs(g, s))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1707_01989_b200 import partitioned as pt
+    blob = bytes([rank]) * 128                      # stands in for two 64-byte IPC handles
+    allh = pt.exchange_handles(blob)
+    q.put((rank, [h[:1] for h in allh], [len(h) for h in allh]))
+    dist.destroy_process_group()
+
+
+def test_exchange_handles_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for rank, heads, lens in res:
+        assert heads == [b"\x00", b"\x01"] and lens == [128, 128]

@@ -21,6 +21,7 @@ ap.add_argument("--warm", type=int, default=2)
 ap.add_argument("--n", type=int, default=1)
 ap.add_argument("--threads", type=int, default=512)
 ap.add_argument("--app", default="bfs")
+ap.add_argument("--flags", type=int, default=2, help="2 = COOP_FLAG_DIROPT, 0 = top-down")
 args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
@@ -29,7 +30,7 @@ if args.app == "bfs":
     srcs = gg.sample_sources(g, 8, seed=2)
     out = torch.empty(g.num_vertices, dtype=torch.int32, device=dev)
     for i in range(args.warm + args.n):
-        _, st = coop.bfs(g, srcs[i % 8], out, threads_per_wg=args.threads)
+        _, st = coop.bfs(g, srcs[i % 8], out, threads_per_wg=args.threads, flags=args.flags)
         print(f"call {i}: kernel_ms={st.kernel_ns / 1e6:.3f} edges={st.edges_scanned} levels={st.levels}", flush=True)
 else:
     g = gg.with_weights(gg.grid(2048, 2048, device=dev), seed=1)

@@ -1,0 +1,60 @@
+"""Small configuration sweeps on the GPU box (prints one JSON line per point)."""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import graphgen as gg  # noqa: E402
+from paper_1707_01989_b200 import coop  # noqa: E402
+
+
+def timed(fn, reps=3):
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return min(ts), r
+
+
+what = sys.argv[1] if len(sys.argv) > 1 else "all"
+if what in ("all", "rtt"):
+    print(json.dumps({"l2_atomic_rtt_ns": coop.l2_atomic_rtt(200000)}), flush=True)
+if what in ("all", "barrier"):
+    for n in (148, 296, 592, 1184):
+        for plain in (True, False):
+            r = coop.barrier_bench(n, 100000, threads=128, plain=plain, resize_prob=0 if plain else 1 / 64)
+            print(json.dumps({"barrier_ctas": n, "plain": plain, **r}), flush=True)
+if what in ("all", "sssp"):
+    g = gg.with_weights(gg.grid(2048, 2048, device="cuda"), seed=1)
+    g.max_weight = 1000
+    out = torch.empty(g.num_vertices, dtype=torch.int32, device="cuda")
+    for threads in (256, 512, 1024):
+        for n in (1, 4, 16, 32, 74, 148):
+            try:
+                t, (_, st) = timed(lambda: coop.sssp(g, 0, out, threads_per_wg=threads, max_wgs=n), reps=2)
+            except coop.CoopError as e:
+                print(json.dumps({"sssp": True, "threads": threads, "N": n, "err": str(e)}), flush=True)
+                continue
+            print(json.dumps({"sssp": True, "threads": threads, "N": n, "ms": t, "rounds": st.levels,
+                              "frontier_total": st.frontier_total, "edges": st.edges_scanned,
+                              "us_per_round": t * 1e3 / st.levels}), flush=True)
+if what in ("all", "bfs"):
+    g = gg.rmat(24, seed=1, device="cuda", chunk=1 << 26)
+    out = torch.empty(g.num_vertices, dtype=torch.int32, device="cuda")
+    srcs = gg.sample_sources(g, 4, seed=2)
+    for flags in (coop.FLAG_DIROPT, 0):
+        for threads in (256, 512, 1024):
+            ts = []
+            for s in srcs:
+                t, (_, st) = timed(lambda: coop.bfs(g, s, out, threads_per_wg=threads, flags=flags), reps=2)
+                ts.append(t)
+            print(json.dumps({"bfs": True, "flags": flags, "threads": threads, "ms": sorted(ts)[len(ts) // 2],
+                              "levels": st.levels, "bu": st.bottom_up_levels}), flush=True)
