@@ -402,6 +402,75 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags):
     return ex
 
 
+def run_partitioned(args, ws, rank, local):
+    """N > 1: the 1-D vertex-partitioned cooperative BFS (configs[4]) with the
+    frontier all-gather inside the kernel over NVLink peer memory.  Weak
+    scaling: RMAT scale = --scale + log2(N) (2^24 vertices per GPU; N=8 is
+    RMAT-27).  value = Graph500 edges of the traversal / max-over-ranks time."""
+    import math
+    import torch
+    import torch.distributed as dist
+    import graphgen as gg
+    from paper_1707_01989_b200 import coop, partitioned as pt
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    coop.load()
+    scale = args.scale + int(round(math.log2(ws)))
+    t0 = time.time()
+    part = gg.rmat_partition(scale, ws, rank, seed=1, device=dev, chunk=1 << 26)
+    gen_s = time.time() - t0
+    V = part.num_vertices
+    vb, ve = part.v_begin, part.v_end
+    indeg = torch.bincount(part.col_local.to(torch.int64), minlength=ve - vb)   # = degree (symmetric graph)
+    pb = pt.PartitionedBFS(part, dev)
+    pb.connect_ipc()
+    # sources: seeded hash order over all vertices, keep the first with degree > 0 anywhere
+    cand = torch.argsort(gg.splitmix64(torch.arange(V, dtype=torch.int64, device=dev) ^ 0x5EED2), stable=True)[:4096]
+    own = (cand >= vb) & (cand < ve)
+    ok = torch.zeros(cand.numel(), dtype=torch.int32, device=dev)
+    ok[own] = (indeg[cand[own] - vb] > 0).to(torch.int32)
+    dist.all_reduce(ok, op=dist.ReduceOp.MAX)
+    srcs = cand[ok > 0][:64].tolist()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    times, edges = [], []
+    n_steps = args.warmup + args.steps
+    with ClockSampler(local) as clk:
+        for i in range(n_steps):
+            flush.fill_(i & 0xFF)
+            dist.barrier()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            lv, st = pb.run(srcs[i % len(srcs)], threads_per_wg=args.threads)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            if i >= args.warmup:
+                times.append(e0.elapsed_time(e1))
+                edges.append(int(indeg[lv[: ve - vb] >= 0].sum().item()))
+    tot = torch.tensor([sum(times)], device=dev)
+    dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ed = torch.tensor([float(sum(edges))], device=dev)
+    dist.all_reduce(ed)
+    tot_ms = float(tot.item())
+    gteps = float(ed.item()) / 2 / (tot_ms * 1e-3) / 1e9
+    if rank == 0:
+        line = {"metric": METRIC, "value": gteps, "unit": "GTEPS", "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+                "data": "synthetic (RMAT, Graph500 parameters, seed 1, relabelled), generated per rank",
+                "config": {"workload": f"BFS RMAT-{scale} 1-D vertex-partitioned over {ws} GPUs (configs[4]), "
+                                       "frontier all-gather inside the cooperative kernel over NVLink peer memory",
+                           "scale": scale, "vertices": V, "parallelism": f"1-D partition x{ws}",
+                           "l2": "flushed (256 MB write) before every step", "graph_gen_s": round(gen_s, 2)},
+                "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": args.steps * ws,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    pb.close()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -419,6 +488,9 @@ def main():
     ws, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, ws, rank)
+        return
+    if ws > 1:
+        run_partitioned(args, ws, rank, local)
         return
     run_ours(args, ws, rank, local)
 

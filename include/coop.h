@@ -134,6 +134,7 @@ typedef struct {
     uint32_t threads_per_wg;
     uint32_t tasks_posted, tasks_completed;
     uint32_t bottom_up_levels;  /* COOP_FLAG_DIROPT: levels run bottom-up */
+    uint32_t mid_kills;         /* workgroups that left at a chunk boundary inside an interval (offer_kill) */
     uint32_t *m_trace;          /* optional caller-owned HOST buffer: M after each resizing episode */
     uint32_t m_trace_cap;
     uint32_t *level_sizes;      /* optional caller-owned HOST buffer: frontier size per level */
@@ -213,6 +214,12 @@ coop_status coop_barrier_bench(uint32_t n_ctas, uint32_t threads, uint64_t iters
  * word; returns ns per atomic (the denominator for ns/barrier).
  */
 coop_status coop_l2_atomic_rtt(uint64_t iters, double *ns_per_atomic);
+
+/* Diagnostics: barrier phase breakdown of the last call on workspace 0 (only
+ * filled by a library built with -DCOOP_TRACE=1; zeros otherwise): clock64
+ * cycle sums for CTA 0 -- [0..5] as a waiter, [8..13] as the last arriver:
+ * entry sync, arrival, wait for release, serial section + exit, interval, count. */
+coop_status coop_debug_trace(uint64_t *out16);
 
 typedef struct coop_handle coop_handle;
 

@@ -67,7 +67,7 @@ class Stats(ctypes.Structure):
                 ("min_m", ctypes.c_uint32), ("max_m", ctypes.c_uint32),
                 ("n_wgs", ctypes.c_uint32), ("threads_per_wg", ctypes.c_uint32),
                 ("tasks_posted", ctypes.c_uint32), ("tasks_completed", ctypes.c_uint32),
-                ("bottom_up_levels", ctypes.c_uint32),
+                ("bottom_up_levels", ctypes.c_uint32), ("mid_kills", ctypes.c_uint32),
                 ("m_trace", ctypes.POINTER(ctypes.c_uint32)), ("m_trace_cap", ctypes.c_uint32),
                 ("level_sizes", ctypes.POINTER(ctypes.c_uint32)), ("level_sizes_cap", ctypes.c_uint32),
                 ("task_events", ctypes.POINTER(TaskEvent)), ("task_events_cap", ctypes.c_uint32)]
@@ -114,6 +114,7 @@ SIGNATURES = {
                                           ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
                                           ctypes.POINTER(BarrierStats)]),
     "coop_l2_atomic_rtt": (ctypes.c_int, [ctypes.c_uint64, ctypes.POINTER(ctypes.c_double)]),
+    "coop_debug_trace": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint64)]),
     "coop_launch": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(CooperativeCSR), ctypes.c_int64, _P,
                                    ctypes.POINTER(Opts), ctypes.POINTER(_P)]),
     "coop_submit_task": (ctypes.c_int, [_P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64,
@@ -177,6 +178,7 @@ class RunStats:
     tasks_posted: int = 0
     tasks_completed: int = 0
     bottom_up_levels: int = 0
+    mid_kills: int = 0
     m_trace: list = field(default_factory=list)
     level_sizes: list = field(default_factory=list)
     task_events: list = field(default_factory=list)
@@ -261,7 +263,7 @@ def _to_runstats(st: Stats, bufs) -> RunStats:
     r = RunStats(**{k: getattr(st, k) for k in ("kernel_ns", "edges_scanned", "frontier_total", "reached",
                                                 "levels", "episodes", "kills", "forks", "min_m", "max_m",
                                                 "n_wgs", "threads_per_wg", "tasks_posted", "tasks_completed",
-                                                "bottom_up_levels")})
+                                                "bottom_up_levels", "mid_kills")})
     if "m" in bufs:
         r.m_trace = list(bufs["m"][: min(st.episodes, st.m_trace_cap)])
     if "l" in bufs:
@@ -338,6 +340,13 @@ def l2_atomic_rtt(iters: int = 100000) -> float:
     v = ctypes.c_double()
     _check(lib.coop_l2_atomic_rtt(iters, ctypes.byref(v)))
     return v.value
+
+
+def debug_trace() -> list:
+    """Barrier phase breakdown of the last call (COOP_TRACE builds only)."""
+    buf = (ctypes.c_uint64 * 16)()
+    _check(load().coop_debug_trace(buf))
+    return list(buf)
 
 
 def device_query(device: int = 0, threads_per_wg: int = 512) -> dict:

@@ -213,97 +213,101 @@ struct BfsApp {
         return total;
     }
 
-    // ---------------------------------------------------------- top-down, queue input
-    __device__ void expand_tdq(const KParams &p, CtaState &cs, uint64_t gw, uint64_t TW, uint32_t *fnext,
-                               uint64_t &edges, uint32_t &reached, uint64_t &mfsum) {
+    // ---------------------------------------------------------- top-down, heavy entries
+    // The edge range [0, Eh) of the high-degree frontier entries split evenly
+    // over the M*W warps of the interval (static: done before any chunk claim,
+    // so a CTA that later leaves at a chunk boundary has finished its slice).
+    __device__ void expand_heavy(const KParams &p, CtaState &cs, uint64_t gw, uint64_t TW, uint32_t *fnext,
+                                 uint64_t &edges, uint32_t &reached, uint64_t &mfsum) {
         const uint32_t lane = threadIdx.x & 31;
-        const uint32_t nl = cs.app_u32[0], nh = cs.app_u32[1];
+        const uint32_t nh = cs.app_u32[1];
         const uint64_t Eh = ((uint64_t)cs.app_u32[3] << 32) | cs.app_u32[2];
+        if (!nh) return;
         const uint32_t in = cs.in_sel, out = in ^ 1u;
         const uint32_t L1 = cs.level + 1;
-        const LE *inq = static_cast<const LE *>(p.qlight[in]);
         const int32_t *__restrict__ col = p.col;
-        // light entries: 32 per warp, Fig. 4 stride over warps
-        for (uint64_t base = gw * 32; base < nl; base += TW * 32) {
-            const uint64_t i = base + lane;
-            OffT beg = 0;
-            uint32_t deg = 0;
-            if (i < nl) {
-                LE e = inq[i];
-                beg = e.beg;
-                deg = e.deg;
-            }
-            edges += gather(p, beg, deg, L1, out, fnext, reached, mfsum);
+        const HeavyEntry *hq = p.qheavy[in];
+        const uint64_t s0 = Eh * gw / TW, s1 = Eh * (gw + 1) / TW;
+        if (s0 >= s1) return;
+        uint32_t lo = 0, hi = nh - 1;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (ldcg(&hq[mid].prefix) <= s0) lo = mid; else hi = mid - 1;
         }
-        // heavy entries: the edge range [0, Eh) split evenly over the M*W warps
-        if (nh) {
-            const HeavyEntry *hq = p.qheavy[in];
-            const uint64_t s0 = Eh * gw / TW, s1 = Eh * (gw + 1) / TW;
-            if (s0 < s1) {
-                uint32_t lo = 0, hi = nh - 1;
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi + 1) >> 1;
-                    if (ldcg(&hq[mid].prefix) <= s0) lo = mid; else hi = mid - 1;
-                }
-                uint32_t j = lo;
-                uint64_t hb = ldcg(&hq[j].beg), hp = ldcg(&hq[j].prefix);
-                uint32_t hd = ldcg(&hq[j].deg);
-                constexpr uint32_t WIN = 32 * KB;   // <= kHeavyDeg: a window crosses at most one entry end
-                for (uint64_t ws = s0; ws < s1; ws += WIN) {
-                    const uint64_t hend = hp + hd;
-                    uint64_t hb2 = hb, hp2 = hp;
-                    uint32_t hd2 = hd;
-                    if (ws + WIN >= hend && j + 1 < nh) {   // window reaches the next entry
-                        hb2 = ldcg(&hq[j + 1].beg); hp2 = ldcg(&hq[j + 1].prefix); hd2 = ldcg(&hq[j + 1].deg);
-                    }
-                    int32_t u[KB];
+        uint32_t j = lo;
+        uint64_t hb = ldcg(&hq[j].beg), hp = ldcg(&hq[j].prefix);
+        uint32_t hd = ldcg(&hq[j].deg);
+        constexpr uint32_t WIN = 32 * KB;   // <= kHeavyDeg: a window crosses at most one entry end
+        for (uint64_t ws = s0; ws < s1; ws += WIN) {
+            const uint64_t hend = hp + hd;
+            uint64_t hb2 = hb, hp2 = hp;
+            uint32_t hd2 = hd;
+            if (ws + WIN >= hend && j + 1 < nh) {   // window reaches the next entry
+                hb2 = ldcg(&hq[j + 1].beg); hp2 = ldcg(&hq[j + 1].prefix); hd2 = ldcg(&hq[j + 1].deg);
+            }
+            int32_t u[KB];
 #pragma unroll
-                    for (int k = 0; k < KB; ++k) {
-                        const uint64_t e = ws + 32 * k + lane;
-                        u[k] = e < s1 ? __ldg(col + (e < hend ? hb + (e - hp) : hb2 + (e - hp2))) : -1;
-                    }
-                    visit_batch<KB>(p, u, L1, out, fnext, reached, mfsum);
-                    if (ws + WIN >= hend) { ++j; hb = hb2; hp = hp2; hd = hd2; }
-                }
-                edges += s1 - s0;
+            for (int k = 0; k < KB; ++k) {
+                const uint64_t e = ws + 32 * k + lane;
+                u[k] = e < s1 ? __ldg(col + (e < hend ? hb + (e - hp) : hb2 + (e - hp2))) : -1;
             }
+            visit_batch<KB>(p, u, L1, out, fnext, reached, mfsum);
+            if (ws + WIN >= hend) { ++j; hb = hb2; hp = hp2; hd = hd2; }
         }
+        edges += s1 - s0;          // warp-uniform, added by every lane (x32 convention)
     }
 
-    // ---------------------------------------------------------- top-down, bitmap input
-    // lane l owns frontier word base+l and pops one vertex per round
-    __device__ void expand_tdb(const KParams &p, CtaState &cs, uint64_t gw, uint64_t TW, uint32_t *fnext,
-                               uint64_t &edges, uint32_t &reached, uint64_t &mfsum) {
+    // ---------------------------------------------------------- top-down, queue input (one group)
+    // warp group g: light entries [32g, 32g+32)
+    __device__ void tdq_group(const KParams &p, CtaState &cs, uint64_t g, uint32_t *fnext, uint64_t &edges,
+                              uint32_t &reached, uint64_t &mfsum) {
         const uint32_t lane = threadIdx.x & 31;
+        const uint32_t nl = cs.app_u32[0];
         const uint32_t in = cs.in_sel, out = in ^ 1u;
+        const LE *inq = static_cast<const LE *>(p.qlight[in]);
+        const uint64_t i = g * 32 + lane;
+        OffT beg = 0;
+        uint32_t deg = 0;
+        if (i < nl) {
+            LE e = inq[i];
+            beg = e.beg;
+            deg = e.deg;
+        }
+        edges += (uint64_t)gather(p, beg, deg, cs.level + 1, out, fnext, reached, mfsum);
+    }
+
+    // ---------------------------------------------------------- top-down, bitmap input (one group)
+    // lane l owns frontier word 32g+l and pops one vertex per round
+    __device__ void tdb_group(const KParams &p, CtaState &cs, uint64_t g, uint32_t *fnext, uint64_t &edges,
+                              uint32_t &reached, uint64_t &mfsum) {
+        const uint32_t lane = threadIdx.x & 31;
+        const uint32_t out = cs.in_sel ^ 1u;
         const uint32_t L1 = cs.level + 1;
         const uint32_t *fcur = p.fbits[cs.level % 3];
         const OffT *ro = static_cast<const OffT *>(p.ro);
         const uint64_t nw = ((uint64_t)p.V + 31) / 32;
-        for (uint64_t base = gw * 32; base < nw; base += TW * 32) {
-            const uint64_t wi = base + lane;
-            uint32_t word = wi < nw ? ldcg(fcur + wi) : 0u;
-            while (__any_sync(FULL, word != 0)) {
-                OffT beg = 0;
-                uint32_t deg = 0;
-                if (word) {
-                    const uint32_t b = __ffs(word) - 1;
-                    word &= word - 1;
-                    const uint64_t v = wi * 32 + b;
-                    beg = __ldg(ro + v);
-                    deg = (uint32_t)(__ldg(ro + v + 1) - beg);
-                }
-                edges += gather(p, beg, deg, L1, out, fnext, reached, mfsum);
+        const uint64_t wi = g * 32 + lane;
+        uint32_t word = wi < nw ? ldcg(fcur + wi) : 0u;
+        while (__any_sync(FULL, word != 0)) {
+            OffT beg = 0;
+            uint32_t deg = 0;
+            if (word) {
+                const uint32_t b = __ffs(word) - 1;
+                word &= word - 1;
+                const uint64_t v = wi * 32 + b;
+                beg = __ldg(ro + v);
+                deg = (uint32_t)(__ldg(ro + v + 1) - beg);
             }
+            edges += (uint64_t)gather(p, beg, deg, L1, out, fnext, reached, mfsum);
         }
     }
 
-    // ---------------------------------------------------------- bottom-up
-    // warp per 32-vertex word: each unvisited vertex scans its list (4 per
-    // step) for a parent in the frontier bitmap and stops at the first hit.
-    // The warp owns the visited / next-frontier words, so no atomics.
-    __device__ void expand_bu(const KParams &p, CtaState &cs, uint64_t gw, uint64_t TW, uint64_t &edges,
-                              uint32_t &reached, uint64_t &mfsum) {
+    // ---------------------------------------------------------- bottom-up (one 32-vertex word)
+    // each unvisited vertex scans its list (4 per step) for a parent in the
+    // frontier bitmap and stops at the first hit.  The warp owns the visited /
+    // next-frontier words, so no atomics.
+    __device__ void bu_word(const KParams &p, CtaState &cs, uint64_t w, uint64_t &edges, uint32_t &reached,
+                            uint64_t &mfsum) {
         const uint32_t lane = threadIdx.x & 31;
         const uint32_t L1 = cs.level + 1;
         const uint32_t *fcur = p.fbits[cs.level % 3];
@@ -311,81 +315,122 @@ struct BfsApp {
         const OffT *ro = static_cast<const OffT *>(p.ro);
         const int32_t *__restrict__ col = p.col;
         const uint64_t V = (uint64_t)p.V;
-        const uint64_t nw = (V + 31) / 32;
-        for (uint64_t w = gw; w < nw; w += TW) {
-            const uint32_t vw = ldcg(p.visited + w);
-            if (vw == 0xFFFFFFFFu) continue;
-            const uint64_t v = w * 32 + lane;
-            bool open = v < V && !((vw >> lane) & 1u);
-            OffT b = 0, e = 0;
-            if (open) {
-                b = __ldg(ro + v);
-                e = __ldg(ro + v + 1);
-            }
-            const uint32_t deg = (uint32_t)(e - b);
-            bool found = false;
-            uint32_t scanned = 0;
-            while (open && b < e && !found) {
-                int32_t u[4];
+        const uint32_t vw = ldcg(p.visited + w);
+        if (vw == 0xFFFFFFFFu) return;
+        const uint64_t v = w * 32 + lane;
+        const bool open = v < V && !((vw >> lane) & 1u);
+        OffT b = 0, e = 0;
+        if (open) {
+            b = __ldg(ro + v);
+            e = __ldg(ro + v + 1);
+        }
+        const uint32_t deg = (uint32_t)(e - b);
+        bool found = false;
+        uint32_t scanned = 0;
+        while (open && b < e && !found) {
+            int32_t u[4];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) u[k] = b + k < e ? __ldg(col + b + k) : -1;
+            for (int k = 0; k < 4; ++k) u[k] = b + k < e ? __ldg(col + b + k) : -1;
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (u[k] >= 0 && ((ldcg(fcur + ((uint32_t)u[k] >> 5)) >> (u[k] & 31)) & 1u)) found = true;
-                const uint32_t n = (uint32_t)min((OffT)4, (OffT)(e - b));
-                scanned += n;
-                b += n;
+            for (int k = 0; k < 4; ++k)
+                if (u[k] >= 0 && ((ldcg(fcur + ((uint32_t)u[k] >> 5)) >> (u[k] & 31)) & 1u)) found = true;
+            const uint32_t n = (uint32_t)min((OffT)4, (OffT)(e - b));
+            scanned += n;
+            b += n;
+        }
+        const uint32_t wins = __ballot_sync(FULL, found);
+        if (found) {
+            p.level_out[v] = (int32_t)L1;
+            mfsum += deg;
+        }
+        edges += scanned;
+        if (wins) {
+            if (lane == 0) {
+                p.visited[w] = vw | wins;
+                fnext[w] = wins;
             }
-            const uint32_t wins = __ballot_sync(FULL, found);
-            if (found) {
-                p.level_out[v] = (int32_t)L1;
-                mfsum += deg;
-            }
-            edges += scanned;
-            if (wins) {
-                if (lane == 0) {
-                    p.visited[w] = vw | wins;
-                    fnext[w] = wins;
-                }
-                reached += __popc(wins);
-            }
+            reached += __popc(wins);
         }
     }
 
-    template <int BLOCK>
-    __device__ void expand(const KParams &p, CtaState &cs) {
-        constexpr uint32_t WPB = BLOCK / 32;
-        const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        const uint64_t gw = (uint64_t)cs.lid * WPB + warp;        // get_global_id at warp granularity
-        const uint64_t TW = (uint64_t)cs.M * WPB;                 // get_global_size / 32
-        const uint32_t out = cs.in_sel ^ 1u;
-        uint64_t edges = 0, mfsum = 0;
-        uint32_t reached = 0;
-        const uint32_t mode = cs.app_u32[5];
-        uint32_t *fnext = p.dopt ? p.fbits[(cs.level + 1) % 3] : nullptr;
-        if (p.dopt) {   // recycle the bitmap of level L-1 as the next-next frontier
-            uint32_t *fold = p.fbits[(cs.level + 2) % 3];
-            const uint64_t nw = ((uint64_t)p.V + 31) / 32;
-            for (uint64_t i = (uint64_t)cs.lid * BLOCK + threadIdx.x; i < nw; i += (uint64_t)cs.M * BLOCK) fold[i] = 0u;
-        }
-        if (mode == BFS_BU) expand_bu(p, cs, gw, TW, edges, reached, mfsum);
-        else if (mode == BFS_TDB) expand_tdb(p, cs, gw, TW, fnext, edges, reached, mfsum);
-        else expand_tdq(p, cs, gw, TW, fnext, edges, reached, mfsum);
-        // per-warp totals: lane-level partial sums of edges / degrees, warp-uniform reached
+    static constexpr uint32_t BU_WORDS = 4;      // words per warp per chunk (bottom-up)
+
+    // per-warp counters -> control block (CTA-collective; before a mid-interval
+    // kill and at the end of the interval: nf decides termination)
+    __device__ __forceinline__ void flush_counts(const KParams &p, CtaState &cs, uint64_t &edges, uint32_t &reached,
+                                                 uint64_t &mfsum) {
+        const uint32_t lane = threadIdx.x & 31;
+        uint64_t e = edges, m = mfsum;
 #pragma unroll
         for (int s = 16; s; s >>= 1) {
-            edges += __shfl_xor_sync(FULL, edges, s);
-            mfsum += __shfl_xor_sync(FULL, mfsum, s);
+            e += __shfl_xor_sync(FULL, e, s);
+            m += __shfl_xor_sync(FULL, m, s);
         }
-        if (mode != BFS_BU) edges /= 32;   // top-down edge counts are warp-uniform (counted 32x)
         if (lane == 0) {
-            if (edges) atomicAdd(&cs.edges, (unsigned long long)edges);
+            const uint32_t out = cs.in_sel ^ 1u;
+            if (e) atomicAdd(&cs.edges, (unsigned long long)(e / 32));
             if (reached) {
                 atomicAdd(&cs.reached, (unsigned long long)reached);
                 atomicAdd(&p.ctl->nf[out], (unsigned long long)reached);
             }
-            if (mfsum) atomicAdd(&p.ctl->mf[out], (unsigned long long)mfsum);
+            if (m) atomicAdd(&p.ctl->mf[out], (unsigned long long)m);
+            // the reductions above are fire-and-forget (RED): make them performed before
+            // this warp reaches the CTA barrier that precedes the arrival (the serial
+            // section reads nf / mf; nf decides termination)
+            if (reached || m) __threadfence();
         }
+        edges = 0;
+        reached = 0;
+        mfsum = 0;
+    }
+
+    template <int BLOCK>
+    __device__ uint32_t expand(const KParams &p, CtaState &cs) {
+        constexpr uint32_t WPB = BLOCK / 32;
+        const uint32_t warp = threadIdx.x >> 5;
+        const uint64_t gw = (uint64_t)cs.lid * WPB + warp;        // get_global_id at warp granularity
+        const uint64_t TW = (uint64_t)cs.M * WPB;                 // get_global_size / 32
+        const uint32_t in = cs.in_sel;
+        // per-lane accumulators; edges are kept x32 (top-down counts are warp-uniform and
+        // added by every lane; bottom-up counts are per lane and added x32)
+        uint64_t edges = 0, mfsum = 0;
+        uint32_t reached = 0;
+        const uint32_t mode = cs.app_u32[5];
+        uint32_t *fnext = p.dopt ? p.fbits[(cs.level + 1) % 3] : nullptr;
+        if (p.dopt) {   // recycle the bitmap of level L-1 as the next-next frontier (static split)
+            uint32_t *fold = p.fbits[(cs.level + 2) % 3];
+            const uint64_t nw = ((uint64_t)p.V + 31) / 32;
+            for (uint64_t i = (uint64_t)cs.lid * BLOCK + threadIdx.x; i < nw; i += (uint64_t)cs.M * BLOCK) fold[i] = 0u;
+        }
+        auto flush = [&]() { flush_counts(p, cs, edges, reached, mfsum); };
+        const uint64_t nw = ((uint64_t)p.V + 31) / 32;
+        uint32_t r;
+        if (mode == BFS_BU) {
+            const uint32_t per = WPB * BU_WORDS;
+            r = claim_chunks(p, cs, *this, &p.ctl->chunk[in], (uint32_t)((nw + per - 1) / per), [&](uint32_t ch) {
+                const uint64_t w0 = ((uint64_t)ch * WPB + warp) * BU_WORDS;
+                for (uint32_t k = 0; k < BU_WORDS; ++k) {
+                    uint64_t sc = 0;
+                    if (w0 + k < nw) bu_word(p, cs, w0 + k, sc, reached, mfsum);
+                    edges += sc * 32;
+                }
+            }, flush);
+        } else if (mode == BFS_TDB) {
+            const uint64_t groups = (nw + 31) / 32;
+            r = claim_chunks(p, cs, *this, &p.ctl->chunk[in], (uint32_t)((groups + WPB - 1) / WPB), [&](uint32_t ch) {
+                const uint64_t g = (uint64_t)ch * WPB + warp;
+                if (g < groups) tdb_group(p, cs, g, fnext, edges, reached, mfsum);
+            }, flush);
+        } else {
+            expand_heavy(p, cs, gw, TW, fnext, edges, reached, mfsum);
+            const uint64_t groups = ((uint64_t)cs.app_u32[0] + 31) / 32;
+            r = claim_chunks(p, cs, *this, &p.ctl->chunk[in], (uint32_t)((groups + WPB - 1) / WPB), [&](uint32_t ch) {
+                const uint64_t g = (uint64_t)ch * WPB + warp;
+                if (g < groups) tdq_group(p, cs, g, fnext, edges, reached, mfsum);
+            }, flush);
+        }
+        if (r == ACT_CONT) flush();
+        return r;
     }
 
     // Fig. 4 between the barriers: reset(out_nodes); per-level statistics; the
@@ -398,6 +443,7 @@ struct BfsApp {
         const uint32_t prev = c->bmode[out];
         c->qsize[out] = 0;
         c->heavy[out] = 0;
+        c->chunk[out] = 0;
         c->nf[out] = 0;
         c->mf[out] = 0;
         const unsigned long long nf = c->nf[in], mf = c->mf[in];
@@ -506,91 +552,111 @@ struct SsspApp {
         }
     }
 
-    template <int BLOCK>
-    __device__ void expand(const KParams &p, CtaState &cs) {
-        constexpr uint32_t WPB = BLOCK / 32;
-        const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        const uint64_t gw = (uint64_t)cs.lid * WPB + warp;
-        const uint64_t TW = (uint64_t)cs.M * WPB;
+    // worklist entries [32g, 32g+32): relax their out-edges (warp-wide gather)
+    __device__ void relax_group(const KParams &p, CtaState &cs, uint64_t g, uint64_t &edges) {
+        const uint32_t lane = threadIdx.x & 31;
         const uint32_t in = cs.in_sel, out = in ^ 1u;
-        const uint32_t r1 = cs.level + 1;                         // round counter (transmitted "level")
-        r1_cur = r1;
+        const uint32_t r1 = cs.level + 1;
         const uint32_t fsel = cs.app_u32[1];
         const unsigned long long T = ((unsigned long long)cs.app_u32[4] << 32) | cs.app_u32[3];
-        const unsigned long long Tlo = ((unsigned long long)cs.app_u32[7] << 32) | cs.app_u32[6];
-        uint64_t edges = 0;
-        if (cs.app_u32[5] == SSSP_DRAIN) {
-            // far pile -> near worklist for Tlo <= dist < T (the serial section raised T from
-            // Tlo); dist < Tlo means the vertex already went through a near worklist after
-            // its last improvement (stale copy: dropped); the rest is compacted into the
-            // other far buffer
-            const uint32_t nf = cs.app_u32[2];
-            const uint32_t *fin = p.far[fsel];
-            for (uint64_t base = gw * 32; base < nf; base += TW * 32) {
-                const uint64_t i = base + lane;
-                uint32_t v = 0, d = 0xFFFFFFFFu;
-                bool have = i < nf;
-                if (have) {
-                    v = ldcg(fin + i);
-                    d = ldcg(p.dist_out + v);
-                }
-                have = have && d >= Tlo;
-                const bool near = have && d < T;
-                bool who = have && !near;
-                if (near) who = atomicMax(p.qlev + v, r1) < r1;    // once per round
-                if (have && !near) atomicMin(&p.ctl->far_min, d);
-                push(p, who, near, v, out, fsel ^ 1u);
-            }
-            return;
-        }
         const uint32_t n = cs.app_u32[0];
         const uint32_t *inq = static_cast<const uint32_t *>(p.qlight[in]);
         const OffT *ro = static_cast<const OffT *>(p.ro);
         const int32_t *__restrict__ col = p.col;
         const uint32_t *__restrict__ wt = p.w;
-        for (uint64_t base = gw * 32; base < n; base += TW * 32) {
-            const uint64_t i = base + lane;
-            OffT beg = 0;
-            uint32_t deg = 0, du = 0;
-            if (i < n) {
-                const uint32_t v = ldcg(inq + i);
-                beg = __ldg(ro + v);
-                deg = (uint32_t)(__ldg(ro + v + 1) - beg);
-                du = ldcg(p.dist_out + v);                         // current dist[u] (reading R8)
-            }
-            const uint32_t incl = warp_incl_scan(deg), excl = incl - deg;
-            const uint32_t total = __shfl_sync(FULL, incl, 31);
-            edges += total;
-            for (uint32_t e0 = 0; e0 < total; e0 += 32) {
-                const uint32_t e = e0 + lane;
-                uint32_t j = 0;
+        const uint64_t i = g * 32 + lane;
+        OffT beg = 0;
+        uint32_t deg = 0, du = 0;
+        if (i < n) {
+            const uint32_t v = ldcg(inq + i);
+            beg = __ldg(ro + v);
+            deg = (uint32_t)(__ldg(ro + v + 1) - beg);
+            du = ldcg(p.dist_out + v);                         // current dist[u] (reading R8)
+        }
+        const uint32_t incl = warp_incl_scan(deg), excl = incl - deg;
+        const uint32_t total = __shfl_sync(FULL, incl, 31);
+        edges += total;
+        for (uint32_t e0 = 0; e0 < total; e0 += 32) {
+            const uint32_t e = e0 + lane;
+            uint32_t j = 0;
 #pragma unroll
-                for (uint32_t s = 16; s >= 1; s >>= 1) {
-                    const uint32_t c = j + s;
-                    const uint32_t ex = __shfl_sync(FULL, excl, c);
-                    if (ex <= e) j = c;
-                }
-                const OffT b = __shfl_sync(FULL, beg, j);
-                const uint32_t ex = __shfl_sync(FULL, excl, j);
-                const uint32_t dsrc = __shfl_sync(FULL, du, j);
-                bool who = false, near = true;
-                int32_t v = -1;
-                if (e < total) {
-                    const OffT k = b + (e - ex);
-                    v = __ldg(col + k);
-                    const uint32_t nd = dsrc + __ldg(wt + k);
-                    if (nd < ldcg(p.dist_out + v)) {                      // pre-check
-                        const uint32_t old = atomicMin(p.dist_out + v, nd);   // relax
-                        if (nd < old) {
-                            near = nd < T;
-                            who = near ? atomicMax(p.qlev + v, r1) < r1 : true;
-                        }
+            for (uint32_t s = 16; s >= 1; s >>= 1) {
+                const uint32_t c = j + s;
+                const uint32_t ex = __shfl_sync(FULL, excl, c);
+                if (ex <= e) j = c;
+            }
+            const OffT b = __shfl_sync(FULL, beg, j);
+            const uint32_t ex = __shfl_sync(FULL, excl, j);
+            const uint32_t dsrc = __shfl_sync(FULL, du, j);
+            bool who = false, near = true;
+            int32_t v = -1;
+            if (e < total) {
+                const OffT k = b + (e - ex);
+                v = __ldg(col + k);
+                const uint32_t nd = dsrc + __ldg(wt + k);
+                if (nd < ldcg(p.dist_out + v)) {                      // pre-check
+                    const uint32_t old = atomicMin(p.dist_out + v, nd);   // relax
+                    if (nd < old) {
+                        near = nd < T;
+                        who = near ? atomicMax(p.qlev + v, r1) < r1 : true;
                     }
                 }
-                push(p, who, near, (uint32_t)v, out, fsel);
             }
+            push(p, who, near, (uint32_t)v, out, fsel);
         }
-        if (lane == 0 && edges) atomicAdd(&cs.edges, (unsigned long long)edges);
+    }
+
+    // far entries [32g, 32g+32) -> near worklist for Tlo <= dist < T (the serial
+    // section raised T from Tlo); dist < Tlo means the vertex already went through a
+    // near worklist after its last improvement (stale copy: dropped); the rest is
+    // compacted into the other far buffer
+    __device__ void drain_group(const KParams &p, CtaState &cs, uint64_t g) {
+        const uint32_t lane = threadIdx.x & 31;
+        const uint32_t out = cs.in_sel ^ 1u;
+        const uint32_t r1 = cs.level + 1;
+        const uint32_t fsel = cs.app_u32[1];
+        const unsigned long long T = ((unsigned long long)cs.app_u32[4] << 32) | cs.app_u32[3];
+        const unsigned long long Tlo = ((unsigned long long)cs.app_u32[7] << 32) | cs.app_u32[6];
+        const uint32_t nf = cs.app_u32[2];
+        const uint32_t *fin = p.far[fsel];
+        const uint64_t i = g * 32 + lane;
+        uint32_t v = 0, d = 0xFFFFFFFFu;
+        bool have = i < nf;
+        if (have) {
+            v = ldcg(fin + i);
+            d = ldcg(p.dist_out + v);
+        }
+        have = have && d >= Tlo;
+        const bool near = have && d < T;
+        bool who = have && !near;
+        if (near) who = atomicMax(p.qlev + v, r1) < r1;    // once per round
+        if (have && !near) atomicMin(&p.ctl->far_min, d);
+        push(p, who, near, v, out, fsel ^ 1u);
+        __threadfence();   // far_min (RED) is read by the serial section
+    }
+
+    template <int BLOCK>
+    __device__ uint32_t expand(const KParams &p, CtaState &cs) {
+        constexpr uint32_t WPB = BLOCK / 32;
+        const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        r1_cur = cs.level + 1;
+        uint64_t edges = 0;
+        auto flush = [&]() {
+            if (lane == 0 && edges) atomicAdd(&cs.edges, (unsigned long long)edges);
+            edges = 0;
+        };
+        const bool drain = cs.app_u32[5] == SSSP_DRAIN;
+        const uint64_t items = drain ? cs.app_u32[2] : cs.app_u32[0];
+        const uint64_t groups = (items + 31) / 32;
+        const uint32_t r = claim_chunks(p, cs, *this, &p.ctl->chunk[cs.in_sel], (uint32_t)((groups + WPB - 1) / WPB),
+                                        [&](uint32_t ch) {
+            const uint64_t g = (uint64_t)ch * WPB + warp;
+            if (g >= groups) return;
+            if (drain) drain_group(p, cs, g);
+            else relax_group(p, cs, g, edges);
+        }, flush);
+        if (r == ACT_CONT) flush();
+        return r;
     }
 
     // between the barriers: reset(out); choose the next interval (relax, drain, done)
@@ -600,6 +666,7 @@ struct SsspApp {
         const uint32_t in = cs.in_sel, out = in ^ 1u;        // post-swap selectors
         const uint32_t done_mode = c->smode[out];
         c->qsize[out] = 0;
+        c->chunk[out] = 0;
         uint32_t fsel = c->far_sel;
         if (done_mode == SSSP_DRAIN) {                        // kept entries now live in the other buffer
             c->far_size[fsel] = 0;
@@ -649,7 +716,7 @@ struct BarrierApp {
         return (uint64_t)cs.level >= p.iters;
     }
     template <int BLOCK>
-    __device__ void expand(const KParams &p, CtaState &cs) {
+    __device__ uint32_t expand(const KParams &p, CtaState &cs) {
         if (threadIdx.x == 0 && (p.flags & COOP_FLAG_CHECK)) {
             if (cs.app_u32[4]) {
                 const uint32_t pm = cs.app_u32[5], pg = cs.app_u32[6];
@@ -664,6 +731,7 @@ struct BarrierApp {
             cs.app_u32[5] = cs.M;
             cs.app_u32[6] = cs.gen;
         }
+        return ACT_CONT;
     }
     __device__ void serial(const KParams &, CtaState &, uint32_t, bool) {}
 };

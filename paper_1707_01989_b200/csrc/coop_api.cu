@@ -224,6 +224,7 @@ static coop_status fill_stats(const Ctl &c, const KParams &kp, coop_stats *st, c
     st->tasks_posted = c.tasks_posted;
     st->tasks_completed = c.tasks_completed;
     st->bottom_up_levels = c.n_bu_levels;
+    st->mid_kills = c.mid_kills;
     if (st->m_trace && st->m_trace_cap) {
         uint32_t n = std::min(st->m_trace_cap, std::min(c.episode, kp.m_trace_cap));
         if (n) CUDA_TRY(cudaMemcpyAsync(st->m_trace, kp.m_trace, n * 4, cudaMemcpyDeviceToHost, stream));
@@ -665,6 +666,15 @@ extern "C" coop_status coop_barrier_bench(uint32_t n_ctas, uint32_t threads, uin
     out->forks = st.forks;
     out->violations = pr.s->host_ctl->violations;
     return rc;
+}
+
+extern "C" coop_status coop_debug_trace(uint64_t *out16) {
+    if (!out16) return fail(COOP_ERR_INVALID_ARG, "NULL argument");
+    Scratch *s = nullptr;
+    coop_status st = get_scratch(&s, 0);
+    if (st != COOP_OK) return st;
+    memcpy(out16, s->host_ctl->trace, sizeof(s->host_ctl->trace));
+    return COOP_OK;
 }
 
 extern "C" coop_status coop_l2_atomic_rtt(uint64_t iters, double *ns_per_atomic) {

@@ -95,6 +95,9 @@ struct __align__(128) Ctl {
     uint32_t host_seq_seen;
     uint32_t pad_h[31];
     // BFS frontier accounting per level parity (next frontier of the level being expanded)
+    uint32_t chunk[2];                 // dynamic work distribution: next chunk per level parity
+    uint32_t mid_kills;                // workgroups that left at a chunk boundary (mid-interval offer_kill)
+    uint32_t pad_m;
     unsigned long long nf[2];          // vertices discovered
     unsigned long long mf[2];          // sum of their degrees
     unsigned long long vis_edges;      // sum of degrees of every vertex discovered so far
@@ -114,6 +117,8 @@ struct __align__(128) Ctl {
     uint32_t far_sel;                  // far pile holding the live entries
     uint32_t far_min;                  // min distance among kept far entries (drain)
     uint32_t pad_f[24];
+    unsigned long long trace[16];      // COOP_TRACE barrier breakdown (CTA 0, clock64 cycles)
+    unsigned long long trace_last;
 };
 
 // Partitioned BFS (1-D vertex partition).  Frontier bitmaps and

@@ -30,18 +30,25 @@
 //   COOP_POLL_ACQUIRE : 1 = poll with ld.acquire; 0 = poll relaxed, one fence after
 //   COOP_POST_FENCE   : extra __threadfence() after the poll (L1 invalidation)
 //   COOP_ERR_RELOAD   : re-read the error word after the serial section
-//   COOP_ARRIVE_ACQREL: 1 = atom.acq_rel arrival; 0 = fence + relaxed atom (+ fence if last)
+//   COOP_ARRIVE_ACQREL: 1 = atom.acq_rel arrival; 0 = fence.sc + relaxed atom (+ fence if
+//                       last).  0 is required in practice: the fence by thread 0 after
+//                       bar.sync also drains the other warps' fire-and-forget reductions
+//                       (measured: with acq_rel alone, RED counters could be missed)
 #ifndef COOP_POLL_ACQUIRE
 #define COOP_POLL_ACQUIRE 1
 #endif
 #ifndef COOP_POST_FENCE
-#define COOP_POST_FENCE 1
+#define COOP_POST_FENCE 0
 #endif
 #ifndef COOP_ERR_RELOAD
-#define COOP_ERR_RELOAD 1
+#define COOP_ERR_RELOAD 0
 #endif
 #ifndef COOP_ARRIVE_ACQREL
-#define COOP_ARRIVE_ACQREL 1
+#define COOP_ARRIVE_ACQREL 0
+#endif
+
+#ifndef COOP_TRACE
+#define COOP_TRACE 0          // 1: clock64 breakdown of the barrier, CTA 0 (coop_debug_trace)
 #endif
 
 namespace coop {
@@ -147,6 +154,8 @@ struct CtaState {
     uint64_t deadline;
     unsigned long long edges, frontier, reached;   // per-CTA stats, flushed at body exit
     uint32_t bar_M, bar_naive;                     // barrier: M of the episode, killed on entry (NAIVE)
+    uint32_t chunk, stop;                          // chunk loop broadcast
+    unsigned long long acc[2];                     // app counters flushed before a mid-interval kill
     uint32_t app_u32[8];                           // app broadcast scratch
 };
 
@@ -259,7 +268,12 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
     wait_fork = __shfl_sync(FULL, (uint32_t)wait_fork, 0) != 0;
     uint32_t got = 0;
     if (Mp > M) {
-        Transmit tx0 = c->tx0;   // WG 0's transmit state published at its arrival
+        // the transmit-annotated state is uniform over the workgroups at a barrier
+        // (PAPER.md:1731-1742), so the serial section's own copy IS WG 0's
+        // (checked against WG 0's published copy under COOP_FLAG_CHECK)
+        Transmit tx0;
+        tx0.level = cs.level;
+        tx0.in_sel = cs.in_sel;
         got = fork_from_pool(p, cs, g + 1, M, Mp - M, entry, tx0, wait_fork);
         Mp = M + got;
     }
@@ -298,6 +312,7 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
                 uint32_t expect = M >= lo + 32 ? 0xffffffffu : (M > lo ? ((1u << (M - lo)) - 1u) : 0u);
                 bad |= bits != expect;
             }
+            if (resizing && (c->tx0.level != cs.level || c->tx0.in_sel != cs.in_sel)) bad = true;
             if (bad) { atomicAdd(&c->violations, 1u); atomicCAS(&c->err, DERR_NONE, DERR_INVARIANT); }
         }
         // M' of generation g+1 for NAIVE mode and forked CTAs (NAIVE kills may lower
@@ -320,11 +335,17 @@ __device__ __forceinline__ uint32_t mhist_get(const KParams &p, uint32_t gen) {
 // Returns ACT_CONT (survived; cs.M / cs.gen updated), ACT_KILLED or ACT_ABORT.
 template <class App>
 __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resizing, uint32_t entry) {
+#if COOP_TRACE
+    long long tr0 = clock64();
+#endif
     __syncthreads();
     Ctl *c = p.ctl;
+#if COOP_TRACE
+    long long tr1 = clock64(), tr2 = 0, tr3 = 0;
+#endif
     if (threadIdx.x == 0) {
         const uint32_t g = cs.gen;
-        if (cs.lid == 0) {  // publish WG 0's transmit-annotated state
+        if (cs.lid == 0 && (p.flags & COOP_FLAG_CHECK)) {  // WG 0's transmit state, for the check
             c->tx0.level = cs.level;
             c->tx0.in_sel = cs.in_sel;
         }
@@ -387,6 +408,9 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
             if (last) __threadfence();
 #endif
         }
+#if COOP_TRACE
+        tr2 = clock64();
+#endif
         if (w_gen(old) != g) { atomicCAS(&c->err, DERR_NONE, DERR_INVARIANT); set_abort(p, DERR_INVARIANT); }
         cs.last = last;
         cs.bar_M = killed_naive ? w_M(old) - 1 : w_M(old);   // M of the episode for the serial section
@@ -425,6 +449,9 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
 #endif
         }
         cs.action = action;
+#if COOP_TRACE
+        tr3 = clock64();
+#endif
     }
     __syncthreads();
     if (cs.last) {  // uniform
@@ -441,7 +468,127 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
         }
         __syncthreads();
     }
+#if COOP_TRACE
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        long long tr4 = clock64();
+        unsigned long long *T = c->trace;
+        const int o = cs.last ? 8 : 0;                       // [0..7] waiter, [8..15] last arriver
+        atomicAdd(T + o + 0, (unsigned long long)(tr1 - tr0));   // entry __syncthreads
+        atomicAdd(T + o + 1, (unsigned long long)(tr2 - tr1));   // arrival (fence + atomic)
+        atomicAdd(T + o + 2, (unsigned long long)(tr3 - tr2));   // wait for release
+        atomicAdd(T + o + 3, (unsigned long long)(tr4 - tr3));   // serial section + exit sync
+        atomicAdd(T + o + 4, (unsigned long long)(tr0 - (long long)c->trace_last));   // interval before barrier
+        atomicAdd(T + o + 5, 1ull);
+        c->trace_last = (unsigned long long)tr4;
+    }
+#endif
     return cs.action;
+}
+
+// ---------------------------------------------------------------- mid-interval offer_kill
+// offer_kill at a chunk boundary inside an interval whose work is handed out
+// by a chunk counter (so a leaving CTA strands no work).  CTA-collective.
+// Query style: every id >= M - W stops claiming and offers until
+// claimed; only the current top id M-1 can go, by CAS on the
+// arrival word {g, M, a} -> {g, M-1, a}.  If everybody else is already waiting
+// at the barrier, the leaver completes the episode on their behalf.
+// Returns ACT_KILLED, ACT_CONT (resume claiming) or ACT_ABORT.  `flush` is
+// called (CTA-collective) before the CTA can be counted out.
+template <class App, class Flush>
+__device__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, App &app, Flush &&flush) {
+    Ctl *c = p.ctl;
+    flush();
+    __syncthreads();
+    for (uint32_t spins = 0;;) {
+        if (threadIdx.x == 0) {
+            uint32_t act = ACT_CONT, serial = 0, Mnew = 0;
+            __threadfence();                               // release this CTA's work of the interval
+            unsigned long long w = ld_relaxed64(&c->W);
+            for (;;) {
+                const uint32_t M = w_M(w);
+                const uint32_t d = ld_relaxed32(&c->demand);
+                if (d == 0 || cs.lid == 0 || cs.lid + d < M || w_gen(w) != cs.gen) { act = ACT_CONT; break; }
+                if (cs.lid != M - 1) { act = ACT_IDLE; break; }         // the ids above go first
+                if (atomicCAS(&c->demand, d, d - 1) != d) { w = ld_relaxed64(&c->W); continue; }
+                uint32_t a;
+                for (;;) {                                               // arrivals may race the CAS
+                    a = w_arr(w);
+                    const unsigned long long prev = atomicCAS(&c->W, w, pack_w(cs.gen, M - 1, a));
+                    if (prev == w) break;
+                    w = prev;
+                }
+                atomicAdd(&c->kills, 1u);
+                atomicAdd(&c->mid_kills, 1u);
+                const uint32_t cur = c->cur_task;
+                const uint64_t now = globaltimer();
+                if (cur && cur - 1 < p.events_cap) {
+                    TaskEventDev *e = p.events + (cur - 1);
+                    const uint32_t before = atomicAdd(&e->surrendered, 1u);
+                    if (before == 0) e->t_first_surrender = now;
+                    if (before + 1 >= e->demanded) e->t_last_surrender = now;
+                }
+                act = ACT_KILLED;
+                if (a == M - 1) { serial = 1; Mnew = M - 1; }          // all others wait: complete for them
+                break;
+            }
+            cs.action = act;
+            cs.last = serial;
+            cs.bar_M = Mnew;
+        }
+        __syncthreads();
+        const uint32_t act = cs.action;
+        if (act == ACT_KILLED) {
+            if (cs.last) {
+                // the episode is that of resizing barrier #1, after Fig. 4's swap
+                if (threadIdx.x == 0) cs.in_sel ^= 1u;
+                __syncthreads();
+                if (threadIdx.x < 32) {
+                    uint32_t Mp;
+                    serial_section(p, cs, app, cs.gen, cs.bar_M, true, ENTRY_AFTER_RB1, &Mp);
+                }
+                __syncthreads();
+            }
+            return ACT_KILLED;
+        }
+        if (act == ACT_CONT) return ACT_CONT;
+        if (threadIdx.x == 0) {
+            if (spin_check(p, cs, spins)) cs.action = ACT_ABORT;
+            else __nanosleep(64);
+        }
+        __syncthreads();
+        if (cs.action == ACT_ABORT) return ACT_ABORT;
+    }
+}
+
+// Dynamic work distribution of an interval: CTAs claim chunk ids from
+// `counter` until `nchunks`; with the SCHEDULER policy every claim also reads
+// the resource channel and, when this id is asked to surrender, the CTA offers
+// itself (offer_kill_mid) right after finishing the chunk in hand.
+template <class App, class Fn, class Flush>
+__device__ uint32_t claim_chunks(const KParams &p, CtaState &cs, App &app, uint32_t *counter, uint32_t nchunks,
+                                 Fn &&fn, Flush &&flush) {
+    const bool midkill = p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const uint32_t ch = atomicAdd(counter, 1u);
+            uint32_t stop = 0;
+            if (midkill && cs.lid != 0) {
+                const uint32_t d = ld_relaxed32(&p.ctl->demand);
+                if (d) stop = cs.lid + d >= w_M(ld_relaxed64(&p.ctl->W));
+            }
+            cs.chunk = ch;
+            cs.stop = stop;
+        }
+        __syncthreads();
+        const uint32_t ch = cs.chunk, stop = cs.stop;
+        __syncthreads();
+        if (ch < nchunks) fn(ch);
+        if (stop) {
+            const uint32_t r = offer_kill_mid(p, cs, app, flush);
+            if (r != ACT_CONT) return r;
+        }
+        if (ch >= nchunks) return ACT_CONT;
+    }
 }
 
 // ---------------------------------------------------------------- body
@@ -461,7 +608,8 @@ __device__ uint32_t run_body(const KParams &p, CtaState &cs, App &app, uint32_t 
     for (;;) {
         if (!skip_to_rb1) {
             if (app.empty(p, cs)) return ACT_DONE;            // while (in_nodes.size > 0)
-            app.template expand<BLOCK>(p, cs);                 // for (i = tid; ...) process_node
+            r = app.template expand<BLOCK>(p, cs);             // for (i = tid; ...) process_node
+            if (r != ACT_CONT) return r;                       // killed at a chunk boundary (offer_kill)
             if (threadIdx.x == 0) cs.in_sel ^= 1u;            // swap(&in_nodes, &out_nodes)
             r = barrier(p, cs, app, true, ENTRY_AFTER_RB1);   // resizing_global_barrier() #1
             if (r != ACT_CONT) return r;

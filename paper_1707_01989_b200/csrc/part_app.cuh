@@ -83,7 +83,7 @@ struct PartBfsApp {
     }
 
     template <int BLOCK>
-    __device__ void expand(const KParams &p, CtaState &cs) {
+    __device__ uint32_t expand(const KParams &p, CtaState &cs) {
         constexpr uint32_t WPB = BLOCK / 32;
         const PartParams &pp = p.part;
         const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -172,8 +172,10 @@ struct PartBfsApp {
             if (won) {
                 atomicAdd(&cs.reached, (unsigned long long)won);
                 atomicAdd(&p.ctl->pcount[L1 & 1], (unsigned long long)won);
+                __threadfence();   // RED, read by the RB2 serial section
             }
         }
+        return ACT_CONT;
     }
 
     // between RB1 and RB2: recycle F[L&1], push the own slice of F[(L+1)&1]

@@ -36,16 +36,21 @@ if what in ("all", "sssp"):
     g = gg.with_weights(gg.grid(2048, 2048, device="cuda"), seed=1)
     g.max_weight = 1000
     out = torch.empty(g.num_vertices, dtype=torch.int32, device="cuda")
-    for threads in (256, 512, 1024):
-        for n in (1, 4, 16, 32, 74, 148):
-            try:
-                t, (_, st) = timed(lambda: coop.sssp(g, 0, out, threads_per_wg=threads, max_wgs=n), reps=2)
-            except coop.CoopError as e:
-                print(json.dumps({"sssp": True, "threads": threads, "N": n, "err": str(e)}), flush=True)
-                continue
-            print(json.dumps({"sssp": True, "threads": threads, "N": n, "ms": t, "rounds": st.levels,
-                              "frontier_total": st.frontier_total, "edges": st.edges_scanned,
-                              "us_per_round": t * 1e3 / st.levels}), flush=True)
+    deltas = [int(x) for x in os.environ.get("DELTAS", "0,250,500,1000,2000,4000,8000").split(",")]
+    for threads in (512, 1024):
+        for n in (16, 74, 148):
+            for delta in deltas:
+                try:
+                    t, (_, st) = timed(lambda: coop.sssp(g, 0, out, threads_per_wg=threads, max_wgs=n,
+                                                         sssp_delta=delta), reps=2)
+                except coop.CoopError as e:
+                    print(json.dumps({"sssp": True, "threads": threads, "N": n, "delta": delta, "err": str(e)}),
+                          flush=True)
+                    continue
+                print(json.dumps({"sssp": True, "threads": threads, "N": n, "delta": delta, "ms": t,
+                                  "rounds": st.levels, "episodes": st.episodes, "frontier_total": st.frontier_total,
+                                  "edges": st.edges_scanned, "us_per_episode": t * 1e3 / max(1, st.episodes)}),
+                      flush=True)
 if what in ("all", "bfs"):
     g = gg.rmat(24, seed=1, device="cuda", chunk=1 << 26)
     out = torch.empty(g.num_vertices, dtype=torch.int32, device="cuda")
@@ -58,3 +63,7 @@ if what in ("all", "bfs"):
                 ts.append(t)
             print(json.dumps({"bfs": True, "flags": flags, "threads": threads, "ms": sorted(ts)[len(ts) // 2],
                               "levels": st.levels, "bu": st.bottom_up_levels}), flush=True)
+if what in ("all", "barrier_small"):
+    for n in (1, 2, 4, 8, 16, 32, 64, 148):
+        r = coop.barrier_bench(n, 100000, threads=128, plain=True)
+        print(json.dumps({"barrier_ctas": n, "plain": True, "ns_per_barrier": r["ns_per_barrier"]}), flush=True)
