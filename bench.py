@@ -425,6 +425,9 @@ def run_partitioned(args, ws, rank, local):
     indeg = torch.bincount(part.col_local.to(torch.int64), minlength=ve - vb)   # = degree (symmetric graph)
     pb = pt.PartitionedBFS(part, dev)
     pb.connect_ipc()
+    eg = torch.tensor([float(part.num_edges)], device=dev, dtype=torch.float64)
+    dist.all_reduce(eg)
+    pb.E_global = int(eg.item())
     # sources: seeded hash order over all vertices, keep the first with degree > 0 anywhere
     cand = torch.argsort(gg.splitmix64(torch.arange(V, dtype=torch.int64, device=dev) ^ 0x5EED2), stable=True)[:4096]
     own = (cand >= vb) & (cand < ve)
@@ -443,7 +446,8 @@ def run_partitioned(args, ws, rank, local):
             torch.cuda.synchronize(dev)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            lv, st = pb.run(srcs[i % len(srcs)], threads_per_wg=args.threads)
+            lv, st = pb.run(srcs[i % len(srcs)], threads_per_wg=args.threads,
+                            flags=0 if args.topdown else coop.FLAG_DIROPT)
             e1.record(stream)
             torch.cuda.synchronize(dev)
             if i >= args.warmup:

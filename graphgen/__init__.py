@@ -283,6 +283,25 @@ class PartCSR:
         return self.row_offsets[1:] - self.row_offsets[:-1]
 
 
+def part_rows(part: PartCSR) -> tuple[torch.Tensor, torch.Tensor]:
+    """Owned ROWS of a symmetric graph from its column partition: the neighbour
+    list of owned vertex v (global ids, ascending) = the sources of the local edges
+    pointing to v.  Returns (row_offsets int64[v_end - v_begin + 1], col int32)."""
+    V = part.num_vertices
+    nown = part.v_end - part.v_begin
+    dev = part.col_local.device
+    src = torch.repeat_interleave(torch.arange(V, dtype=torch.int64, device=dev), part.local_degrees())
+    dst = part.col_local.to(torch.int64)
+    key = torch.sort(dst * V + src).values
+    del src
+    rcol = (key % V).to(torch.int32)
+    counts = torch.bincount(dst, minlength=nown)
+    del key, dst
+    rro = torch.zeros(nown + 1, dtype=torch.int64, device=dev)
+    rro[1:] = torch.cumsum(counts, 0)
+    return rro, rcol
+
+
 def part_bounds(V: int, P: int) -> list[int]:
     """Owned-range boundaries, multiples of 32 (whole bitmap words per rank)."""
     nw = (V + 31) // 32

@@ -70,7 +70,9 @@ typedef enum {
 
 #define COOP_FLAG_CHECK 0x1u   /* per-episode arrival / contiguity / message-passing checks -> COOP_ERR_INVARIANT */
 #define COOP_FLAG_DIROPT 0x2u  /* BFS: direction-optimising levels (bottom-up on large frontiers, Beamer's
-                                  alpha=14 / beta=24 switch); results are identical, only the work differs */
+                                  alpha=14 / beta=24 switch); results are identical, only the work differs.
+                                  Requires a symmetric CSR (undirected graph): bottom-up reads out-lists as
+                                  in-lists. */
 
 /* CSR graph, device memory, neighbour lists of vertex v at [row_offsets[v], row_offsets[v+1]). */
 typedef struct {
@@ -139,6 +141,9 @@ typedef struct {
     uint32_t m_trace_cap;
     uint32_t *level_sizes;      /* optional caller-owned HOST buffer: frontier size per level */
     uint32_t level_sizes_cap;
+    uint64_t *level_end_ns;     /* optional caller-owned HOST buffer: %globaltimer when each level's
+                                   expand finished (its first resizing barrier released), minus kernel start */
+    uint32_t level_end_ns_cap;
     coop_task_event *task_events; /* optional caller-owned HOST buffer */
     uint32_t task_events_cap;
 } coop_stats;
@@ -245,7 +250,11 @@ typedef struct {
     const uint64_t *hub_prefix; /* device, num_hubs + 1 prefix sums of the hubs' local degrees */
     uint32_t num_hubs, hub_degree;
     uint32_t *frontier[COOP_MAX_RANKS][2]; /* rank q's two frontier bitmaps, ceil(V/32) words each, device-visible */
-    uint64_t *flags[COOP_MAX_RANKS];       /* rank q's flag block, 2*COOP_MAX_RANKS uint64, zeroed once when allocated */
+    uint64_t *flags[COOP_MAX_RANKS];       /* rank q's flag block, 4*COOP_MAX_RANKS uint64, zeroed once when allocated */
+    /* COOP_FLAG_DIROPT (bottom-up levels; symmetric graph only): */
+    const void *rows_offsets;   /* device, v_end - v_begin + 1 offsets of the OWNED rows (offset_bits wide) */
+    const int32_t *rows_col;    /* device, their neighbours (global ids) */
+    int64_t num_edges_global;   /* directed edges of the whole graph */
 } coop_part;
 
 /* Blocking partitioned BFS of this rank.  levels_owned_out: device int32[v_end - v_begin];

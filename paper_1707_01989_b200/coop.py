@@ -70,6 +70,7 @@ class Stats(ctypes.Structure):
                 ("bottom_up_levels", ctypes.c_uint32), ("mid_kills", ctypes.c_uint32),
                 ("m_trace", ctypes.POINTER(ctypes.c_uint32)), ("m_trace_cap", ctypes.c_uint32),
                 ("level_sizes", ctypes.POINTER(ctypes.c_uint32)), ("level_sizes_cap", ctypes.c_uint32),
+                ("level_end_ns", ctypes.POINTER(ctypes.c_uint64)), ("level_end_ns_cap", ctypes.c_uint32),
                 ("task_events", ctypes.POINTER(TaskEvent)), ("task_events_cap", ctypes.c_uint32)]
 
 
@@ -92,7 +93,9 @@ class CoopPart(ctypes.Structure):
                 ("col_local", ctypes.c_void_p), ("num_edges", ctypes.c_int64),
                 ("hub_ids", ctypes.c_void_p), ("hub_prefix", ctypes.c_void_p),
                 ("num_hubs", ctypes.c_uint32), ("hub_degree", ctypes.c_uint32),
-                ("frontier", (ctypes.c_void_p * 2) * 8), ("flags", ctypes.c_void_p * 8)]
+                ("frontier", (ctypes.c_void_p * 2) * 8), ("flags", ctypes.c_void_p * 8),
+                ("rows_offsets", ctypes.c_void_p), ("rows_col", ctypes.c_void_p),
+                ("num_edges_global", ctypes.c_int64)]
 
 
 # every function declared in include/coop.h: name -> (restype, argtypes)
@@ -181,6 +184,7 @@ class RunStats:
     mid_kills: int = 0
     m_trace: list = field(default_factory=list)
     level_sizes: list = field(default_factory=list)
+    level_end_ns: list = field(default_factory=list)
     task_events: list = field(default_factory=list)
 
 
@@ -253,6 +257,8 @@ def _stats_struct(trace_cap=0, level_cap=0, event_cap=0):
     if level_cap:
         bufs["l"] = (ctypes.c_uint32 * level_cap)()
         st.level_sizes, st.level_sizes_cap = ctypes.cast(bufs["l"], ctypes.POINTER(ctypes.c_uint32)), level_cap
+        bufs["t"] = (ctypes.c_uint64 * level_cap)()
+        st.level_end_ns, st.level_end_ns_cap = ctypes.cast(bufs["t"], ctypes.POINTER(ctypes.c_uint64)), level_cap
     if event_cap:
         bufs["e"] = (TaskEvent * event_cap)()
         st.task_events, st.task_events_cap = ctypes.cast(bufs["e"], ctypes.POINTER(TaskEvent)), event_cap
@@ -268,6 +274,7 @@ def _to_runstats(st: Stats, bufs) -> RunStats:
         r.m_trace = list(bufs["m"][: min(st.episodes, st.m_trace_cap)])
     if "l" in bufs:
         r.level_sizes = list(bufs["l"][: min(st.levels, st.level_sizes_cap)])
+        r.level_end_ns = list(bufs["t"][: min(st.levels, st.level_end_ns_cap)])
     if "e" in bufs:
         n = min(st.tasks_posted, st.task_events_cap)
         r.task_events = [{f: getattr(bufs["e"][i], f) for f, _ in TaskEvent._fields_} for i in range(n)]

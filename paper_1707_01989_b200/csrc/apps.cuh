@@ -17,6 +17,10 @@
 #include <type_traits>
 #include "coop_rt.cuh"
 
+#ifndef COOP_BU_KW
+#define COOP_BU_KW 4
+#endif
+
 namespace coop {
 
 template <typename T>
@@ -40,7 +44,7 @@ struct BfsApp {
     __device__ void between(const KParams &, CtaState &) {}
 
     template <int BLOCK>
-    __device__ void init(const KParams &p, CtaState &cs) {
+    __device__ __noinline__ void init(const KParams &p, CtaState &cs) {
         const uint64_t tid = (uint64_t)cs.lid * BLOCK + threadIdx.x;
         const uint64_t nth = (uint64_t)cs.M * BLOCK;
         const int64_t V = p.V, s = p.source;
@@ -62,8 +66,21 @@ struct BfsApp {
         for (uint64_t i = h + 4 * nvec + tid; i < (uint64_t)V; i += nth) lv[i] = (int64_t)i == s ? 0 : -1;
         const uint64_t nw = ((uint64_t)V + 31) / 32;
         const uint32_t sw = (uint32_t)(s >> 5), sb = 1u << (s & 31);
+        if (p.dopt) {
+            // symmetric graph: a degree-0 vertex is never a neighbour, so it starts
+            // "visited" and bottom-up levels skip it; warp per word, lane per vertex
+            const OffT *rof = static_cast<const OffT *>(p.ro);
+            const uint32_t lane = threadIdx.x & 31;
+            const uint64_t TW = nth / 32;
+            for (uint64_t w = tid / 32; w < nw; w += TW) {
+                const uint64_t v = w * 32 + lane;
+                const bool deg0 = v < (uint64_t)V && __ldg(rof + v + 1) == __ldg(rof + v);
+                const uint32_t m = __ballot_sync(FULL, deg0);
+                if (lane == 0) p.visited[w] = m | (w == sw ? sb : 0u);
+            }
+        }
         for (uint64_t i = tid; i < nw; i += nth) {
-            p.visited[i] = i == sw ? sb : 0u;
+            if (!p.dopt) p.visited[i] = i == sw ? sb : 0u;
             if (p.dopt) {
                 p.fbits[0][i] = i == sw ? sb : 0u;
                 p.fbits[1][i] = 0u;
@@ -98,17 +115,34 @@ struct BfsApp {
     __device__ bool empty(const KParams &p, CtaState &cs) {
         if (threadIdx.x == 0) {
             const uint32_t in = cs.in_sel;
-            const unsigned long long hv = ld_relaxed64(&p.ctl->heavy[in]);
+            // plain loads after the barrier's acquire: independent, so they overlap
+            // (the asm-volatile relaxed loads serialise one round trip each)
+            const Ctl *c = p.ctl;
+            const unsigned long long hv = c->heavy[in];
             const uint64_t Eh = hv & kMask40;
-            cs.app_u32[0] = ld_relaxed32(&p.ctl->qsize[in]);
+            cs.app_u32[0] = c->qsize[in];
             cs.app_u32[1] = (uint32_t)(hv >> 40);
             cs.app_u32[2] = (uint32_t)Eh;
             cs.app_u32[3] = (uint32_t)(Eh >> 32);
-            cs.app_u32[4] = ld_relaxed64(&p.ctl->nf[in]) ? 1u : 0u;
-            cs.app_u32[5] = ld_relaxed32(&p.ctl->bmode[in]);
+            cs.app_u32[4] = c->nf[in] ? 1u : 0u;
+            cs.app_u32[5] = c->bmode[in];
         }
         __syncthreads();
         return cs.app_u32[4] == 0;
+    }
+
+    static constexpr uint32_t kQueueRes = 256;   // per-warp queue reservation (>= 2 * 32 * KB)
+
+    // empty entries in the unused reserved slots [res.x, res.y) (warp-collective)
+    __device__ __forceinline__ static void fill_holes(LE *q, uint2 &res) {
+        const uint32_t lane = threadIdx.x & 31;
+        for (uint32_t i = res.x + lane; i < res.y; i += 32) {
+            LE z;
+            z.beg = 0;
+            z.deg = 0;
+            q[i] = z;
+        }
+        res = make_uint2(0, 0);
     }
 
     // ---------------------------------------------------------- top-down claim
@@ -119,7 +153,7 @@ struct BfsApp {
     template <int K>
     __device__ __forceinline__ void visit_batch(const KParams &p, const int32_t (&u)[K], uint32_t L1,
                                                 uint32_t out, uint32_t *fnext, uint32_t &reached,
-                                                uint64_t &mfsum) {
+                                                uint64_t &mfsum, uint2 &res) {
         const uint32_t lane = threadIdx.x & 31;
         uint32_t *vis = p.visited;
         uint32_t cur[K];
@@ -159,10 +193,20 @@ struct BfsApp {
             tot += __popc(m[k]);
         }
         if (tot) {
-            uint32_t pos = 0;
-            if (lane == 0) pos = atomicAdd(&p.ctl->qsize[out], tot);
-            pos = __shfl_sync(FULL, pos, 0);
+            // slots come from a per-warp reservation of kQueueRes entries (one queue
+            // atomic per kQueueRes appends instead of one per batch: the single counter
+            // serialises every warp of the grid); unused slots are filled with empty
+            // entries (deg 0), which expand to nothing
             LE *q = static_cast<LE *>(p.qlight[out]);
+            if (res.x + tot > res.y) {
+                fill_holes(q, res);
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(&p.ctl->qsize[out], kQueueRes);
+                base = __shfl_sync(FULL, base, 0);
+                res = make_uint2(base, base + kQueueRes);
+            }
+            const uint32_t pos = res.x;
+            res.x += tot;
             const uint32_t lt = lanemask_lt();
 #pragma unroll
             for (int k = 0; k < K; ++k) {
@@ -187,7 +231,7 @@ struct BfsApp {
     // of the degrees, then 32*KB edges per iteration, owner found by a shuffle
     // binary search (warp-level load balancing of short lists)
     __device__ __forceinline__ uint32_t gather(const KParams &p, OffT beg, uint32_t deg, uint32_t L1, uint32_t out,
-                                               uint32_t *fnext, uint32_t &reached, uint64_t &mfsum) {
+                                               uint32_t *fnext, uint32_t &reached, uint64_t &mfsum, uint2 &res) {
         const uint32_t lane = threadIdx.x & 31;
         const int32_t *__restrict__ col = p.col;
         const uint32_t incl = warp_incl_scan(deg), excl = incl - deg;
@@ -208,7 +252,7 @@ struct BfsApp {
                 const uint32_t ex = __shfl_sync(FULL, excl, j);
                 u[k] = e < total ? __ldg(col + b + (e - ex)) : -1;
             }
-            visit_batch<KB>(p, u, L1, out, fnext, reached, mfsum);
+            visit_batch<KB>(p, u, L1, out, fnext, reached, mfsum, res);
         }
         return total;
     }
@@ -218,7 +262,7 @@ struct BfsApp {
     // over the M*W warps of the interval (static: done before any chunk claim,
     // so a CTA that later leaves at a chunk boundary has finished its slice).
     __device__ void expand_heavy(const KParams &p, CtaState &cs, uint64_t gw, uint64_t TW, uint32_t *fnext,
-                                 uint64_t &edges, uint32_t &reached, uint64_t &mfsum) {
+                                 uint64_t &edges, uint32_t &reached, uint64_t &mfsum, uint2 &res) {
         const uint32_t lane = threadIdx.x & 31;
         const uint32_t nh = cs.app_u32[1];
         const uint64_t Eh = ((uint64_t)cs.app_u32[3] << 32) | cs.app_u32[2];
@@ -251,7 +295,7 @@ struct BfsApp {
                 const uint64_t e = ws + 32 * k + lane;
                 u[k] = e < s1 ? __ldg(col + (e < hend ? hb + (e - hp) : hb2 + (e - hp2))) : -1;
             }
-            visit_batch<KB>(p, u, L1, out, fnext, reached, mfsum);
+            visit_batch<KB>(p, u, L1, out, fnext, reached, mfsum, res);
             if (ws + WIN >= hend) { ++j; hb = hb2; hp = hp2; hd = hd2; }
         }
         edges += s1 - s0;          // warp-uniform, added by every lane (x32 convention)
@@ -259,8 +303,8 @@ struct BfsApp {
 
     // ---------------------------------------------------------- top-down, queue input (one group)
     // warp group g: light entries [32g, 32g+32)
-    __device__ void tdq_group(const KParams &p, CtaState &cs, uint64_t g, uint32_t *fnext, uint64_t &edges,
-                              uint32_t &reached, uint64_t &mfsum) {
+    __device__ __forceinline__ void tdq_group(const KParams &p, CtaState &cs, uint64_t g, uint32_t *fnext, uint64_t &edges,
+                              uint32_t &reached, uint64_t &mfsum, uint2 &res) {
         const uint32_t lane = threadIdx.x & 31;
         const uint32_t nl = cs.app_u32[0];
         const uint32_t in = cs.in_sel, out = in ^ 1u;
@@ -273,13 +317,13 @@ struct BfsApp {
             beg = e.beg;
             deg = e.deg;
         }
-        edges += (uint64_t)gather(p, beg, deg, cs.level + 1, out, fnext, reached, mfsum);
+        edges += (uint64_t)gather(p, beg, deg, cs.level + 1, out, fnext, reached, mfsum, res);
     }
 
     // ---------------------------------------------------------- top-down, bitmap input (one group)
     // lane l owns frontier word 32g+l and pops one vertex per round
-    __device__ void tdb_group(const KParams &p, CtaState &cs, uint64_t g, uint32_t *fnext, uint64_t &edges,
-                              uint32_t &reached, uint64_t &mfsum) {
+    __device__ __forceinline__ void tdb_group(const KParams &p, CtaState &cs, uint64_t g, uint32_t *fnext, uint64_t &edges,
+                              uint32_t &reached, uint64_t &mfsum, uint2 &res) {
         const uint32_t lane = threadIdx.x & 31;
         const uint32_t out = cs.in_sel ^ 1u;
         const uint32_t L1 = cs.level + 1;
@@ -298,7 +342,7 @@ struct BfsApp {
                 beg = __ldg(ro + v);
                 deg = (uint32_t)(__ldg(ro + v + 1) - beg);
             }
-            edges += (uint64_t)gather(p, beg, deg, L1, out, fnext, reached, mfsum);
+            edges += (uint64_t)gather(p, beg, deg, L1, out, fnext, reached, mfsum, res);
         }
     }
 
@@ -306,8 +350,13 @@ struct BfsApp {
     // each unvisited vertex scans its list (4 per step) for a parent in the
     // frontier bitmap and stops at the first hit.  The warp owns the visited /
     // next-frontier words, so no atomics.
-    __device__ void bu_word(const KParams &p, CtaState &cs, uint64_t w, uint64_t &edges, uint32_t &reached,
-                            uint64_t &mfsum) {
+    // KW consecutive words per warp item: lane l owns vertex (w0+k)*32 + l of
+    // each word k, and all KW lists advance together (KW x 4 column loads and
+    // probes in flight per lane) -- the step is latency bound, so this is the
+    // lever, not bandwidth.
+    template <int KW>
+    __device__ __forceinline__ void bu_words(const KParams &p, CtaState &cs, uint64_t w0, uint64_t nw,
+                                             uint64_t &edges, uint32_t &reached, uint64_t &mfsum) {
         const uint32_t lane = threadIdx.x & 31;
         const uint32_t L1 = cs.level + 1;
         const uint32_t *fcur = p.fbits[cs.level % 3];
@@ -315,50 +364,79 @@ struct BfsApp {
         const OffT *ro = static_cast<const OffT *>(p.ro);
         const int32_t *__restrict__ col = p.col;
         const uint64_t V = (uint64_t)p.V;
-        const uint32_t vw = ldcg(p.visited + w);
-        if (vw == 0xFFFFFFFFu) return;
-        const uint64_t v = w * 32 + lane;
-        const bool open = v < V && !((vw >> lane) & 1u);
-        OffT b = 0, e = 0;
-        if (open) {
-            b = __ldg(ro + v);
-            e = __ldg(ro + v + 1);
-        }
-        const uint32_t deg = (uint32_t)(e - b);
-        bool found = false;
-        uint32_t scanned = 0;
-        while (open && b < e && !found) {
-            int32_t u[4];
+        uint32_t vw[KW];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) u[k] = b + k < e ? __ldg(col + b + k) : -1;
+        for (int k = 0; k < KW; ++k) vw[k] = w0 + k < nw ? ldcg(p.visited + w0 + k) : 0xFFFFFFFFu;
+        bool any_open = false;
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (u[k] >= 0 && ((ldcg(fcur + ((uint32_t)u[k] >> 5)) >> (u[k] & 31)) & 1u)) found = true;
-            const uint32_t n = (uint32_t)min((OffT)4, (OffT)(e - b));
-            scanned += n;
-            b += n;
-        }
-        const uint32_t wins = __ballot_sync(FULL, found);
-        if (found) {
-            p.level_out[v] = (int32_t)L1;
-            mfsum += deg;
-        }
-        edges += scanned;
-        if (wins) {
-            if (lane == 0) {
-                p.visited[w] = vw | wins;
-                fnext[w] = wins;
+        for (int k = 0; k < KW; ++k) any_open |= vw[k] != 0xFFFFFFFFu;
+        if (!any_open) return;                                 // warp-uniform
+        OffT b[KW], e[KW];
+        bool found[KW];
+#pragma unroll
+        for (int k = 0; k < KW; ++k) {
+            const uint64_t v = (w0 + k) * 32 + lane;
+            b[k] = 0;
+            e[k] = 0;
+            found[k] = false;
+            if (v < V && !((vw[k] >> lane) & 1u)) {
+                b[k] = __ldg(ro + v);
+                e[k] = __ldg(ro + v + 1);
             }
-            reached += __popc(wins);
+        }
+        uint32_t deg[KW];
+#pragma unroll
+        for (int k = 0; k < KW; ++k) deg[k] = (uint32_t)(e[k] - b[k]);
+        uint32_t scanned = 0;
+        for (;;) {
+            bool more = false;
+#pragma unroll
+            for (int k = 0; k < KW; ++k) more |= (b[k] < e[k] && !found[k]);
+            if (!more) break;
+            int32_t u[KW][4];
+#pragma unroll
+            for (int k = 0; k < KW; ++k) {
+                const bool act = b[k] < e[k] && !found[k];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) u[k][j] = (act && b[k] + j < e[k]) ? __ldg(col + b[k] + j) : -1;
+            }
+#pragma unroll
+            for (int k = 0; k < KW; ++k) {
+                const bool act = b[k] < e[k] && !found[k];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (u[k][j] >= 0 && ((ldcg(fcur + ((uint32_t)u[k][j] >> 5)) >> (u[k][j] & 31)) & 1u)) found[k] = true;
+                if (act) {
+                    const uint32_t n = (uint32_t)min((OffT)4, (OffT)(e[k] - b[k]));
+                    scanned += n;
+                    b[k] += n;
+                }
+            }
+        }
+        edges += (uint64_t)scanned * 32;
+#pragma unroll
+        for (int k = 0; k < KW; ++k) {
+            const uint32_t wins = __ballot_sync(FULL, found[k]);
+            if (found[k]) {
+                p.level_out[(w0 + k) * 32 + lane] = (int32_t)L1;
+                mfsum += deg[k];
+            }
+            if (wins) {
+                if (lane == 0) {
+                    p.visited[w0 + k] = vw[k] | wins;
+                    fnext[w0 + k] = wins;
+                }
+                reached += __popc(wins);
+            }
         }
     }
 
-    static constexpr uint32_t BU_WORDS = 4;      // words per warp per chunk (bottom-up)
+    static constexpr uint32_t BU_KW = COOP_BU_KW;  // bottom-up: words per warp item
 
     // per-warp counters -> control block (CTA-collective; before a mid-interval
     // kill and at the end of the interval: nf decides termination)
-    __device__ __forceinline__ void flush_counts(const KParams &p, CtaState &cs, uint64_t &edges, uint32_t &reached,
-                                                 uint64_t &mfsum) {
+    __device__ __forceinline__ void flush_counts(const KParams &p, CtaState &cs, uint32_t out, uint64_t &edges,
+                                                 uint32_t &reached, uint64_t &mfsum) {
         const uint32_t lane = threadIdx.x & 31;
         uint64_t e = edges, m = mfsum;
 #pragma unroll
@@ -367,7 +445,6 @@ struct BfsApp {
             m += __shfl_xor_sync(FULL, m, s);
         }
         if (lane == 0) {
-            const uint32_t out = cs.in_sel ^ 1u;
             if (e) atomicAdd(&cs.edges, (unsigned long long)(e / 32));
             if (reached) {
                 atomicAdd(&cs.reached, (unsigned long long)reached);
@@ -402,32 +479,26 @@ struct BfsApp {
             const uint64_t nw = ((uint64_t)p.V + 31) / 32;
             for (uint64_t i = (uint64_t)cs.lid * BLOCK + threadIdx.x; i < nw; i += (uint64_t)cs.M * BLOCK) fold[i] = 0u;
         }
-        auto flush = [&]() { flush_counts(p, cs, edges, reached, mfsum); };
+        const uint32_t out = in ^ 1u;                             // parity filled by this level
+        uint2 res = make_uint2(0, 0);
+        auto flush = [&]() {
+            fill_holes(static_cast<LE *>(p.qlight[out]), res);
+            flush_counts(p, cs, out, edges, reached, mfsum);
+        };
         const uint64_t nw = ((uint64_t)p.V + 31) / 32;
         uint32_t r;
-        if (mode == BFS_BU) {
-            const uint32_t per = WPB * BU_WORDS;
-            r = claim_chunks(p, cs, *this, &p.ctl->chunk[in], (uint32_t)((nw + per - 1) / per), [&](uint32_t ch) {
-                const uint64_t w0 = ((uint64_t)ch * WPB + warp) * BU_WORDS;
-                for (uint32_t k = 0; k < BU_WORDS; ++k) {
-                    uint64_t sc = 0;
-                    if (w0 + k < nw) bu_word(p, cs, w0 + k, sc, reached, mfsum);
-                    edges += sc * 32;
-                }
+        if (mode == BFS_BU) {                                 // item = BU_KW 32-vertex words
+            r = claim_items<BLOCK>(p, cs, *this, &p.ctl->chunk[in], (nw + BU_KW - 1) / BU_KW, 128u, [&](uint64_t it) {
+                bu_words<BU_KW>(p, cs, it * BU_KW, nw, edges, reached, mfsum);
             }, flush);
-        } else if (mode == BFS_TDB) {
-            const uint64_t groups = (nw + 31) / 32;
-            r = claim_chunks(p, cs, *this, &p.ctl->chunk[in], (uint32_t)((groups + WPB - 1) / WPB), [&](uint32_t ch) {
-                const uint64_t g = (uint64_t)ch * WPB + warp;
-                if (g < groups) tdb_group(p, cs, g, fnext, edges, reached, mfsum);
+        } else if (mode == BFS_TDB) {                         // item = 32 frontier words
+            r = claim_items<BLOCK>(p, cs, *this, &p.ctl->chunk[in], (nw + 31) / 32, 4u * WPB, [&](uint64_t g) {
+                tdb_group(p, cs, g, fnext, edges, reached, mfsum, res);
             }, flush);
-        } else {
-            expand_heavy(p, cs, gw, TW, fnext, edges, reached, mfsum);
-            const uint64_t groups = ((uint64_t)cs.app_u32[0] + 31) / 32;
-            r = claim_chunks(p, cs, *this, &p.ctl->chunk[in], (uint32_t)((groups + WPB - 1) / WPB), [&](uint32_t ch) {
-                const uint64_t g = (uint64_t)ch * WPB + warp;
-                if (g < groups) tdq_group(p, cs, g, fnext, edges, reached, mfsum);
-            }, flush);
+        } else {                                              // item = 32 light frontier entries
+            expand_heavy(p, cs, gw, TW, fnext, edges, reached, mfsum, res);
+            r = claim_items<BLOCK>(p, cs, *this, &p.ctl->chunk[in], ((uint64_t)cs.app_u32[0] + 31) / 32, 4u * WPB,
+                            [&](uint64_t g) { tdq_group(p, cs, g, fnext, edges, reached, mfsum, res); }, flush);
         }
         if (r == ACT_CONT) flush();
         return r;
@@ -436,7 +507,7 @@ struct BfsApp {
     // Fig. 4 between the barriers: reset(out_nodes); per-level statistics; the
     // direction of the next level (Beamer: TD->BU if m_f > m_u/alpha, BU->TD if
     // n_f < V/beta)
-    __device__ void serial(const KParams &p, CtaState &cs, uint32_t entry, bool resizing) {
+    __device__ __noinline__ void serial(const KParams &p, CtaState &cs, uint32_t entry, bool resizing) {
         if (!resizing || entry != ENTRY_AFTER_RB1) return;
         Ctl *c = p.ctl;
         const uint32_t in = cs.in_sel, out = in ^ 1u;        // post-swap selectors
@@ -456,6 +527,7 @@ struct BfsApp {
             if (mode == BFS_BU) c->n_bu_levels += 1;
         }
         c->bmode[in] = mode;
+        if (cs.level < p.level_cap) p.level_t[cs.level] = globaltimer();   // level L's expand done
         if (nf) {
             const uint32_t L = cs.level + 1;
             if (L < p.level_cap) p.level_sizes[L] = (uint32_t)nf;
@@ -506,11 +578,14 @@ struct SsspApp {
     __device__ bool empty(const KParams &p, CtaState &cs) {
         if (threadIdx.x == 0) {
             const Ctl *c = p.ctl;
-            cs.app_u32[0] = ld_relaxed32(&c->qsize[cs.in_sel]);
-            cs.app_u32[5] = ld_relaxed32(&c->smode[cs.in_sel]);
-            cs.app_u32[1] = ld_relaxed32(&c->far_sel);
-            cs.app_u32[2] = min(ld_relaxed32(&c->far_size[cs.app_u32[1]]), p.far_cap);
-            const unsigned long long T = ld_relaxed64(&c->T), Tlo = ld_relaxed64(&c->T_lo);
+            // plain loads after the barrier's acquire (overlapping round trips)
+            const uint32_t q = c->qsize[cs.in_sel], m = c->smode[cs.in_sel], fs = c->far_sel;
+            const uint32_t f0 = c->far_size[0], f1 = c->far_size[1];
+            const unsigned long long T = c->T, Tlo = c->T_lo;
+            cs.app_u32[0] = q;
+            cs.app_u32[5] = m;
+            cs.app_u32[1] = fs;
+            cs.app_u32[2] = min(fs ? f1 : f0, p.far_cap);
             cs.app_u32[3] = (uint32_t)T;
             cs.app_u32[4] = (uint32_t)(T >> 32);
             cs.app_u32[6] = (uint32_t)Tlo;
@@ -553,7 +628,7 @@ struct SsspApp {
     }
 
     // worklist entries [32g, 32g+32): relax their out-edges (warp-wide gather)
-    __device__ void relax_group(const KParams &p, CtaState &cs, uint64_t g, uint64_t &edges) {
+    __device__ __forceinline__ void relax_group(const KParams &p, CtaState &cs, uint64_t g, uint64_t &edges) {
         const uint32_t lane = threadIdx.x & 31;
         const uint32_t in = cs.in_sel, out = in ^ 1u;
         const uint32_t r1 = cs.level + 1;
@@ -610,7 +685,7 @@ struct SsspApp {
     // section raised T from Tlo); dist < Tlo means the vertex already went through a
     // near worklist after its last improvement (stale copy: dropped); the rest is
     // compacted into the other far buffer
-    __device__ void drain_group(const KParams &p, CtaState &cs, uint64_t g) {
+    __device__ __forceinline__ void drain_group(const KParams &p, CtaState &cs, uint64_t g) {
         const uint32_t lane = threadIdx.x & 31;
         const uint32_t out = cs.in_sel ^ 1u;
         const uint32_t r1 = cs.level + 1;
@@ -647,11 +722,8 @@ struct SsspApp {
         };
         const bool drain = cs.app_u32[5] == SSSP_DRAIN;
         const uint64_t items = drain ? cs.app_u32[2] : cs.app_u32[0];
-        const uint64_t groups = (items + 31) / 32;
-        const uint32_t r = claim_chunks(p, cs, *this, &p.ctl->chunk[cs.in_sel], (uint32_t)((groups + WPB - 1) / WPB),
-                                        [&](uint32_t ch) {
-            const uint64_t g = (uint64_t)ch * WPB + warp;
-            if (g >= groups) return;
+        const uint32_t r = claim_items<BLOCK>(p, cs, *this, &p.ctl->chunk[cs.in_sel], (items + 31) / 32, 2u * WPB,
+                                       [&](uint64_t g) {
             if (drain) drain_group(p, cs, g);
             else relax_group(p, cs, g, edges);
         }, flush);
@@ -691,6 +763,7 @@ struct SsspApp {
             }
         }
         c->smode[in] = mode;
+        if (cs.level < p.level_cap) p.level_t[cs.level] = globaltimer();
         if (n) {
             const uint32_t L = cs.level + 1;
             if (L < p.level_cap) p.level_sizes[L] = n;

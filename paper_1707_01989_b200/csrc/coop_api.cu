@@ -133,7 +133,7 @@ struct DevBuf {
 
 struct Scratch {
     int device = -1;
-    DevBuf ctl, mb, visited, qlev, ql0, ql1, qh0, qh1, stamp, mtrace, lsizes, events, script, wmax, fb0, fb1, fb2,
+    DevBuf ctl, lt, mb, visited, qlev, ql0, ql1, qh0, qh1, stamp, mtrace, lsizes, events, script, wmax, fb0, fb1, fb2,
         far0, far1;
     DevBuf h_ro, h_col, h_w, h_out;   // end-to-end (host-pointer) calls
     Ctl *host_ctl = nullptr;          // pinned staging
@@ -233,6 +233,15 @@ static coop_status fill_stats(const Ctl &c, const KParams &kp, coop_stats *st, c
         uint32_t n = std::min(st->level_sizes_cap, std::min(c.levels + 1, kp.level_cap));
         if (n) CUDA_TRY(cudaMemcpyAsync(st->level_sizes, kp.level_sizes, n * 4, cudaMemcpyDeviceToHost, stream));
     }
+    if (st->level_end_ns && st->level_end_ns_cap) {
+        uint32_t n = std::min(st->level_end_ns_cap, std::min(c.levels, kp.level_cap));
+        std::vector<unsigned long long> tmp(n);
+        if (n) {
+            CUDA_TRY(cudaMemcpyAsync(tmp.data(), kp.level_t, n * 8, cudaMemcpyDeviceToHost, stream));
+            CUDA_TRY(cudaStreamSynchronize(stream));
+        }
+        for (uint32_t i = 0; i < n; ++i) st->level_end_ns[i] = tmp[i] > c.t_start ? tmp[i] - c.t_start : 0;
+    }
     if (st->task_events && st->task_events_cap) {
         uint32_t n = std::min(st->task_events_cap, c.n_events);
         std::vector<TaskEventDev> tmp(n);
@@ -327,6 +336,14 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
             pp.F[q][1] = pt->frontier[q][1];
             pp.flags[q] = reinterpret_cast<unsigned long long *>(pt->flags[q]);
         }
+        if (o.flags & COOP_FLAG_DIROPT) {
+            if (!pt->rows_offsets || (!pt->rows_col && pt->v_end > pt->v_begin) || pt->num_edges_global <= 0)
+                return fail(COOP_ERR_INVALID_ARG, "COOP_FLAG_DIROPT needs rows_offsets / rows_col / num_edges_global");
+            pp.rro = pt->rows_offsets;
+            pp.rcol = pt->rows_col;
+            pp.E_global = pt->num_edges_global;
+            kp.dopt = 1;
+        }
     } else if (r.app != APP_BARRIER) {
         const coop_csr *g = r.g;
         if (!g) return fail(COOP_ERR_INVALID_ARG, "graph is NULL");
@@ -403,12 +420,17 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
     const uint32_t mcap = 1u << 16, lcap = 1u << 16, ecap = 4096;
     CUDA_TRY(s->mtrace.ensure(4ull * mcap));
     CUDA_TRY(s->lsizes.ensure(4ull * lcap));
+    CUDA_TRY(s->lt.ensure(8ull * lcap));
     CUDA_TRY(s->events.ensure(sizeof(TaskEventDev) * ecap));
     if (r.app == APP_BFS) {
         const size_t le = off64 ? sizeof(LightEntry64) : sizeof(LightEntry);
+        // light queues: per-warp reservations of 256 slots may leave holes (empty
+        // entries): at most one partly used reservation per refill (< 128 unused
+        // slots, refills hold >= 128 entries) plus one open reservation per warp
+        const size_t qcap = 2 * V + (size_t)kMaxCtas * 32 * 256;
         CUDA_TRY(s->visited.ensure(4 * ((V + 31) / 32)));
-        CUDA_TRY(s->ql0.ensure(le * V));
-        CUDA_TRY(s->ql1.ensure(le * V));
+        CUDA_TRY(s->ql0.ensure(le * qcap));
+        CUDA_TRY(s->ql1.ensure(le * qcap));
         const size_t nh = E / kHeavyDeg + 1;
         CUDA_TRY(s->qh0.ensure(sizeof(HeavyEntry) * nh));
         CUDA_TRY(s->qh1.ensure(sizeof(HeavyEntry) * nh));
@@ -423,8 +445,6 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
             kp.fbits[2] = static_cast<uint32_t *>(s->fb2.p);
             kp.dopt = 1;
         }
-        kp.alpha = 14;
-        kp.beta = 24;
         kp.qheavy[0] = static_cast<HeavyEntry *>(s->qh0.p);
         kp.qheavy[1] = static_cast<HeavyEntry *>(s->qh1.p);
     } else if (r.app == APP_PBFS) {
@@ -453,6 +473,7 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
     kp.m_trace = static_cast<uint32_t *>(s->mtrace.p);
     kp.m_trace_cap = mcap;
     kp.level_sizes = static_cast<uint32_t *>(s->lsizes.p);
+    kp.level_t = static_cast<unsigned long long *>(s->lt.p);
     kp.level_cap = lcap;
     kp.events = static_cast<TaskEventDev *>(s->events.p);
     kp.events_cap = ecap;
@@ -464,6 +485,8 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
         kp.script_len = o.script_len;
     }
     kp.host = r.host;
+    kp.alpha = 14;                       // Beamer's direction-switch thresholds
+    kp.beta = 24;
     kp.P = P;
     kp.M0 = M0;
     kp.policy = plain ? COOP_POLICY_NEVER : o.policy;

@@ -108,6 +108,8 @@ struct __align__(128) Ctl {
     unsigned long long pcount[2];      // owned vertices discovered per level parity (this rank)
     unsigned long long gcount;         // vertices in the global frontier of the current level (all ranks)
     unsigned long long xwait_ns;       // time spent in the cross-GPU flag exchange
+    unsigned long long pmf[2];         // sum of the degrees of the owned vertices discovered (per parity)
+    uint32_t pmode;                    // BFS_TDB / BFS_BU of the next level (identical on every rank)
     uint32_t pad_p[24];
     // SSSP near-far
     unsigned long long T;              // near threshold
@@ -133,7 +135,10 @@ struct PartParams {
     const uint32_t *hub_ids;
     const unsigned long long *hub_prefix;        // nhub + 1 local-edge prefix over the hubs
     uint32_t *F[kMaxRanks][2];         // F[q][b]: rank q's copy of global frontier bitmap b
-    unsigned long long *flags[kMaxRanks];        // rank q's flag block [kMaxRanks][2]
+    unsigned long long *flags[kMaxRanks];        // rank q's flag block [kMaxRanks][2 parity][2 words]
+    const void *rro;                   // direction optimisation: owned rows (v_end - v_begin + 1 offsets)
+    const int32_t *rcol;               //   their neighbours (global ids)
+    int64_t E_global;                  //   directed edges of the whole graph (Beamer's m_u)
 };
 
 // Host -> GPU packet channel (host-mapped pinned memory; the paper's SVM atomics).
@@ -173,6 +178,7 @@ struct KParams {
     uint32_t far_cap;           // entries per far pile
     uint32_t *m_trace; uint32_t m_trace_cap;
     uint32_t *level_sizes; uint32_t level_cap;
+    unsigned long long *level_t;  // globaltimer at the end of each level's expand (RB1 serial section)
     TaskEventDev *events; uint32_t events_cap;
     const uint32_t *script; uint32_t script_len;
     HostChannel *host;          // host-mapped channel or nullptr

@@ -154,7 +154,11 @@ struct CtaState {
     uint64_t deadline;
     unsigned long long edges, frontier, reached;   // per-CTA stats, flushed at body exit
     uint32_t bar_M, bar_naive;                     // barrier: M of the episode, killed on entry (NAIVE)
-    uint32_t chunk, stop;                          // chunk loop broadcast
+    uint32_t chunk, stop, item_next;               // chunk loop broadcast / per-warp item counter
+#if COOP_TRACE
+    unsigned long long tr[12];
+    long long tr_last;
+#endif
     unsigned long long acc[2];                     // app counters flushed before a mid-interval kill
     uint32_t app_u32[8];                           // app broadcast scratch
 };
@@ -178,7 +182,7 @@ __device__ __forceinline__ uint32_t mhist_get(const KParams &p, uint32_t gen);
 // Warp-collective: claim up to k idle parked CTAs from the pool and assign
 // them logical ids M, M+1, ... with the transmit state of WG 0.
 // With `wait`, keeps trying until k are found (killed CTAs park promptly).
-__device__ uint32_t fork_from_pool(const KParams &p, const CtaState &cs, uint32_t gnext, uint32_t M,
+__device__ __noinline__ uint32_t fork_from_pool(const KParams &p, const CtaState &cs, uint32_t gnext, uint32_t M,
                                    uint32_t k, uint32_t entry, const Transmit &tx0, bool wait) {
     const uint32_t lane = threadIdx.x & 31;
     Ctl *c = p.ctl;
@@ -469,17 +473,17 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
         __syncthreads();
     }
 #if COOP_TRACE
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {               // shared-memory sums: no global traffic
         long long tr4 = clock64();
-        unsigned long long *T = c->trace;
-        const int o = cs.last ? 8 : 0;                       // [0..7] waiter, [8..15] last arriver
-        atomicAdd(T + o + 0, (unsigned long long)(tr1 - tr0));   // entry __syncthreads
-        atomicAdd(T + o + 1, (unsigned long long)(tr2 - tr1));   // arrival (fence + atomic)
-        atomicAdd(T + o + 2, (unsigned long long)(tr3 - tr2));   // wait for release
-        atomicAdd(T + o + 3, (unsigned long long)(tr4 - tr3));   // serial section + exit sync
-        atomicAdd(T + o + 4, (unsigned long long)(tr0 - (long long)c->trace_last));   // interval before barrier
-        atomicAdd(T + o + 5, 1ull);
-        c->trace_last = (unsigned long long)tr4;
+        unsigned long long *T = cs.tr;
+        const int o = cs.last ? 6 : 0;                       // [0..5] waiter, [6..11] last arriver
+        T[o + 0] += tr1 - tr0;                               // entry __syncthreads
+        T[o + 1] += tr2 - tr1;                               // arrival (fence + atomic)
+        T[o + 2] += tr3 - tr2;                               // wait for release
+        T[o + 3] += tr4 - tr3;                               // serial section + exit sync
+        if (cs.tr_last) T[o + 4] += tr0 - cs.tr_last;        // interval before the barrier
+        T[o + 5] += 1;
+        cs.tr_last = tr4;
     }
 #endif
     return cs.action;
@@ -495,7 +499,7 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
 // Returns ACT_KILLED, ACT_CONT (resume claiming) or ACT_ABORT.  `flush` is
 // called (CTA-collective) before the CTA can be counted out.
 template <class App, class Flush>
-__device__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, App &app, Flush &&flush) {
+__device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, App &app, Flush &&flush) {
     Ctl *c = p.ctl;
     flush();
     __syncthreads();
@@ -560,14 +564,30 @@ __device__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, App &app, Flu
     }
 }
 
-// Dynamic work distribution of an interval: CTAs claim chunk ids from
-// `counter` until `nchunks`; with the SCHEDULER policy every claim also reads
-// the resource channel and, when this id is asked to surrender, the CTA offers
-// itself (offer_kill_mid) right after finishing the chunk in hand.
-template <class App, class Fn, class Flush>
-__device__ uint32_t claim_chunks(const KParams &p, CtaState &cs, App &app, uint32_t *counter, uint32_t nchunks,
-                                 Fn &&fn, Flush &&flush) {
+// Dynamic work distribution of an interval over `n_items` warp-sized items:
+// a CTA claims a chunk of `per_chunk` items from `counter`, its warps take the
+// chunk's items one at a time from a shared-memory counter (so a warp waits at
+// most one item for its siblings), then the CTA claims again.  With the
+// SCHEDULER policy every claim also reads the resource channel and, when this
+// id is asked to surrender, the CTA offers itself (offer_kill_mid) right after
+// finishing the chunk in hand.  fn(item) is warp-collective.
+template <int BLOCK, class App, class Fn, class Flush>
+__device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32_t *counter, uint64_t n_items,
+                                uint32_t per_chunk, Fn &&fn, Flush &&flush) {
     const bool midkill = p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY;
+    const uint32_t lane = threadIdx.x & 31;
+    if (!midkill) {
+        // no scheduler can ask for workgroups inside this interval: Fig. 4's static
+        // distribution, item i to warp i mod (M*W) -- no atomics, no syncs
+        constexpr uint32_t WPB = BLOCK / 32;
+        const uint64_t TW = (uint64_t)cs.M * WPB;
+        for (uint64_t it = (uint64_t)cs.lid * WPB + (threadIdx.x >> 5); it < n_items; it += TW) fn(it);
+        (void)counter;
+        (void)per_chunk;
+        (void)lane;
+        return ACT_CONT;
+    }
+    const uint64_t nchunks = (n_items + per_chunk - 1) / per_chunk;
     for (;;) {
         if (threadIdx.x == 0) {
             const uint32_t ch = atomicAdd(counter, 1u);
@@ -578,11 +598,22 @@ __device__ uint32_t claim_chunks(const KParams &p, CtaState &cs, App &app, uint3
             }
             cs.chunk = ch;
             cs.stop = stop;
+            cs.item_next = 0;
         }
         __syncthreads();
         const uint32_t ch = cs.chunk, stop = cs.stop;
-        __syncthreads();
-        if (ch < nchunks) fn(ch);
+        if (ch < nchunks) {
+            const uint64_t base = (uint64_t)ch * per_chunk;
+            const uint32_t cnt = (uint32_t)min((uint64_t)per_chunk, n_items - base);
+            for (;;) {
+                uint32_t it = 0;
+                if (lane == 0) it = atomicAdd(&cs.item_next, 1u);
+                it = __shfl_sync(FULL, it, 0);
+                if (it >= cnt) break;
+                fn(base + it);
+            }
+        }
+        __syncthreads();                                   // chunk done; cs.chunk reusable
         if (stop) {
             const uint32_t r = offer_kill_mid(p, cs, app, flush);
             if (r != ACT_CONT) return r;
@@ -610,6 +641,7 @@ __device__ uint32_t run_body(const KParams &p, CtaState &cs, App &app, uint32_t 
             if (app.empty(p, cs)) return ACT_DONE;            // while (in_nodes.size > 0)
             r = app.template expand<BLOCK>(p, cs);             // for (i = tid; ...) process_node
             if (r != ACT_CONT) return r;                       // killed at a chunk boundary (offer_kill)
+            __syncthreads();                                   // every warp is done reading cs
             if (threadIdx.x == 0) cs.in_sel ^= 1u;            // swap(&in_nodes, &out_nodes)
             r = barrier(p, cs, app, true, ENTRY_AFTER_RB1);   // resizing_global_barrier() #1
             if (r != ACT_CONT) return r;
@@ -638,7 +670,7 @@ __device__ __forceinline__ void flush_stats(const KParams &p, CtaState &cs) {
 // ---------------------------------------------------------------- tasks
 // One block of the synthetic non-cooperative task (K11: occupies a workgroup
 // for a fixed time).  Thread 0 spins on %globaltimer.
-__device__ void run_task_block(const KParams &p, CtaState &cs) {
+__device__ __noinline__ void run_task_block(const KParams &p, CtaState &cs) {
     if (threadIdx.x == 0) {
         Ctl *c = p.ctl;
         uint64_t t0 = globaltimer();
@@ -659,7 +691,7 @@ __device__ void run_task_block(const KParams &p, CtaState &cs) {
 }
 
 // ---------------------------------------------------------------- scheduler CTA
-__device__ void scheduler_loop(const KParams &p, CtaState &cs) {
+__device__ __noinline__ void scheduler_loop(const KParams &p, CtaState &cs) {
     if (threadIdx.x != 0) return;
     Ctl *c = p.ctl;
     const uint64_t t0 = globaltimer();
@@ -734,7 +766,7 @@ __device__ void scheduler_loop(const KParams &p, CtaState &cs) {
 // The megakernel worker pool: wait for a fork assignment,
 // otherwise run blocks of the competing task; exit at termination.
 template <class App, int BLOCK>
-__device__ void park_loop(const KParams &p, CtaState &cs, App &app) {
+__device__ __noinline__ void park_loop(const KParams &p, CtaState &cs, App &app) {
     Ctl *c = p.ctl;
     const uint32_t phys = blockIdx.x;
     const uint32_t wi = phys >> 5, bit = 1u << (phys & 31);
@@ -812,6 +844,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(KParams p) {
     App app;
     if (threadIdx.x == 0) {
         const uint64_t t0 = globaltimer();
+#if COOP_TRACE
+        for (int i = 0; i < 12; ++i) cs.tr[i] = 0;
+        cs.tr_last = 0;
+#endif
         cs.deadline = t0 + p.timeout_ns;
         cs.edges = cs.frontier = cs.reached = 0;
         cs.consumed = 0;
@@ -828,17 +864,19 @@ __global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(KParams p) {
                 p.ctl->t_end = globaltimer();
                 st_release32(&p.ctl->done, 1);
             }
-            if (p.barrier_mode == COOP_BARRIER_PLAIN) return;
         }
         if (r == ACT_ABORT) return;
-        if (threadIdx.x == 0) {   // killed or finished: join the worker pool
+        if (p.barrier_mode != COOP_BARRIER_PLAIN && threadIdx.x == 0) {   // killed or finished: join the pool
             __threadfence();
             atomicOr(&p.ctl->pool[blockIdx.x >> 5], 1u << (blockIdx.x & 31));
         }
         __syncthreads();
     }
-    if (p.barrier_mode == COOP_BARRIER_PLAIN) return;
-    park_loop<App, BLOCK>(p, cs, app);
+    if (p.barrier_mode != COOP_BARRIER_PLAIN) park_loop<App, BLOCK>(p, cs, app);
+#if COOP_TRACE
+    if (threadIdx.x == 0 && blockIdx.x == 0)
+        for (int i = 0; i < 12; ++i) p.ctl->trace[i + (i >= 6 ? 2 : 0)] = cs.tr[i];
+#endif
 }
 
 }  // namespace coop

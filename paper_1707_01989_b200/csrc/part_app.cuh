@@ -19,6 +19,11 @@
 //            the size of the next global frontier (0 = terminate everywhere)
 // Static hubs (local degree >= hub_deg) are processed edge-balanced over
 // all warps so one hub cannot stall a level.
+// With COOP_FLAG_DIROPT (and the owned rows of the symmetric graph) a level
+// can run bottom-up instead: each owned unvisited vertex scans its neighbours
+// for one in the (complete) global frontier bitmap.  The direction is chosen
+// by Beamer's rule from the GLOBAL n_f / m_f exchanged with the counts, so
+// every rank picks the same one.
 #pragma once
 #include "apps.cuh"
 
@@ -40,8 +45,20 @@ struct PartBfsApp {
         for (uint64_t i = tid; i < nown; i += nth) p.level_out[i] = (int64_t)i + pp.vb == s ? 0 : -1;
         const uint64_t nlw = (nown + 31) / 32;
         const bool own_s = s >= pp.vb && s < pp.ve;
-        for (uint64_t i = tid; i < nlw; i += nth)
-            p.visited[i] = (own_s && i == (uint64_t)((s - pp.vb) >> 5)) ? (1u << ((s - pp.vb) & 31)) : 0u;
+        if (p.dopt) {   // owned degree-0 vertices start visited (bottom-up skips them; symmetric graph)
+            const OffT *rro = static_cast<const OffT *>(pp.rro);
+            const uint32_t lane = threadIdx.x & 31;
+            for (uint64_t w = tid / 32; w < nlw; w += nth / 32) {
+                const uint64_t v = w * 32 + lane;
+                const bool d0 = v < nown && __ldg(rro + v + 1) == __ldg(rro + v);
+                const uint32_t m = __ballot_sync(FULL, d0);
+                if (lane == 0)
+                    p.visited[w] = m | ((own_s && w == (uint64_t)((s - pp.vb) >> 5)) ? (1u << ((s - pp.vb) & 31)) : 0u);
+            }
+        } else {
+            for (uint64_t i = tid; i < nlw; i += nth)
+                p.visited[i] = (own_s && i == (uint64_t)((s - pp.vb) >> 5)) ? (1u << ((s - pp.vb) & 31)) : 0u;
+        }
         const uint64_t nw = ((uint64_t)p.V + 31) / 32;
         uint32_t *F0 = pp.F[pp.rank][0], *F1 = pp.F[pp.rank][1];
         for (uint64_t i = tid; i < nw; i += nth) {     // every rank knows the source (level 0 frontier)
@@ -49,6 +66,11 @@ struct PartBfsApp {
             F1[i] = 0u;
         }
         if (cs.lid == 0 && threadIdx.x == 0) {
+            if (own_s && p.dopt) {   // the source's degree, summed over ranks in the init exchange
+                const OffT *rro = static_cast<const OffT *>(pp.rro);
+                p.ctl->pmf[0] = (unsigned long long)(rro[s - pp.vb + 1] - rro[s - pp.vb]);
+            }
+            p.ctl->pmode = BFS_TDB;
             p.ctl->gcount = 1;
             p.ctl->frontier_total = 1;
             p.ctl->levels = 1;
@@ -58,14 +80,17 @@ struct PartBfsApp {
     }
 
     __device__ bool empty(const KParams &p, CtaState &cs) {
-        if (threadIdx.x == 0) cs.app_u32[0] = ld_relaxed64(&p.ctl->gcount) ? 1u : 0u;
+        if (threadIdx.x == 0) {
+            cs.app_u32[0] = p.ctl->gcount ? 1u : 0u;
+            cs.app_u32[5] = p.ctl->pmode;
+        }
         __syncthreads();
         return cs.app_u32[0] == 0;
     }
 
     // claim owned targets t (local ids) -- warp-collective, batch of K per lane
     __device__ __forceinline__ void claim(const KParams &p, const int32_t (&t)[KB], uint32_t L1, uint32_t *fnext,
-                                          uint32_t &won) {
+                                          uint32_t &won, unsigned long long &mf) {
         uint32_t *vis = p.visited;
         uint32_t cur[KB];
 #pragma unroll
@@ -79,7 +104,67 @@ struct PartBfsApp {
             const uint64_t g = (uint64_t)p.part.vb + (uint32_t)t[k];
             atomicOr(fnext + (g >> 5), 1u << (g & 31));
             ++won;
+            if (p.dopt) {
+                const OffT *rro = static_cast<const OffT *>(p.part.rro);
+                mf += (unsigned long long)(__ldg(rro + t[k] + 1) - __ldg(rro + t[k]));
+            }
         }
+    }
+
+    // bottom-up over the owned words: warp per 32 owned vertices, each unvisited
+    // vertex scans its (global) neighbour list for a bit of the global frontier
+    template <int BLOCK>
+    __device__ void bottom_up(const KParams &p, CtaState &cs, uint64_t gw, uint64_t TW, uint64_t &edges,
+                              uint32_t &won, unsigned long long &mf) {
+        const PartParams &pp = p.part;
+        const uint32_t lane = threadIdx.x & 31;
+        const uint32_t L = cs.level, L1 = L + 1;
+        const uint32_t *fcur = pp.F[pp.rank][L & 1];
+        uint32_t *fnext = pp.F[pp.rank][L1 & 1];
+        const OffT *rro = static_cast<const OffT *>(pp.rro);
+        const int32_t *__restrict__ rcol = pp.rcol;
+        const uint64_t nown = (uint64_t)(pp.ve - pp.vb);
+        const uint64_t nlw = (nown + 31) / 32;
+        const uint64_t gw0 = (uint64_t)pp.vb / 32;
+        uint64_t scanned_total = 0;
+        for (uint64_t w = gw; w < nlw; w += TW) {
+            const uint32_t vw = ldcg(p.visited + w);
+            if (vw == 0xFFFFFFFFu) continue;
+            const uint64_t v = w * 32 + lane;
+            const bool open = v < nown && !((vw >> lane) & 1u);
+            OffT b = 0, e = 0;
+            if (open) {
+                b = __ldg(rro + v);
+                e = __ldg(rro + v + 1);
+            }
+            const uint32_t deg = (uint32_t)(e - b);
+            bool found = false;
+            while (open && b < e && !found) {
+                int32_t u[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) u[k] = b + k < e ? __ldg(rcol + b + k) : -1;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (u[k] >= 0 && ((ldcg(fcur + ((uint32_t)u[k] >> 5)) >> (u[k] & 31)) & 1u)) found = true;
+                const uint32_t nstep = (uint32_t)min((OffT)4, (OffT)(e - b));
+                scanned_total += nstep;
+                b += nstep;
+            }
+            const uint32_t wins = __ballot_sync(FULL, found);
+            if (found) {
+                p.level_out[v] = (int32_t)L1;
+                mf += deg;
+                ++won;
+            }
+            if (wins && lane == 0) {
+                p.visited[w] = vw | wins;
+                fnext[gw0 + w] = wins;          // own slice word of the next global frontier
+            }
+        }
+        // per-lane scans -> warp-uniform edge count (the caller adds `edges` once per warp)
+#pragma unroll
+        for (int s = 16; s; s >>= 1) scanned_total += __shfl_xor_sync(FULL, scanned_total, s);
+        edges += scanned_total;
     }
 
     template <int BLOCK>
@@ -96,6 +181,10 @@ struct PartBfsApp {
         const uint64_t nw = ((uint64_t)p.V + 31) / 32;
         uint64_t edges = 0;
         uint32_t won = 0;
+        unsigned long long mf = 0;
+        if (cs.app_u32[5] == BFS_BU) {
+            bottom_up<BLOCK>(p, cs, gw, TW, edges, won, mf);
+        } else {
         // ---- frontier vertices from the bitmap, lane l owns word base+l
         for (uint64_t base = gw * 32; base < nw; base += TW * 32) {
             const uint64_t wi = base + lane;
@@ -130,7 +219,7 @@ struct PartBfsApp {
                         const uint32_t ex = __shfl_sync(FULL, excl, j);
                         t[k] = e < total ? __ldg(col + b + (e - ex)) : -1;
                     }
-                    claim(p, t, L1, fnext, won);
+                    claim(p, t, L1, fnext, won, mf);
                 }
             }
         }
@@ -160,20 +249,25 @@ struct PartBfsApp {
                             const uint64_t e = ws + 32 * k + lane;
                             t[k] = e < z ? __ldg(col + rb + (e - hp)) : -1;
                         }
-                        claim(p, t, L1, fnext, won);
+                        claim(p, t, L1, fnext, won, mf);
                     }
                 }
             }
         }
+        }   // top-down
 #pragma unroll
-        for (int s = 16; s; s >>= 1) won += __shfl_xor_sync(FULL, won, s);
-        if (lane == 0) {   // edges is warp-uniform, won was per lane
+        for (int s = 16; s; s >>= 1) {
+            won += __shfl_xor_sync(FULL, won, s);
+            mf += __shfl_xor_sync(FULL, mf, s);
+        }
+        if (lane == 0) {   // edges is warp-uniform, won / mf were per lane
             if (edges) atomicAdd(&cs.edges, (unsigned long long)edges);
             if (won) {
                 atomicAdd(&cs.reached, (unsigned long long)won);
                 atomicAdd(&p.ctl->pcount[L1 & 1], (unsigned long long)won);
-                __threadfence();   // RED, read by the RB2 serial section
             }
+            if (mf) atomicAdd(&p.ctl->pmf[L1 & 1], mf);
+            if (won || mf) __threadfence();   // REDs, read by the RB2 serial section
         }
         return ACT_CONT;
     }
@@ -207,23 +301,35 @@ struct PartBfsApp {
         __threadfence_system();
     }
 
+    // flag block of rank q: slot [r][parity] = {epoch << 32 | count, mf}; mf is
+    // written first and published by the release store of the epoch word
     __device__ __forceinline__ bool exchange(const KParams &p, const CtaState &cs, uint32_t epoch,
-                                             unsigned long long count, unsigned long long *total) {
+                                             unsigned long long count, unsigned long long mf,
+                                             unsigned long long *total, unsigned long long *mf_total) {
         const PartParams &pp = p.part;
         __threadfence_system();
         const unsigned long long word = ((unsigned long long)epoch << 32) | (count & 0xFFFFFFFFull);
-        for (int q = 0; q < pp.nranks; ++q) st_release_sys64(pp.flags[q] + pp.rank * 2 + (epoch & 1), word);
-        unsigned long long sum = 0;
+        const uint32_t slot = (uint32_t)pp.rank * 4 + (epoch & 1) * 2;
+        for (int q = 0; q < pp.nranks; ++q) {
+            asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(pp.flags[q] + slot + 1), "l"(mf) : "memory");
+            st_release_sys64(pp.flags[q] + slot, word);
+        }
+        unsigned long long sum = 0, msum = 0;
         const unsigned long long *mine = pp.flags[pp.rank];
         uint32_t spins = 0;
         for (int q = 0; q < pp.nranks; ++q) {
+            const uint32_t qs = (uint32_t)q * 4 + (epoch & 1) * 2;
             unsigned long long v;
-            while (((v = ld_acquire_sys64(mine + q * 2 + (epoch & 1))) >> 32) != epoch) {
+            while (((v = ld_acquire_sys64(mine + qs)) >> 32) != epoch) {
                 if (spin_check(p, cs, spins)) return false;
             }
             sum += v & 0xFFFFFFFFull;
+            unsigned long long m;
+            asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(m) : "l"(mine + qs + 1) : "memory");
+            msum += m;
         }
         *total = sum;
+        *mf_total = msum;
         return true;
     }
 
@@ -232,18 +338,33 @@ struct PartBfsApp {
         const uint32_t base = p.part.seq << 16;
         const uint64_t t0 = globaltimer();
         if (!resizing) {   // the init global barrier: every rank cleared its bitmaps before any peer writes
-            unsigned long long tot;
-            exchange(p, cs, base | 1u, 0, &tot);
+            unsigned long long tot, mf;
+            exchange(p, cs, base | 1u, 0, c->pmf[0], &tot, &mf);
+            c->pmf[0] = 0;
+            c->vis_edges = mf;                       // degree of the source
             c->xwait_ns += globaltimer() - t0;
             return;
         }
         if (entry != ENTRY_AFTER_RB2) return;
         const uint32_t L = cs.level;                 // level++ already done before RB2
-        const unsigned long long mine = c->pcount[L & 1];
-        unsigned long long tot = 0;
-        if (!exchange(p, cs, base | (L + 1), mine, &tot)) return;
+        const unsigned long long mine = c->pcount[L & 1], mymf = c->pmf[L & 1];
+        unsigned long long tot = 0, mf = 0;
+        if (!exchange(p, cs, base | (L + 1), mine, mymf, &tot, &mf)) return;
         c->pcount[L & 1] = 0;
+        c->pmf[L & 1] = 0;
         c->gcount = tot;
+        // direction of the next level from the global n_f, m_f (same on every rank)
+        const uint32_t prev = c->pmode;
+        c->vis_edges += mf;
+        uint32_t mode = BFS_TDB;
+        if (p.dopt) {
+            const unsigned long long Eg = (unsigned long long)p.part.E_global;
+            const unsigned long long mu = Eg - min(Eg, c->vis_edges);
+            if (prev == BFS_BU) mode = tot * p.beta < (unsigned long long)p.V ? BFS_TDB : BFS_BU;
+            else mode = mf * p.alpha > mu ? BFS_BU : BFS_TDB;
+            if (mode == BFS_BU) c->n_bu_levels += 1;
+        }
+        c->pmode = mode;
         c->xwait_ns += globaltimer() - t0;
         if (tot) {
             if (L < p.level_cap) p.level_sizes[L] = (uint32_t)tot;

@@ -64,6 +64,12 @@ class PartitionedBFS:
             self.ro = part.row_offsets.to(self.device, torch.int64).contiguous()
             self.bits = 64
         self.col = part.col_local.to(self.device, torch.int32).contiguous()
+        import graphgen as gg
+        rro, rcol = gg.part_rows(part)               # owned rows (bottom-up levels)
+        self.rro = rro.to(self.device, torch.int32 if self.bits == 32 else torch.int64).contiguous()
+        self.rcol = rcol.to(self.device).contiguous()
+        del rro, rcol
+        self.E_global = None                         # set by the caller (sum of num_edges over ranks)
         ids, pref = hubs_of(part, hub_degree)
         self.hub_ids = ids.to(self.device).contiguous()
         self.hub_pref = pref.to(self.device).contiguous()
@@ -76,7 +82,7 @@ class PartitionedBFS:
             f = ctypes.c_void_p()
             coop._check(lib.coop_exchange_alloc(2 * self.nwb, ctypes.byref(f)))
             g = ctypes.c_void_p()
-            coop._check(lib.coop_exchange_alloc(16 * MAX_RANKS, ctypes.byref(g)))
+            coop._check(lib.coop_exchange_alloc(32 * MAX_RANKS, ctypes.byref(g)))
         self.F_ptr, self.flags_ptr = f.value, g.value
         self.levels = torch.empty(max(1, part.v_end - part.v_begin), dtype=torch.int32, device=self.device)
         self.peer_F = [[None, None] for _ in range(MAX_RANKS)]
@@ -139,6 +145,9 @@ class PartitionedBFS:
         for q in range(self.part.nranks):
             s.frontier[q][0], s.frontier[q][1] = self.peer_F[q]
             s.flags[q] = self.peer_flags[q]
+        s.rows_offsets = self.rro.data_ptr()
+        s.rows_col = self.rcol.data_ptr() if self.rcol.numel() else None
+        s.num_edges_global = int(self.E_global) if self.E_global else 0
         return s
 
     def launch(self, source: int, *, seq: Optional[int] = None, **opts):
@@ -182,8 +191,10 @@ def simulate_one_gpu(g, P: int, source: int, *, threads: int = 256, ctas_per_ran
     import graphgen as gg
     if parts is None:
         parts = [PartitionedBFS(gg.partition(g, P, r), device) for r in range(P)]
+    Eg = sum(pb.part.num_edges for pb in parts)
     for pb in parts:
         pb.connect_local(parts)
+        pb.E_global = Eg
     info = coop.device_query(torch.device(device).index or 0, threads)
     n = ctas_per_rank or max(1, (info["max_coresident"] // P) // 2)
     streams = [torch.cuda.Stream(device=device) for _ in range(P)]

@@ -71,3 +71,25 @@ def test_partitioned_rmat_partition_generator(part):
     np.testing.assert_array_equal(lv.cpu().numpy(), tb.bfs(g, s))
     for pb in parts:
         pb.close()
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_partitioned_direction_optimising(part, P):
+    """Bottom-up levels on the owned rows, direction chosen from the globally
+    exchanged n_f / m_f: identical levels, and R-MAT triggers bottom-up."""
+    from paper_1707_01989_b200 import coop
+    g = gg.rmat(14, seed=6)
+    parts = None
+    for s in gg.sample_sources(g, 3):
+        lv, stats, parts = part.simulate_one_gpu(g, P, s, threads=256, ctas_per_rank=16, parts=parts,
+                                                 flags=coop.FLAG_DIROPT, level_cap=64)
+        ref = tb.bfs(g, s)
+        np.testing.assert_array_equal(lv.cpu().numpy(), ref)
+        assert stats[0].level_sizes == tb.level_sizes(ref)
+        assert len({st.bottom_up_levels for st in stats}) == 1      # same direction on every rank
+        assert stats[0].bottom_up_levels >= 1
+    g2 = gg.disjoint_union(gg.grid(30, 30), gg.star(3000))
+    lv, _, p2 = part.simulate_one_gpu(g2, P, 0, threads=256, ctas_per_rank=16, flags=coop.FLAG_DIROPT)
+    np.testing.assert_array_equal(lv.cpu().numpy(), tb.bfs(g2, 0))
+    for pb in parts + p2:
+        pb.close()

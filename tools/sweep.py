@@ -11,6 +11,9 @@ import torch  # noqa: E402
 import graphgen as gg  # noqa: E402
 from paper_1707_01989_b200 import coop  # noqa: E402
 
+if os.environ.get("COOP_LIB"):
+    coop.load(os.path.abspath(os.environ["COOP_LIB"]))
+
 
 def timed(fn, reps=3):
     ts = []
@@ -67,3 +70,15 @@ if what in ("all", "barrier_small"):
     for n in (1, 2, 4, 8, 16, 32, 64, 148):
         r = coop.barrier_bench(n, 100000, threads=128, plain=True)
         print(json.dumps({"barrier_ctas": n, "plain": True, "ns_per_barrier": r["ns_per_barrier"]}), flush=True)
+if what in ("all", "levels"):
+    g = gg.rmat(24, seed=1, device="cuda", chunk=1 << 26)
+    out = torch.empty(g.num_vertices, dtype=torch.int32, device="cuda")
+    for s in gg.sample_sources(g, 3, seed=2):
+        for flags in (coop.FLAG_DIROPT, 0):
+            for rep in range(2):
+                _, st = coop.bfs(g, s, out, threads_per_wg=512, flags=flags, level_cap=64)
+            ends = st.level_end_ns
+            per = [ends[0]] + [b - a for a, b in zip(ends, ends[1:])]
+            print(json.dumps({"levels": True, "src": s, "flags": flags, "kernel_us": st.kernel_ns / 1e3,
+                              "sizes": st.level_sizes, "level_us": [round(x / 1e3, 1) for x in per],
+                              "bu": st.bottom_up_levels, "edges": st.edges_scanned}), flush=True)
