@@ -110,6 +110,8 @@ typedef struct {
     void *ev_kernel_end;        /* optional cudaEvent_t recorded on `stream` right after it (kernel-only timing) */
     uint32_t workspace;         /* scratch set on the device (0..7): concurrent calls on one device need distinct ones */
     uint32_t sssp_delta;        /* SSSP near-far band width (0 = plain worklist Bellman-Ford); results identical */
+    uint32_t bfs_alpha;         /* COOP_FLAG_DIROPT: top-down -> bottom-up when m_f * alpha > m_u (0 = default) */
+    uint32_t bfs_beta;          /* COOP_FLAG_DIROPT: bottom-up -> top-down when n_f * beta < V (0 = default) */
 } coop_opts;
 
 /* One competing-task instance, all times from %globaltimer (ns). */

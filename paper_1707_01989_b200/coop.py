@@ -50,7 +50,8 @@ class Opts(ctypes.Structure):
                 ("task_first_ns", ctypes.c_uint64), ("task_max", ctypes.c_uint32),
                 ("timeout_ns", ctypes.c_uint64), ("stream", ctypes.c_void_p),
                 ("ev_kernel_start", ctypes.c_void_p), ("ev_kernel_end", ctypes.c_void_p),
-                ("workspace", ctypes.c_uint32), ("sssp_delta", ctypes.c_uint32)]
+                ("workspace", ctypes.c_uint32), ("sssp_delta", ctypes.c_uint32),
+                ("bfs_alpha", ctypes.c_uint32), ("bfs_beta", ctypes.c_uint32)]
 
 
 class TaskEvent(ctypes.Structure):
@@ -223,7 +224,8 @@ def _device_csr(g, need_weights: bool):
 def make_opts(*, max_wgs=0, init_wgs=0, threads_per_wg=0, barrier_mode=BARRIER_QUERY, barriers_per_level=1,
               policy=POLICY_NEVER, script: Optional[Sequence[int]] = None, flags=0, seed=0, resize_prob=0.0,
               task_wgs=0, task_blocks=0, task_block_ns=0, task_period_ns=0, task_first_ns=0, task_max=0,
-              timeout_ns=0, stream=None, ev_kernel_start=None, ev_kernel_end=None, workspace=0, sssp_delta=0):
+              timeout_ns=0, stream=None, ev_kernel_start=None, ev_kernel_end=None, workspace=0, sssp_delta=0,
+              bfs_alpha=0, bfs_beta=0):
     import torch
     o = Opts()
     o.max_wgs, o.init_wgs, o.threads_per_wg = max_wgs, init_wgs, threads_per_wg
@@ -242,6 +244,7 @@ def make_opts(*, max_wgs=0, init_wgs=0, threads_per_wg=0, barrier_mode=BARRIER_Q
     o.stream = stream
     o.workspace = workspace
     o.sssp_delta = sssp_delta
+    o.bfs_alpha, o.bfs_beta = bfs_alpha, bfs_beta
     if ev_kernel_start is not None:   # torch.cuda.Event(enable_timing=True)
         o.ev_kernel_start = ev_kernel_start.cuda_event
         o.ev_kernel_end = ev_kernel_end.cuda_event

@@ -18,7 +18,13 @@
 #include "coop_rt.cuh"
 
 #ifndef COOP_BU_KW
-#define COOP_BU_KW 4
+#define COOP_BU_KW 4          // bottom-up: 32-vertex words per warp item
+#endif
+#ifndef COOP_BU_EPS
+#define COOP_BU_EPS 1         // bottom-up: edges probed per list per step (first hits dominate)
+#endif
+#ifndef COOP_BU_PIPE
+#define COOP_BU_PIPE 0        // bottom-up: 1 = speculative offsets + next-item prefetch (static path)
 #endif
 
 namespace coop {
@@ -66,21 +72,8 @@ struct BfsApp {
         for (uint64_t i = h + 4 * nvec + tid; i < (uint64_t)V; i += nth) lv[i] = (int64_t)i == s ? 0 : -1;
         const uint64_t nw = ((uint64_t)V + 31) / 32;
         const uint32_t sw = (uint32_t)(s >> 5), sb = 1u << (s & 31);
-        if (p.dopt) {
-            // symmetric graph: a degree-0 vertex is never a neighbour, so it starts
-            // "visited" and bottom-up levels skip it; warp per word, lane per vertex
-            const OffT *rof = static_cast<const OffT *>(p.ro);
-            const uint32_t lane = threadIdx.x & 31;
-            const uint64_t TW = nth / 32;
-            for (uint64_t w = tid / 32; w < nw; w += TW) {
-                const uint64_t v = w * 32 + lane;
-                const bool deg0 = v < (uint64_t)V && __ldg(rof + v + 1) == __ldg(rof + v);
-                const uint32_t m = __ballot_sync(FULL, deg0);
-                if (lane == 0) p.visited[w] = m | (w == sw ? sb : 0u);
-            }
-        }
         for (uint64_t i = tid; i < nw; i += nth) {
-            if (!p.dopt) p.visited[i] = i == sw ? sb : 0u;
+            p.visited[i] = i == sw ? sb : 0u;
             if (p.dopt) {
                 p.fbits[0][i] = i == sw ? sb : 0u;
                 p.fbits[1][i] = 0u;
@@ -218,11 +211,40 @@ struct BfsApp {
                 }
             }
         }
+        // heavy winners: one packed {count, edges} atomic per warp batch (per-winner
+        // atomics on the single counter serialise: hub levels push 1e4-1e5 of them);
+        // entries take indices in (lane, k) order with prefix = running edge offset
+        uint32_t hcnt = 0;
+        uint64_t hdeg = 0;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             if (win[k] && nd[k] >= kHeavyDeg) {
-                const unsigned long long old = atomicAdd(&p.ctl->heavy[out], (1ull << 40) | nd[k]);
-                p.qheavy[out][old >> 40] = HeavyEntry{(uint64_t)nb[k], old & kMask40, nd[k], 0u};
+                hcnt += 1;
+                hdeg += nd[k];
+            }
+        }
+        if (__any_sync(FULL, hcnt != 0)) {
+            uint32_t ci = hcnt;
+            uint64_t di = hdeg;
+#pragma unroll
+            for (int s = 1; s < 32; s <<= 1) {
+                const uint32_t cn = __shfl_up_sync(FULL, ci, s);
+                const uint64_t dn = __shfl_up_sync(FULL, di, s);
+                if (lane >= (uint32_t)s) { ci += cn; di += dn; }
+            }
+            const uint32_t ctot = __shfl_sync(FULL, ci, 31);
+            const uint64_t dtot = __shfl_sync(FULL, di, 31);
+            unsigned long long old = 0;
+            if (lane == 0) old = atomicAdd(&p.ctl->heavy[out], ((unsigned long long)ctot << 40) | dtot);
+            old = __shfl_sync(FULL, old, 0);
+            uint64_t idx = (old >> 40) + (ci - hcnt), pre = (old & kMask40) + (di - hdeg);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if (win[k] && nd[k] >= kHeavyDeg) {
+                    p.qheavy[out][idx] = HeavyEntry{(uint64_t)nb[k], pre, nd[k], 0u};
+                    idx += 1;
+                    pre += nd[k];
+                }
             }
         }
     }
@@ -302,17 +324,17 @@ struct BfsApp {
     }
 
     // ---------------------------------------------------------- top-down, queue input (one group)
-    // warp group g: light entries [32g, 32g+32)
-    __device__ __forceinline__ void tdq_group(const KParams &p, CtaState &cs, uint64_t g, uint32_t *fnext, uint64_t &edges,
-                              uint32_t &reached, uint64_t &mfsum, uint2 &res) {
+    // warp group g: light entries [sz*g, sz*g + sz), sz <= 32 (one per lane)
+    __device__ __forceinline__ void tdq_group(const KParams &p, CtaState &cs, uint64_t g, uint32_t sz, uint32_t *fnext,
+                              uint64_t &edges, uint32_t &reached, uint64_t &mfsum, uint2 &res) {
         const uint32_t lane = threadIdx.x & 31;
         const uint32_t nl = cs.app_u32[0];
         const uint32_t in = cs.in_sel, out = in ^ 1u;
         const LE *inq = static_cast<const LE *>(p.qlight[in]);
-        const uint64_t i = g * 32 + lane;
+        const uint64_t i = g * sz + lane;
         OffT beg = 0;
         uint32_t deg = 0;
-        if (i < nl) {
+        if (lane < sz && i < nl) {
             LE e = inq[i];
             beg = e.beg;
             deg = e.deg;
@@ -346,68 +368,95 @@ struct BfsApp {
         }
     }
 
-    // ---------------------------------------------------------- bottom-up (one 32-vertex word)
+    // ---------------------------------------------------------- bottom-up (KW 32-vertex words)
     // each unvisited vertex scans its list (4 per step) for a parent in the
     // frontier bitmap and stops at the first hit.  The warp owns the visited /
     // next-frontier words, so no atomics.
     // KW consecutive words per warp item: lane l owns vertex (w0+k)*32 + l of
     // each word k, and all KW lists advance together (KW x 4 column loads and
-    // probes in flight per lane) -- the step is latency bound, so this is the
-    // lever, not bandwidth.
+    // probes in flight per lane).  The step is latency bound (visited + offsets ->
+    // columns -> frontier probe), so an item is split into a load half (bu_load:
+    // the visited words and the row offsets, issued speculatively for every lane,
+    // independent of each other) and a process half (bu_process), and the static
+    // driver (bu_pipelined) issues item i+1's loads before processing item i.
     template <int KW>
-    __device__ __forceinline__ void bu_words(const KParams &p, CtaState &cs, uint64_t w0, uint64_t nw,
-                                             uint64_t &edges, uint32_t &reached, uint64_t &mfsum) {
+    struct BuItem {
+        uint32_t vw[KW];   // visited words
+        OffT b[KW];        // ro[v] of this lane's vertex (v <= V)
+        OffT e31[KW];      // lane 31: ro[v + 1] (other lanes take the next lane's b)
+    };
+
+    // SPEC: offsets for every lane, independent of the visited words (one round
+    // trip less, but the offsets of fully visited words are read too); else the
+    // offsets of the unvisited lanes only, after the visited words arrive
+    template <int KW, bool SPEC>
+    __device__ __forceinline__ void bu_load(const KParams &p, uint64_t w0, uint64_t nw, BuItem<KW> &x) {
+        const uint32_t lane = threadIdx.x & 31;
+        const OffT *ro = static_cast<const OffT *>(p.ro);
+        const uint64_t V = (uint64_t)p.V;
+#pragma unroll
+        for (int k = 0; k < KW; ++k) x.vw[k] = w0 + k < nw ? p.visited[w0 + k] : 0xFFFFFFFFu;
+#pragma unroll
+        for (int k = 0; k < KW; ++k) {
+            const uint64_t v = (w0 + k) * 32 + lane;
+            const bool want = SPEC || (x.vw[k] != 0xFFFFFFFFu);
+            x.b[k] = (want && v <= V) ? __ldg(ro + v) : (OffT)0;
+            x.e31[k] = (want && lane == 31 && v < V) ? __ldg(ro + v + 1) : (OffT)0;
+        }
+    }
+
+    static constexpr int EPS = COOP_BU_EPS;
+
+    template <int KW>
+    __device__ __forceinline__ void bu_process(const KParams &p, CtaState &cs, uint64_t w0, const BuItem<KW> &x,
+                                               uint64_t &edges, uint32_t &reached, uint64_t &mfsum) {
         const uint32_t lane = threadIdx.x & 31;
         const uint32_t L1 = cs.level + 1;
         const uint32_t *fcur = p.fbits[cs.level % 3];
         uint32_t *fnext = p.fbits[L1 % 3];
-        const OffT *ro = static_cast<const OffT *>(p.ro);
         const int32_t *__restrict__ col = p.col;
         const uint64_t V = (uint64_t)p.V;
-        uint32_t vw[KW];
-#pragma unroll
-        for (int k = 0; k < KW; ++k) vw[k] = w0 + k < nw ? ldcg(p.visited + w0 + k) : 0xFFFFFFFFu;
         bool any_open = false;
 #pragma unroll
-        for (int k = 0; k < KW; ++k) any_open |= vw[k] != 0xFFFFFFFFu;
+        for (int k = 0; k < KW; ++k) any_open |= x.vw[k] != 0xFFFFFFFFu;
         if (!any_open) return;                                 // warp-uniform
         OffT b[KW], e[KW];
         bool found[KW];
+        uint32_t deg[KW], dead[KW];
 #pragma unroll
         for (int k = 0; k < KW; ++k) {
             const uint64_t v = (w0 + k) * 32 + lane;
-            b[k] = 0;
-            e[k] = 0;
+            const OffT nx = __shfl_down_sync(FULL, x.b[k], 1);
+            const bool open = v < V && !((x.vw[k] >> lane) & 1u);
+            b[k] = open ? x.b[k] : (OffT)0;
+            e[k] = open ? (lane == 31 ? x.e31[k] : nx) : (OffT)0;
             found[k] = false;
-            if (v < V && !((vw[k] >> lane) & 1u)) {
-                b[k] = __ldg(ro + v);
-                e[k] = __ldg(ro + v + 1);
-            }
+            deg[k] = (uint32_t)(e[k] - b[k]);
+            // unvisited and degree 0: never a neighbour (symmetric CSR), so it is
+            // retired here once and later bottom-up levels skip it
+            dead[k] = __ballot_sync(FULL, open && deg[k] == 0);
         }
-        uint32_t deg[KW];
-#pragma unroll
-        for (int k = 0; k < KW; ++k) deg[k] = (uint32_t)(e[k] - b[k]);
         uint32_t scanned = 0;
         for (;;) {
             bool more = false;
 #pragma unroll
             for (int k = 0; k < KW; ++k) more |= (b[k] < e[k] && !found[k]);
             if (!more) break;
-            int32_t u[KW][4];
+            int32_t u[KW][EPS];
 #pragma unroll
             for (int k = 0; k < KW; ++k) {
                 const bool act = b[k] < e[k] && !found[k];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) u[k][j] = (act && b[k] + j < e[k]) ? __ldg(col + b[k] + j) : -1;
+                for (int j = 0; j < EPS; ++j) u[k][j] = (act && b[k] + j < e[k]) ? __ldg(col + b[k] + j) : -1;
             }
 #pragma unroll
             for (int k = 0; k < KW; ++k) {
                 const bool act = b[k] < e[k] && !found[k];
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (u[k][j] >= 0 && ((ldcg(fcur + ((uint32_t)u[k][j] >> 5)) >> (u[k][j] & 31)) & 1u)) found[k] = true;
+                for (int j = 0; j < EPS; ++j)
+                    if (u[k][j] >= 0 && ((fcur[(uint32_t)u[k][j] >> 5] >> (u[k][j] & 31)) & 1u)) found[k] = true;
                 if (act) {
-                    const uint32_t n = (uint32_t)min((OffT)4, (OffT)(e[k] - b[k]));
+                    const uint32_t n = (uint32_t)min((OffT)EPS, (OffT)(e[k] - b[k]));
                     scanned += n;
                     b[k] += n;
                 }
@@ -421,13 +470,38 @@ struct BfsApp {
                 p.level_out[(w0 + k) * 32 + lane] = (int32_t)L1;
                 mfsum += deg[k];
             }
-            if (wins) {
+            if (wins | dead[k]) {
                 if (lane == 0) {
-                    p.visited[w0 + k] = vw[k] | wins;
-                    fnext[w0 + k] = wins;
+                    p.visited[w0 + k] = x.vw[k] | wins | dead[k];
+                    if (wins) fnext[w0 + k] = wins;
                 }
                 reached += __popc(wins);
             }
+        }
+    }
+
+    template <int KW>
+    __device__ __forceinline__ void bu_words(const KParams &p, CtaState &cs, uint64_t w0, uint64_t nw,
+                                             uint64_t &edges, uint32_t &reached, uint64_t &mfsum) {
+        BuItem<KW> x;
+        bu_load<KW, false>(p, w0, nw, x);
+        bu_process<KW>(p, cs, w0, x, edges, reached, mfsum);
+    }
+
+    // static distribution (no scheduler in the interval): items gw, gw + TW, ...
+    // with the next item's loads in flight while this one is processed
+    template <int KW>
+    __device__ __forceinline__ void bu_pipelined(const KParams &p, CtaState &cs, uint64_t gw, uint64_t TW,
+                                                 uint64_t n_items, uint64_t nw, uint64_t &edges, uint32_t &reached,
+                                                 uint64_t &mfsum) {
+        if (gw >= n_items) return;
+        BuItem<KW> cur, nxt;
+        bu_load<KW, true>(p, gw * KW, nw, cur);
+        for (uint64_t it = gw; it < n_items; it += TW) {
+            const bool has_next = it + TW < n_items;
+            if (has_next) bu_load<KW, true>(p, (it + TW) * KW, nw, nxt);
+            bu_process<KW>(p, cs, it * KW, cur, edges, reached, mfsum);
+            if (has_next) cur = nxt;
         }
     }
 
@@ -479,6 +553,7 @@ struct BfsApp {
             const uint64_t nw = ((uint64_t)p.V + 31) / 32;
             for (uint64_t i = (uint64_t)cs.lid * BLOCK + threadIdx.x; i < nw; i += (uint64_t)cs.M * BLOCK) fold[i] = 0u;
         }
+        LTRACE(4);
         const uint32_t out = in ^ 1u;                             // parity filled by this level
         uint2 res = make_uint2(0, 0);
         auto flush = [&]() {
@@ -487,7 +562,11 @@ struct BfsApp {
         };
         const uint64_t nw = ((uint64_t)p.V + 31) / 32;
         uint32_t r;
-        if (mode == BFS_BU) {                                 // item = BU_KW 32-vertex words
+        const bool midkill = p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY;
+        if (COOP_BU_PIPE && mode == BFS_BU && !midkill) {                     // static: software-pipelined items
+            bu_pipelined<BU_KW>(p, cs, gw, TW, (nw + BU_KW - 1) / BU_KW, nw, edges, reached, mfsum);
+            r = ACT_CONT;
+        } else if (mode == BFS_BU) {                          // item = BU_KW 32-vertex words
             r = claim_items<BLOCK>(p, cs, *this, &p.ctl->chunk[in], (nw + BU_KW - 1) / BU_KW, 128u, [&](uint64_t it) {
                 bu_words<BU_KW>(p, cs, it * BU_KW, nw, edges, reached, mfsum);
             }, flush);
@@ -497,10 +576,19 @@ struct BfsApp {
             }, flush);
         } else {                                              // item = 32 light frontier entries
             expand_heavy(p, cs, gw, TW, fnext, edges, reached, mfsum, res);
-            r = claim_items<BLOCK>(p, cs, *this, &p.ctl->chunk[in], ((uint64_t)cs.app_u32[0] + 31) / 32, 4u * WPB,
-                            [&](uint64_t g) { tdq_group(p, cs, g, fnext, edges, reached, mfsum, res); }, flush);
+            LTRACE(5);
+            // entries per warp item: 32 (a full gather) when there are enough items for
+            // every warp, else fewer, down to one list per warp -- a small frontier of
+            // lists just under the heavy threshold would otherwise sit on a few warps
+            const uint64_t nl = cs.app_u32[0];
+            uint32_t sz = 32;
+            while (sz > 1 && (nl + sz - 1) / sz < TW) sz >>= 1;
+            r = claim_items<BLOCK>(p, cs, *this, &p.ctl->chunk[in], (nl + sz - 1) / sz, 4u * WPB,
+                            [&](uint64_t g) { tdq_group(p, cs, g, sz, fnext, edges, reached, mfsum, res); }, flush);
         }
+        LTRACE(6);
         if (r == ACT_CONT) flush();
+        LTRACE(7);
         return r;
     }
 
@@ -511,28 +599,32 @@ struct BfsApp {
         if (!resizing || entry != ENTRY_AFTER_RB1) return;
         Ctl *c = p.ctl;
         const uint32_t in = cs.in_sel, out = in ^ 1u;        // post-swap selectors
+        // every load first, as one batch of independent round trips (this runs on
+        // the critical path of the barrier, while all other CTAs wait)
         const uint32_t prev = c->bmode[out];
+        const unsigned long long nf = c->nf[in], mf = c->mf[in];
+        const unsigned long long vis = c->vis_edges + mf, ftot = c->frontier_total;
+        const uint32_t nlev = c->levels, nbu = c->n_bu_levels;
         c->qsize[out] = 0;
         c->heavy[out] = 0;
         c->chunk[out] = 0;
         c->nf[out] = 0;
         c->mf[out] = 0;
-        const unsigned long long nf = c->nf[in], mf = c->mf[in];
-        c->vis_edges += mf;
+        c->vis_edges = vis;
         uint32_t mode = BFS_TDQ;
         if (p.dopt) {
-            const unsigned long long mu = (unsigned long long)p.E - min((unsigned long long)p.E, c->vis_edges);
+            const unsigned long long mu = (unsigned long long)p.E - min((unsigned long long)p.E, vis);
             if (prev == BFS_BU) mode = nf * p.beta < (unsigned long long)p.V ? BFS_TDB : BFS_BU;
             else mode = mf * p.alpha > mu ? BFS_BU : BFS_TDQ;
-            if (mode == BFS_BU) c->n_bu_levels += 1;
+            if (mode == BFS_BU) c->n_bu_levels = nbu + 1;
         }
         c->bmode[in] = mode;
         if (cs.level < p.level_cap) p.level_t[cs.level] = globaltimer();   // level L's expand done
         if (nf) {
             const uint32_t L = cs.level + 1;
             if (L < p.level_cap) p.level_sizes[L] = (uint32_t)nf;
-            c->frontier_total += nf;
-            c->levels += 1;
+            c->frontier_total = ftot + nf;
+            c->levels = nlev + 1;
         }
     }
 };
@@ -736,27 +828,30 @@ struct SsspApp {
         if (!resizing || entry != ENTRY_AFTER_RB1) return;
         Ctl *c = p.ctl;
         const uint32_t in = cs.in_sel, out = in ^ 1u;        // post-swap selectors
+        // every load first, one batch of independent round trips (critical path)
         const uint32_t done_mode = c->smode[out];
+        uint32_t fsel = c->far_sel;
+        const uint32_t n = c->qsize[in];
+        const uint32_t fs0 = c->far_size[0], fs1 = c->far_size[1], fmin = c->far_min;
+        const unsigned long long T0 = c->T, ftot = c->frontier_total;
+        const uint32_t nlev = c->levels;
         c->qsize[out] = 0;
         c->chunk[out] = 0;
-        uint32_t fsel = c->far_sel;
         if (done_mode == SSSP_DRAIN) {                        // kept entries now live in the other buffer
             c->far_size[fsel] = 0;
             fsel ^= 1u;
             c->far_sel = fsel;
         }
-        const uint32_t n = c->qsize[in];
-        const uint32_t nfar = min(c->far_size[fsel], p.far_cap);
+        const uint32_t nfar = min(fsel ? fs1 : fs0, p.far_cap);
         uint32_t mode = SSSP_RELAX;
         if (n == 0) {
             if (nfar == 0) {
                 mode = SSSP_DONE;
             } else {
                 // raise the threshold; skip empty bands using the smallest kept distance
-                unsigned long long T = c->T + p.delta;
-                if (done_mode == SSSP_DRAIN && c->far_min != 0xFFFFFFFFu && c->far_min >= T)
-                    T = (unsigned long long)c->far_min + 1;
-                c->T_lo = c->T;
+                unsigned long long T = T0 + p.delta;
+                if (done_mode == SSSP_DRAIN && fmin != 0xFFFFFFFFu && fmin >= T) T = (unsigned long long)fmin + 1;
+                c->T_lo = T0;
                 c->T = T;
                 c->far_min = 0xFFFFFFFFu;
                 mode = SSSP_DRAIN;
@@ -767,8 +862,8 @@ struct SsspApp {
         if (n) {
             const uint32_t L = cs.level + 1;
             if (L < p.level_cap) p.level_sizes[L] = n;
-            c->frontier_total += n;
-            c->levels += 1;
+            c->frontier_total = ftot + n;
+            c->levels = nlev + 1;
         }
     }
 };

@@ -141,6 +141,8 @@ struct Scratch {
 };
 
 constexpr uint32_t kWorkspaces = 8;
+constexpr uint32_t kDefaultAlpha = 14;   // Beamer et al.'s direction-switch thresholds (reading R14)
+constexpr uint32_t kDefaultBeta = 24;
 static Scratch g_scratch[16][kWorkspaces];
 
 static coop_status get_scratch(Scratch **out, uint32_t ws) {
@@ -427,7 +429,7 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
         // light queues: per-warp reservations of 256 slots may leave holes (empty
         // entries): at most one partly used reservation per refill (< 128 unused
         // slots, refills hold >= 128 entries) plus one open reservation per warp
-        const size_t qcap = 2 * V + (size_t)kMaxCtas * 32 * 256;
+        const size_t qcap = 2 * V + (size_t)P * (threads / 32) * 256;
         CUDA_TRY(s->visited.ensure(4 * ((V + 31) / 32)));
         CUDA_TRY(s->ql0.ensure(le * qcap));
         CUDA_TRY(s->ql1.ensure(le * qcap));
@@ -485,8 +487,8 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
         kp.script_len = o.script_len;
     }
     kp.host = r.host;
-    kp.alpha = 14;                       // Beamer's direction-switch thresholds
-    kp.beta = 24;
+    kp.alpha = o.bfs_alpha ? o.bfs_alpha : kDefaultAlpha;   // direction-switch thresholds (Beamer et al.)
+    kp.beta = o.bfs_beta ? o.bfs_beta : kDefaultBeta;
     kp.P = P;
     kp.M0 = M0;
     kp.policy = plain ? COOP_POLICY_NEVER : o.policy;
@@ -699,6 +701,21 @@ extern "C" coop_status coop_debug_trace(uint64_t *out16) {
     memcpy(out16, s->host_ctl->trace, sizeof(s->host_ctl->trace));
     return COOP_OK;
 }
+
+#if COOP_LTRACE
+// debug builds only (not part of the ABI in include/coop.h): the per-level stamps
+extern "C" coop_status coop_debug_ltrace(uint64_t *out, size_t n) {
+    if (!out) {   // clear
+        void *a = nullptr;
+        CUDA_TRY(cudaGetSymbolAddress(&a, coop::g_ltrace));
+        CUDA_TRY(cudaMemset(a, 0, sizeof(coop::g_ltrace)));
+        return COOP_OK;
+    }
+    n = std::min(n, sizeof(coop::g_ltrace) / sizeof(uint64_t));
+    CUDA_TRY(cudaMemcpyFromSymbol(out, coop::g_ltrace, n * sizeof(uint64_t)));
+    return COOP_OK;
+}
+#endif
 
 extern "C" coop_status coop_l2_atomic_rtt(uint64_t iters, double *ns_per_atomic) {
     if (!ns_per_atomic || iters == 0) return fail(COOP_ERR_INVALID_ARG, "bad arguments");

@@ -51,7 +51,25 @@
 #define COOP_TRACE 0          // 1: clock64 breakdown of the barrier, CTA 0 (coop_debug_trace)
 #endif
 
+#ifndef COOP_LTRACE
+#define COOP_LTRACE 0         // 1: per-level per-CTA %globaltimer stamps (tools/level_trace.py)
+#endif
+
 namespace coop {
+
+#if COOP_LTRACE
+// [level][blockIdx][expand start, expand end, after RB1, after RB2, app stamps 4..7]
+__device__ unsigned long long g_ltrace[64][1184][8];
+#define LTRACE(k)                                                                         \
+    do {                                                                                  \
+        if (threadIdx.x == 0 && cs.level < 64 && blockIdx.x < 1184)                       \
+            g_ltrace[cs.level][blockIdx.x][k] = globaltimer();                            \
+    } while (0)
+#define LTRACE_RB2(l) (g_ltrace[l][blockIdx.x][3] = globaltimer())
+#else
+#define LTRACE(k) do {} while (0)
+#define LTRACE_RB2(l) ((void)0)
+#endif
 
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -639,12 +657,15 @@ __device__ uint32_t run_body(const KParams &p, CtaState &cs, App &app, uint32_t 
     for (;;) {
         if (!skip_to_rb1) {
             if (app.empty(p, cs)) return ACT_DONE;            // while (in_nodes.size > 0)
+            LTRACE(0);
             r = app.template expand<BLOCK>(p, cs);             // for (i = tid; ...) process_node
             if (r != ACT_CONT) return r;                       // killed at a chunk boundary (offer_kill)
             __syncthreads();                                   // every warp is done reading cs
+            LTRACE(1);
             if (threadIdx.x == 0) cs.in_sel ^= 1u;            // swap(&in_nodes, &out_nodes)
             r = barrier(p, cs, app, true, ENTRY_AFTER_RB1);   // resizing_global_barrier() #1
             if (r != ACT_CONT) return r;
+            LTRACE(2);
         }
         skip_to_rb1 = false;
         app.template between<BLOCK>(p, cs);                   // CTA work between Fig. 4's two barriers
@@ -652,6 +673,8 @@ __device__ uint32_t run_body(const KParams &p, CtaState &cs, App &app, uint32_t 
         if (p.bpl == 2) {
             r = barrier(p, cs, app, true, ENTRY_AFTER_RB2);   // resizing_global_barrier() #2
             if (r != ACT_CONT) return r;
+            if (threadIdx.x == 0 && cs.level >= 1 && cs.level <= 64 && blockIdx.x < 1184 && COOP_LTRACE)
+                LTRACE_RB2(cs.level - 1);
         } else {
             __syncthreads();
         }

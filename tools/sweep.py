@@ -82,3 +82,34 @@ if what in ("all", "levels"):
             print(json.dumps({"levels": True, "src": s, "flags": flags, "kernel_us": st.kernel_ns / 1e3,
                               "sizes": st.level_sizes, "level_us": [round(x / 1e3, 1) for x in per],
                               "bu": st.bottom_up_levels, "edges": st.edges_scanned}), flush=True)
+if what == "ab":   # direction-switch thresholds (alpha, beta) on RMAT-24, mean kernel time over 8 sources
+    g = gg.rmat(24, seed=1, device="cuda", chunk=1 << 26)
+    out = torch.empty(g.num_vertices, dtype=torch.int32, device="cuda")
+    srcs = gg.sample_sources(g, 8, seed=2)
+    l2 = torch.empty(1 << 26, dtype=torch.int32, device="cuda")   # 256 MB > L2: flushed before every run
+    for a in (2, 4, 8, 14, 32):
+        for b in (8, 24, 64, 256):
+            ks = []
+            for s in srcs:
+                best = None
+                for rep in range(2):
+                    l2.fill_(rep)
+                    _, st = coop.bfs(g, s, out, threads_per_wg=512, flags=coop.FLAG_DIROPT, bfs_alpha=a, bfs_beta=b)
+                    best = st.kernel_ns if best is None else min(best, st.kernel_ns)
+                ks.append(best / 1e3)
+            print(json.dumps({"alpha": a, "beta": b, "mean_kernel_us": round(sum(ks) / len(ks), 1),
+                              "per_source_us": [round(k, 1) for k in ks]}), flush=True)
+if what == "srcs":   # mean DIROPT kernel time on RMAT-24 over 8 sources (L2 flushed before every run)
+    g = gg.rmat(24, seed=1, device="cuda", chunk=1 << 26)
+    out = torch.empty(g.num_vertices, dtype=torch.int32, device="cuda")
+    l2 = torch.empty(1 << 26, dtype=torch.int32, device="cuda")
+    ks = []
+    for s in gg.sample_sources(g, 8, seed=2):
+        best = None
+        for rep in range(3):
+            l2.fill_(rep)
+            _, st = coop.bfs(g, s, out, threads_per_wg=512, flags=coop.FLAG_DIROPT)
+            best = st.kernel_ns if best is None else min(best, st.kernel_ns)
+        ks.append(best / 1e3)
+    print(json.dumps({"lib": os.environ.get("COOP_LIB", "default"), "mean_kernel_us": round(sum(ks) / len(ks), 1),
+                      "per_source_us": [round(k, 1) for k in ks]}), flush=True)
