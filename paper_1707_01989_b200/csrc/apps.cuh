@@ -23,8 +23,17 @@
 #ifndef COOP_BU_EPS
 #define COOP_BU_EPS 1         // bottom-up: edges probed per list per step (first hits dominate)
 #endif
-#ifndef COOP_BU_PIPE
-#define COOP_BU_PIPE 0        // bottom-up: 1 = speculative offsets + next-item prefetch (static path)
+#ifndef COOP_BU_COMPACT
+#define COOP_BU_COMPACT 1     // bottom-up: compacted candidates over 32-word items (else lane per vertex)
+#endif
+#ifndef COOP_BU_K
+#define COOP_BU_K 4           // bottom-up (compacted): candidates per lane per round
+#endif
+#ifndef COOP_BU_SOLO
+#define COOP_BU_SOLO 8        // bottom-up (compacted): per-lane steps before the warp takes a list over
+#endif
+#ifndef COOP_BU_DENSE_W
+#define COOP_BU_DENSE_W 16    // bottom-up (compacted): words per item in the first (dense) level
 #endif
 
 namespace coop {
@@ -119,6 +128,7 @@ struct BfsApp {
             cs.app_u32[3] = (uint32_t)(Eh >> 32);
             cs.app_u32[4] = c->nf[in] ? 1u : 0u;
             cs.app_u32[5] = c->bmode[in];
+            cs.app_u32[6] = c->n_bu_levels;                  // 1 during the first bottom-up level
         }
         __syncthreads();
         return cs.app_u32[4] == 0;
@@ -372,13 +382,11 @@ struct BfsApp {
     // each unvisited vertex scans its list (4 per step) for a parent in the
     // frontier bitmap and stops at the first hit.  The warp owns the visited /
     // next-frontier words, so no atomics.
-    // KW consecutive words per warp item: lane l owns vertex (w0+k)*32 + l of
-    // each word k, and all KW lists advance together (KW x 4 column loads and
-    // probes in flight per lane).  The step is latency bound (visited + offsets ->
-    // columns -> frontier probe), so an item is split into a load half (bu_load:
-    // the visited words and the row offsets, issued speculatively for every lane,
-    // independent of each other) and a process half (bu_process), and the static
-    // driver (bu_pipelined) issues item i+1's loads before processing item i.
+    // Lane-per-vertex variant (COOP_BU_COMPACT=0): KW consecutive words per warp
+    // item, lane l owns vertex (w0+k)*32 + l of each word k, all KW lists advance
+    // together (EPS column loads and probes per list per step); an item is a load
+    // half (bu_load: visited words, then the offsets of open words) and a process
+    // half (bu_process).
     template <int KW>
     struct BuItem {
         uint32_t vw[KW];   // visited words
@@ -386,10 +394,8 @@ struct BfsApp {
         OffT e31[KW];      // lane 31: ro[v + 1] (other lanes take the next lane's b)
     };
 
-    // SPEC: offsets for every lane, independent of the visited words (one round
-    // trip less, but the offsets of fully visited words are read too); else the
-    // offsets of the unvisited lanes only, after the visited words arrive
-    template <int KW, bool SPEC>
+    // offsets of the words with an unvisited lane, after the visited words arrive
+    template <int KW>
     __device__ __forceinline__ void bu_load(const KParams &p, uint64_t w0, uint64_t nw, BuItem<KW> &x) {
         const uint32_t lane = threadIdx.x & 31;
         const OffT *ro = static_cast<const OffT *>(p.ro);
@@ -399,7 +405,7 @@ struct BfsApp {
 #pragma unroll
         for (int k = 0; k < KW; ++k) {
             const uint64_t v = (w0 + k) * 32 + lane;
-            const bool want = SPEC || (x.vw[k] != 0xFFFFFFFFu);
+            const bool want = x.vw[k] != 0xFFFFFFFFu;
             x.b[k] = (want && v <= V) ? __ldg(ro + v) : (OffT)0;
             x.e31[k] = (want && lane == 31 && v < V) ? __ldg(ro + v + 1) : (OffT)0;
         }
@@ -484,25 +490,158 @@ struct BfsApp {
     __device__ __forceinline__ void bu_words(const KParams &p, CtaState &cs, uint64_t w0, uint64_t nw,
                                              uint64_t &edges, uint32_t &reached, uint64_t &mfsum) {
         BuItem<KW> x;
-        bu_load<KW, false>(p, w0, nw, x);
+        bu_load<KW>(p, w0, nw, x);
         bu_process<KW>(p, cs, w0, x, edges, reached, mfsum);
     }
 
-    // static distribution (no scheduler in the interval): items gw, gw + TW, ...
-    // with the next item's loads in flight while this one is processed
-    template <int KW>
-    __device__ __forceinline__ void bu_pipelined(const KParams &p, CtaState &cs, uint64_t gw, uint64_t TW,
-                                                 uint64_t n_items, uint64_t nw, uint64_t &edges, uint32_t &reached,
-                                                 uint64_t &mfsum) {
-        if (gw >= n_items) return;
-        BuItem<KW> cur, nxt;
-        bu_load<KW, true>(p, gw * KW, nw, cur);
-        for (uint64_t it = gw; it < n_items; it += TW) {
-            const bool has_next = it + TW < n_items;
-            if (has_next) bu_load<KW, true>(p, (it + TW) * KW, nw, nxt);
-            bu_process<KW>(p, cs, it * KW, cur, edges, reached, mfsum);
-            if (has_next) cur = nxt;
+    // ---------------------------------------------------------- bottom-up, compacted candidates
+    // Warp item = 32 visited words (lane l owns word w0 + l, one load for all).
+    // The unvisited vertices of the 32 words are enumerated densely (warp prefix
+    // sum of the per-word counts, then select the r-th open bit of the owner
+    // word) and handed out K per lane per round, so every lane checks a real
+    // candidate: sparse levels cost one visited load per 1024 vertices instead of
+    // one per 128, and dense ones keep all lanes busy.  Found / degree-0 bits are
+    // merged into the owner lane's word in shared memory (per-warp slots).
+    __device__ __forceinline__ static uint32_t select_bit(uint32_t m, uint32_t r) {   // r-th set bit (0-based)
+        uint32_t pos = 0;
+#pragma unroll
+        for (uint32_t w = 16; w; w >>= 1) {
+            const uint32_t c = __popc(m & ((1u << w) - 1u));
+            if (r >= c) { r -= c; m >>= w; pos += w; }
         }
+        return pos;
+    }
+
+    template <int K>
+    __device__ __forceinline__ void bu_compact(const KParams &p, CtaState &cs, uint64_t w0, uint64_t nw,
+                                               uint32_t nwords, uint32_t *s_found, uint32_t *s_dead,
+                                               uint64_t &edges, uint32_t &reached, uint64_t &mfsum) {
+        const uint32_t lane = threadIdx.x & 31;
+        const uint32_t L1 = cs.level + 1;
+        const uint32_t *fcur = p.fbits[cs.level % 3];
+        uint32_t *fnext = p.fbits[L1 % 3];
+        const OffT *ro = static_cast<const OffT *>(p.ro);
+        const int32_t *__restrict__ col = p.col;
+        const uint64_t V = (uint64_t)p.V;
+        const uint64_t w = w0 + lane;
+        uint32_t vw = 0xFFFFFFFFu;
+        if (lane < nwords && w < nw) {
+            vw = p.visited[w];
+            const uint64_t vend = (w + 1) * 32;
+            if (vend > V) vw |= ~((1u << (uint32_t)(32 - (vend - V))) - 1u);   // bits past V: closed
+        }
+        const uint32_t open = ~vw;
+        const uint32_t cnt = __popc(open);
+        const uint32_t incl = warp_incl_scan(cnt), excl = incl - cnt;
+        const uint32_t total = __shfl_sync(FULL, incl, 31);
+        if (total == 0) return;                                  // warp-uniform
+        s_found[lane] = 0u;
+        s_dead[lane] = 0u;
+        __syncwarp();
+        uint32_t scanned = 0;
+        for (uint32_t base = 0; base < total; base += 32 * K) {
+            uint32_t own[K], bit[K];
+            OffT b[K], e[K];
+            bool found[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const uint32_t j = base + 32 * k + lane;
+                uint32_t o = 0;   // owner lane: largest o with excl_o <= j
+#pragma unroll
+                for (uint32_t st = 16; st >= 1; st >>= 1) {
+                    const uint32_t ex = __shfl_sync(FULL, excl, o + st);
+                    if (ex <= j) o += st;
+                }
+                const uint32_t om = __shfl_sync(FULL, open, o), oe = __shfl_sync(FULL, excl, o);
+                own[k] = o;
+                bit[k] = j < total ? select_bit(om, j - oe) : 32u;
+                b[k] = 0;
+                e[k] = 0;
+                found[k] = false;
+                if (bit[k] < 32) {
+                    const uint64_t v = (w0 + o) * 32 + bit[k];
+                    b[k] = __ldg(ro + v);
+                    e[k] = __ldg(ro + v + 1);
+                }
+            }
+            uint32_t deg[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                deg[k] = (uint32_t)(e[k] - b[k]);
+                if (bit[k] < 32 && deg[k] == 0) atomicOr(&s_dead[own[k]], 1u << bit[k]);   // never a neighbour
+            }
+            for (int step = 0; step < COOP_BU_SOLO; ++step) {   // per-lane: the first hits dominate
+                bool more = false;
+#pragma unroll
+                for (int k = 0; k < K; ++k) more |= (b[k] < e[k] && !found[k]);
+                if (!__any_sync(FULL, more)) break;
+                int32_t u[K][EPS];
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const bool act = b[k] < e[k] && !found[k];
+#pragma unroll
+                    for (int jj = 0; jj < EPS; ++jj) u[k][jj] = (act && b[k] + jj < e[k]) ? __ldg(col + b[k] + jj) : -1;
+                }
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const bool act = b[k] < e[k] && !found[k];
+#pragma unroll
+                    for (int jj = 0; jj < EPS; ++jj)
+                        if (u[k][jj] >= 0 && ((fcur[(uint32_t)u[k][jj] >> 5] >> (u[k][jj] & 31)) & 1u)) found[k] = true;
+                    if (act) {
+                        const uint32_t n = (uint32_t)min((OffT)EPS, (OffT)(e[k] - b[k]));
+                        scanned += n;
+                        b[k] += n;
+                    }
+                }
+            }
+            // the rest of the long lists: one list at a time, 32 edges per warp step
+            // (a lane walking a long list alone would hold the whole warp)
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                uint32_t m = __ballot_sync(FULL, b[k] < e[k] && !found[k]);
+                while (m) {
+                    const uint32_t ld = __ffs(m) - 1;
+                    m &= m - 1;
+                    const OffT lb = __shfl_sync(FULL, b[k], ld), le = __shfl_sync(FULL, e[k], ld);
+                    bool hit = false;
+                    for (OffT x = lb; x < le; x += 32) {
+                        const OffT xe = x + lane;
+                        const int32_t uu = xe < le ? __ldg(col + xe) : -1;
+                        const bool h = uu >= 0 && ((fcur[(uint32_t)uu >> 5] >> (uu & 31)) & 1u);
+                        const uint32_t hm = __ballot_sync(FULL, h);
+                        const OffT lim = min((OffT)32, (OffT)(le - x));
+                        if (hm) {
+                            scanned += lane == ld ? (uint32_t)(__ffs(hm)) : 0u;
+                            hit = true;
+                            break;
+                        }
+                        scanned += lane == ld ? (uint32_t)lim : 0u;
+                    }
+                    if (lane == ld) {
+                        found[k] = hit;
+                        b[k] = e[k];
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if (found[k]) {
+                    p.level_out[(w0 + own[k]) * 32 + bit[k]] = (int32_t)L1;
+                    atomicOr(&s_found[own[k]], 1u << bit[k]);
+                    mfsum += deg[k];
+                }
+            }
+        }
+        edges += (uint64_t)scanned * 32;
+        __syncwarp();
+        const uint32_t f = s_found[lane], d = s_dead[lane];
+        if (f | d) {   // only lanes that own an in-range word can have bits
+            p.visited[w] = vw | f | d;
+            if (f) fnext[w] = f;
+        }
+        reached += __reduce_add_sync(FULL, __popc(f));   // warp-uniform, like the other modes
+        __syncwarp();
     }
 
     static constexpr uint32_t BU_KW = COOP_BU_KW;  // bottom-up: words per warp item
@@ -562,10 +701,15 @@ struct BfsApp {
         };
         const uint64_t nw = ((uint64_t)p.V + 31) / 32;
         uint32_t r;
-        const bool midkill = p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY;
-        if (COOP_BU_PIPE && mode == BFS_BU && !midkill) {                     // static: software-pipelined items
-            bu_pipelined<BU_KW>(p, cs, gw, TW, (nw + BU_KW - 1) / BU_KW, nw, edges, reached, mfsum);
-            r = ACT_CONT;
+        if (COOP_BU_COMPACT && mode == BFS_BU) {          // item = 32 words, compacted candidates
+            __shared__ uint32_t s_bits[2][BLOCK];
+            const uint32_t wb = (threadIdx.x >> 5) * 32;
+            // the first bottom-up level is dense (most vertices still open): smaller
+            // items so the static split stays balanced; later levels: 32 words
+            const uint32_t W = cs.app_u32[6] <= 1 ? COOP_BU_DENSE_W : 32u;
+            r = claim_items<BLOCK>(p, cs, *this, &p.ctl->chunk[in], (nw + W - 1) / W, 16u, [&](uint64_t it) {
+                bu_compact<COOP_BU_K>(p, cs, it * W, nw, W, &s_bits[0][wb], &s_bits[1][wb], edges, reached, mfsum);
+            }, flush);
         } else if (mode == BFS_BU) {                          // item = BU_KW 32-vertex words
             r = claim_items<BLOCK>(p, cs, *this, &p.ctl->chunk[in], (nw + BU_KW - 1) / BU_KW, 128u, [&](uint64_t it) {
                 bu_words<BU_KW>(p, cs, it * BU_KW, nw, edges, reached, mfsum);

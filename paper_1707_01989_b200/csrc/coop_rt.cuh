@@ -134,6 +134,9 @@ __device__ __forceinline__ uint32_t w_gen(unsigned long long w) { return (uint32
 __device__ __forceinline__ uint32_t w_M(unsigned long long w) { return (uint32_t)(w >> 16) & 0xFFFF; }
 __device__ __forceinline__ uint32_t w_arr(unsigned long long w) { return (uint32_t)w & 0xFFFF; }
 
+__device__ __forceinline__ void prefetch_l2(const void *a) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+}
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
     const uint32_t lane = threadIdx.x & 31;
 #pragma unroll
