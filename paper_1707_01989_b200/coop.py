@@ -147,6 +147,8 @@ def load(path: str = LIB_PATH):
     """Load libcoop.so (raises if it has not been built -- no fallback)."""
     global _lib
     if _lib is None:
+        if path == LIB_PATH and os.environ.get("COOP_LIB"):   # a build variant (tools/, experiments)
+            path = os.path.abspath(os.environ["COOP_LIB"])
         if not os.path.exists(path):
             raise RuntimeError(f"{path} not built: run `python -m paper_1707_01989_b200.build` "
                                "(or __graft_entry__.build()); there is no CPU fallback")

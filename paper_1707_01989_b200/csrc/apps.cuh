@@ -23,6 +23,9 @@
 #ifndef COOP_BU_EPS
 #define COOP_BU_EPS 1         // bottom-up: edges probed per list per step (first hits dominate)
 #endif
+#ifndef COOP_INIT_DEAD
+#define COOP_INIT_DEAD 1      // direction-optimising BFS: close degree-0 vertices in init
+#endif
 #ifndef COOP_BU_COMPACT
 #define COOP_BU_COMPACT 1     // bottom-up: compacted candidates over 32-word items (else lane per vertex)
 #endif
@@ -81,8 +84,39 @@ struct BfsApp {
         for (uint64_t i = h + 4 * nvec + tid; i < (uint64_t)V; i += nth) lv[i] = (int64_t)i == s ? 0 : -1;
         const uint64_t nw = ((uint64_t)V + 31) / 32;
         const uint32_t sw = (uint32_t)(s >> 5), sb = 1u << (s & 31);
+        if (p.dopt && COOP_INIT_DEAD && sizeof(OffT) == 4 && ((uintptr_t)p.ro & 15) == 0) {
+            // symmetric CSR: a degree-0 vertex is never a neighbour, so it starts
+            // closed and the bottom-up levels do not enumerate it (about half of
+            // an R-MAT graph's vertices).  Thread per word: the 33 offsets of its
+            // 32 vertices as 8 independent 16-B loads + 1.
+            const uint32_t *ro = reinterpret_cast<const uint32_t *>(p.ro);
+            for (uint64_t i = tid; i < nw; i += nth) {
+                uint32_t m = 0;
+                if ((i + 1) * 32 <= (uint64_t)V) {
+                    const uint4 *r4 = reinterpret_cast<const uint4 *>(ro + i * 32);
+                    uint4 q[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) q[k] = __ldg(r4 + k);
+                    const uint32_t last = __ldg(ro + i * 32 + 32);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const uint32_t nx = k < 7 ? q[k + 1].x : last;
+                        m |= (q[k].x == q[k].y ? 1u : 0u) << (4 * k);
+                        m |= (q[k].y == q[k].z ? 1u : 0u) << (4 * k + 1);
+                        m |= (q[k].z == q[k].w ? 1u : 0u) << (4 * k + 2);
+                        m |= (q[k].w == nx ? 1u : 0u) << (4 * k + 3);
+                    }
+                } else {
+                    for (uint64_t v = i * 32; v < (uint64_t)V; ++v)
+                        if (__ldg(ro + v + 1) == __ldg(ro + v)) m |= 1u << (v - i * 32);
+                }
+                if (i == sw) m = (m & ~sb) | sb;   // the source is reached, not closed-as-isolated
+                p.visited[i] = m | (i == sw ? sb : 0u);
+            }
+        }
         for (uint64_t i = tid; i < nw; i += nth) {
-            p.visited[i] = i == sw ? sb : 0u;
+            if (!(p.dopt && COOP_INIT_DEAD && sizeof(OffT) == 4 && ((uintptr_t)p.ro & 15) == 0))
+                p.visited[i] = i == sw ? sb : 0u;
             if (p.dopt) {
                 p.fbits[0][i] = i == sw ? sb : 0u;
                 p.fbits[1][i] = 0u;
