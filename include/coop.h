@@ -293,6 +293,92 @@ coop_status coop_current_m(coop_handle *h, uint32_t *M);   /* active workgroups 
 coop_status coop_wait(coop_handle *h, coop_stats *stats);  /* wait for termination, fill stats */
 void coop_destroy(coop_handle *h);
 
+
+/* ---- user cooperative kernels: host half of the device API in coop_device.cuh ----
+ * A kernel written against coop_device.cuh (offer_kill P:529-550, request_fork
+ * P:553-592, global_barrier P:600-610, resizing_global_barrier P:612-638)
+ * takes a `coop_dev *` control block.  The host creates a handle once
+ * (coop_dev_create), re-arms the block before each launch (coop_dev_arm: N
+ * CTAs, M0 active, the others parked in the pool), launches (coop_dev_launch in
+ * coop_device.cuh, or a library app below) and reads the outcome
+ * (coop_dev_collect).  coop_dev_demand / coop_dev_grant post resource messages
+ * and may be called from another host thread while the kernel runs
+ * (policy COOP_POLICY_SCHEDULER). */
+typedef struct coop_dev coop_dev;                 /* device control block (layout in coop_device.cuh) */
+typedef struct coop_dev_handle coop_dev_handle;
+
+typedef struct {
+    uint32_t max_wgs;           /* cap on N (0 = the kernel's co-resident capacity) */
+    uint32_t init_wgs;          /* M0 in [1, N] (0 = N) */
+    uint32_t policy;            /* coop_policy (SCHEDULER = host resource messages) */
+    uint32_t flags;             /* COOP_FLAG_CHECK: arrival-count / contiguity checks at every barrier */
+    uint64_t seed;              /* RANDOM */
+    double resize_prob;         /* RANDOM: per resizing barrier, M' ~ U[1, N] */
+    double kill_prob;           /* RANDOM: per bare offer_kill call (accepted only for id M-1 > 0) */
+    double fork_prob;           /* RANDOM: per bare request_fork call, k ~ U[1, max_fork] */
+    uint32_t max_fork;          /* RANDOM: 0 = 4, at most 32 */
+    const uint32_t *script;     /* host, SCRIPTED: M' per resizing episode (0 = unchanged) */
+    uint32_t script_len;
+    uint32_t m_trace_cap;       /* M' of the first m_trace_cap resizing episodes (read by coop_dev_collect) */
+    uint64_t timeout_ns;        /* watchdog for every spin (0 = 20 s) */
+} coop_dev_opts;
+
+typedef struct {
+    uint64_t kernel_ns;         /* %globaltimer from CTA 0's start to the first finishing CTA */
+    uint32_t n_wgs;             /* N launched */
+    uint32_t kills, forks;      /* workgroups killed / forked (bare calls and barriers) */
+    uint32_t episodes;          /* resizing barriers */
+    uint32_t barriers;          /* all barriers */
+    uint32_t offers;            /* bare offer_kill calls */
+    uint32_t fork_calls;        /* bare request_fork calls */
+    uint32_t min_m, max_m;      /* range of M */
+    uint32_t final_m;           /* M at termination */
+    uint32_t violations;        /* COOP_FLAG_CHECK failures (status is then COOP_ERR_INVARIANT) */
+    uint32_t *m_trace;          /* optional caller-owned HOST buffer: M' per resizing episode */
+    uint32_t m_trace_cap;
+} coop_dev_stats;
+
+coop_status coop_dev_create(const coop_dev_opts *opts, coop_dev_handle **handle);
+/* Reset the control block for a launch of n_wgs CTAs (enqueued on `stream`);
+ * *dev_out is the kernel argument.  COOP_ERR_INVALID_ARG if n_wgs is 0 or
+ * exceeds COOP_DEV_MAX_CTAS, or init_wgs > n_wgs. */
+coop_status coop_dev_arm(coop_dev_handle *h, uint32_t n_wgs, void *stream, coop_dev **dev_out);
+coop_status coop_dev_demand(coop_dev_handle *h, uint32_t kills);   /* surrender `kills` WGs (query/offer_kill) */
+coop_status coop_dev_grant(coop_dev_handle *h, uint32_t forks);    /* fork up to `forks` WGs */
+/* Synchronise `stream`, read the control block, map its error word:
+ * timeout -> COOP_ERR_TIMEOUT, invariant -> COOP_ERR_INVARIANT, overflow -> COOP_ERR_OVERFLOW. */
+coop_status coop_dev_collect(coop_dev_handle *h, void *stream, coop_dev_stats *stats);
+void coop_dev_destroy(coop_dev_handle *h);
+
+/* Fig. 4 exactly, written on the device API: thread-strided
+ * frontier with tid/stride recomputed after every resizing barrier, claims by
+ * CAS on the level array, two resizing barriers per level transmitting
+ * {level, in_nodes/out_nodes}.  32-bit offsets.  levels_out: device
+ * int32[V], -1 unreachable.  Blocking. */
+coop_status coop_fig4_bfs(coop_dev_handle *h, const coop_csr *g, int64_t source, int32_t *levels_out,
+                          uint32_t threads_per_wg, coop_dev_stats *stats);
+
+/* Cooperative work stealing (Fig. 2, adapted per §3.2):
+ * per-workgroup task queues guarded by CAS mutexes, offer_kill and
+ * request_fork at the head of the main loop, queue id read after the fork
+ * point.  The task set is the seeded implicit tree of DESIGN.md reading R19. */
+typedef struct {
+    uint64_t seed;              /* root task id */
+    uint32_t depth;             /* D <= 62 */
+    uint32_t max_fanout;        /* B */
+    uint32_t fixed;             /* 1: every inner task has exactly B children */
+    uint32_t rounds;            /* R: splitmix64 rounds per lane of work */
+    uint32_t queue_cap;         /* entries per queue, power of two (0 = 1024) */
+} coop_ws_tree;
+typedef struct {
+    uint64_t count;             /* tasks processed */
+    uint64_t total;             /* sum of task values mod 2^64 */
+    uint64_t hist[64];          /* tasks per depth */
+    uint64_t steals;            /* tasks taken from another workgroup's queue */
+} coop_ws_result;
+coop_status coop_work_steal(coop_dev_handle *h, const coop_ws_tree *tree, uint32_t threads_per_wg,
+                            coop_ws_result *result, coop_dev_stats *stats);
+
 #ifdef __cplusplus
 }
 #endif

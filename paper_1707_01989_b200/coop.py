@@ -99,6 +99,32 @@ class CoopPart(ctypes.Structure):
                 ("num_edges_global", ctypes.c_int64)]
 
 
+class DevOpts(ctypes.Structure):
+    _fields_ = [("max_wgs", ctypes.c_uint32), ("init_wgs", ctypes.c_uint32), ("policy", ctypes.c_uint32),
+                ("flags", ctypes.c_uint32), ("seed", ctypes.c_uint64), ("resize_prob", ctypes.c_double),
+                ("kill_prob", ctypes.c_double), ("fork_prob", ctypes.c_double), ("max_fork", ctypes.c_uint32),
+                ("script", ctypes.POINTER(ctypes.c_uint32)), ("script_len", ctypes.c_uint32),
+                ("m_trace_cap", ctypes.c_uint32), ("timeout_ns", ctypes.c_uint64)]
+
+
+class DevStats(ctypes.Structure):
+    _fields_ = [("kernel_ns", ctypes.c_uint64), ("n_wgs", ctypes.c_uint32), ("kills", ctypes.c_uint32),
+                ("forks", ctypes.c_uint32), ("episodes", ctypes.c_uint32), ("barriers", ctypes.c_uint32),
+                ("offers", ctypes.c_uint32), ("fork_calls", ctypes.c_uint32), ("min_m", ctypes.c_uint32),
+                ("max_m", ctypes.c_uint32), ("final_m", ctypes.c_uint32), ("violations", ctypes.c_uint32),
+                ("m_trace", ctypes.POINTER(ctypes.c_uint32)), ("m_trace_cap", ctypes.c_uint32)]
+
+
+class WsTree(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("depth", ctypes.c_uint32), ("max_fanout", ctypes.c_uint32),
+                ("fixed", ctypes.c_uint32), ("rounds", ctypes.c_uint32), ("queue_cap", ctypes.c_uint32)]
+
+
+class WsResult(ctypes.Structure):
+    _fields_ = [("count", ctypes.c_uint64), ("total", ctypes.c_uint64), ("hist", ctypes.c_uint64 * 64),
+                ("steals", ctypes.c_uint64)]
+
+
 # every function declared in include/coop.h: name -> (restype, argtypes)
 _P = ctypes.c_void_p
 SIGNATURES = {
@@ -138,6 +164,16 @@ SIGNATURES = {
     "coop_ipc_get_handle": (ctypes.c_int, [_P, _P]),
     "coop_ipc_open": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
     "coop_ipc_close": (ctypes.c_int, [_P]),
+    "coop_dev_create": (ctypes.c_int, [ctypes.POINTER(DevOpts), ctypes.POINTER(_P)]),
+    "coop_dev_arm": (ctypes.c_int, [_P, ctypes.c_uint32, _P, ctypes.POINTER(_P)]),
+    "coop_dev_demand": (ctypes.c_int, [_P, ctypes.c_uint32]),
+    "coop_dev_grant": (ctypes.c_int, [_P, ctypes.c_uint32]),
+    "coop_dev_collect": (ctypes.c_int, [_P, _P, ctypes.POINTER(DevStats)]),
+    "coop_dev_destroy": (None, [_P]),
+    "coop_fig4_bfs": (ctypes.c_int, [_P, ctypes.POINTER(CooperativeCSR), ctypes.c_int64, _P, ctypes.c_uint32,
+                                     ctypes.POINTER(DevStats)]),
+    "coop_work_steal": (ctypes.c_int, [_P, ctypes.POINTER(WsTree), ctypes.c_uint32, ctypes.POINTER(WsResult),
+                                       ctypes.POINTER(DevStats)]),
 }
 
 _lib = None
@@ -427,3 +463,88 @@ class Handle:
             self.close()
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------- device API (coop_device.cuh)
+class DevHandle:
+    """Control block of the device API (coop_dev_create); resource messages
+    (demand / grant) may be posted from another thread while a call runs."""
+
+    def __init__(self, *, max_wgs=0, init_wgs=0, policy=POLICY_NEVER, flags=0, seed=1, resize_prob=0.0,
+                 kill_prob=0.0, fork_prob=0.0, max_fork=0, script=None, m_trace_cap=0, timeout_ns=0):
+        lib = load()
+        o = DevOpts(max_wgs=max_wgs, init_wgs=init_wgs, policy=policy, flags=flags, seed=seed,
+                    resize_prob=resize_prob, kill_prob=kill_prob, fork_prob=fork_prob, max_fork=max_fork,
+                    m_trace_cap=m_trace_cap, timeout_ns=timeout_ns)
+        if script is not None:
+            self._script = (ctypes.c_uint32 * len(script))(*script)
+            o.script = self._script
+            o.script_len = len(script)
+        self.m_trace_cap = m_trace_cap
+        h = _P()
+        _check(lib.coop_dev_create(ctypes.byref(o), ctypes.byref(h)))
+        self.h = h
+
+    def demand(self, n: int):
+        _check(load().coop_dev_demand(self.h, n))
+
+    def grant(self, n: int):
+        _check(load().coop_dev_grant(self.h, n))
+
+    def _stats(self):
+        st = DevStats()
+        buf = None
+        if self.m_trace_cap:
+            buf = (ctypes.c_uint32 * self.m_trace_cap)()
+            st.m_trace = buf
+            st.m_trace_cap = self.m_trace_cap
+        return st, buf
+
+    @staticmethod
+    def _to_dict(st, buf):
+        d = {k: getattr(st, k) for k, _ in DevStats._fields_ if k not in ("m_trace", "m_trace_cap")}
+        d["m_trace"] = list(buf[: min(st.episodes, len(buf))]) if buf is not None else []
+        return d
+
+    def close(self):
+        if getattr(self, "h", None):
+            load().coop_dev_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def fig4_bfs(h: DevHandle, g, source: int, levels_out=None, *, threads_per_wg=256):
+    """Fig. 4 on the device API; returns (levels int32 tensor, stats dict)."""
+    import torch
+    csr, keep = _device_csr(g, False)
+    if levels_out is None:
+        levels_out = torch.empty(g.num_vertices, dtype=torch.int32, device=g.col_idx.device)
+    st, buf = h._stats()
+    _check(load().coop_fig4_bfs(h.h, ctypes.byref(csr), int(source), levels_out.data_ptr(), threads_per_wg,
+                                ctypes.byref(st)))
+    del keep
+    return levels_out, DevHandle._to_dict(st, buf)
+
+
+def work_steal(h: DevHandle, *, seed: int, depth: int, max_fanout: int, fixed=False, rounds=0, queue_cap=0,
+               threads_per_wg=256):
+    """Cooperative work stealing (Fig. 2 + §3.2) over the implicit task tree R19.
+    Returns (result dict {count, total, hist, steals}, stats dict)."""
+    t = WsTree(seed=seed & 0xFFFFFFFFFFFFFFFF, depth=depth, max_fanout=max_fanout, fixed=1 if fixed else 0,
+               rounds=rounds, queue_cap=queue_cap)
+    r = WsResult()
+    st, buf = h._stats()
+    _check(load().coop_work_steal(h.h, ctypes.byref(t), threads_per_wg, ctypes.byref(r), ctypes.byref(st)))
+    res = {"count": r.count, "total": r.total, "hist": list(r.hist[: depth + 1]), "steals": r.steals}
+    return res, DevHandle._to_dict(st, buf)

@@ -164,7 +164,7 @@ struct BfsApp {
             cs.app_u32[5] = c->bmode[in];
             cs.app_u32[6] = c->n_bu_levels;                  // 1 during the first bottom-up level
         }
-        __syncthreads();
+        cta_sync();
         return cs.app_u32[4] == 0;
     }
 
@@ -861,7 +861,7 @@ struct SsspApp {
             cs.app_u32[6] = (uint32_t)Tlo;
             cs.app_u32[7] = (uint32_t)(Tlo >> 32);
         }
-        __syncthreads();
+        cta_sync();
         return cs.app_u32[5] == SSSP_DONE;
     }
 

@@ -24,6 +24,8 @@ using namespace coop;
 
 // ------------------------------------------------------------------ errors
 static thread_local char g_err[512];
+// shared with coop_dev_api.cu (the device-API half of the ABI)
+char *coop_internal_errbuf() { return g_err; }
 
 static coop_status fail(coop_status s, const char *fmt, ...) {
     va_list ap;

@@ -73,6 +73,20 @@ __device__ unsigned long long g_ltrace[64][1184][8];
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// CTA barrier that is safe after thread-0-only regions.  Measured on sm_100a
+// (tools/fork_repro.cu, the device-API twin of this runtime): when ptxas lays a
+// straight-line `if (threadIdx.x == 0) {...}` out as a plain forward branch
+// with no reconvergence point, lanes 1..31 reach the warp-aligned bar.sync
+// before lane 0, the warp is counted twice and the NEXT barrier releases the
+// other warps early.  ptxas deletes a plain __syncwarp() there (it believes the
+// warp converged), so the reconvergence takes a mask it cannot fold, and the
+// barrier is the non-aligned barrier.sync.
+__device__ const uint32_t g_full_mask = 0xffffffffu;
+__device__ __forceinline__ void cta_sync() {
+    __syncwarp(*(const volatile uint32_t *)&g_full_mask);
+    asm volatile("barrier.sync 0;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
@@ -363,7 +377,7 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
 #if COOP_TRACE
     long long tr0 = clock64();
 #endif
-    __syncthreads();
+    cta_sync();
     Ctl *c = p.ctl;
 #if COOP_TRACE
     long long tr1 = clock64(), tr2 = 0, tr3 = 0;
@@ -478,7 +492,7 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
         tr3 = clock64();
 #endif
     }
-    __syncthreads();
+    cta_sync();
     if (cs.last) {  // uniform
         if (threadIdx.x < 32) {
             uint32_t Mp;
@@ -491,7 +505,7 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
 #endif
             }
         }
-        __syncthreads();
+        cta_sync();
     }
 #if COOP_TRACE
     if (threadIdx.x == 0 && blockIdx.x == 0) {               // shared-memory sums: no global traffic
@@ -523,7 +537,7 @@ template <class App, class Flush>
 __device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, App &app, Flush &&flush) {
     Ctl *c = p.ctl;
     flush();
-    __syncthreads();
+    cta_sync();
     for (uint32_t spins = 0;;) {
         if (threadIdx.x == 0) {
             uint32_t act = ACT_CONT, serial = 0, Mnew = 0;
@@ -560,18 +574,18 @@ __device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, 
             cs.last = serial;
             cs.bar_M = Mnew;
         }
-        __syncthreads();
+        cta_sync();
         const uint32_t act = cs.action;
         if (act == ACT_KILLED) {
             if (cs.last) {
                 // the episode is that of resizing barrier #1, after Fig. 4's swap
                 if (threadIdx.x == 0) cs.in_sel ^= 1u;
-                __syncthreads();
+                cta_sync();
                 if (threadIdx.x < 32) {
                     uint32_t Mp;
                     serial_section(p, cs, app, cs.gen, cs.bar_M, true, ENTRY_AFTER_RB1, &Mp);
                 }
-                __syncthreads();
+                cta_sync();
             }
             return ACT_KILLED;
         }
@@ -580,7 +594,7 @@ __device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, 
             if (spin_check(p, cs, spins)) cs.action = ACT_ABORT;
             else __nanosleep(64);
         }
-        __syncthreads();
+        cta_sync();
         if (cs.action == ACT_ABORT) return ACT_ABORT;
     }
 }
@@ -621,7 +635,7 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
             cs.stop = stop;
             cs.item_next = 0;
         }
-        __syncthreads();
+        cta_sync();
         const uint32_t ch = cs.chunk, stop = cs.stop;
         if (ch < nchunks) {
             const uint64_t base = (uint64_t)ch * per_chunk;
@@ -634,7 +648,7 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
                 fn(base + it);
             }
         }
-        __syncthreads();                                   // chunk done; cs.chunk reusable
+        cta_sync();                                   // chunk done; cs.chunk reusable
         if (stop) {
             const uint32_t r = offer_kill_mid(p, cs, app, flush);
             if (r != ACT_CONT) return r;
@@ -663,7 +677,7 @@ __device__ uint32_t run_body(const KParams &p, CtaState &cs, App &app, uint32_t 
             LTRACE(0);
             r = app.template expand<BLOCK>(p, cs);             // for (i = tid; ...) process_node
             if (r != ACT_CONT) return r;                       // killed at a chunk boundary (offer_kill)
-            __syncthreads();                                   // every warp is done reading cs
+            cta_sync();                                   // every warp is done reading cs
             LTRACE(1);
             if (threadIdx.x == 0) cs.in_sel ^= 1u;            // swap(&in_nodes, &out_nodes)
             r = barrier(p, cs, app, true, ENTRY_AFTER_RB1);   // resizing_global_barrier() #1
@@ -679,7 +693,7 @@ __device__ uint32_t run_body(const KParams &p, CtaState &cs, App &app, uint32_t 
             if (threadIdx.x == 0 && cs.level >= 1 && cs.level <= 64 && blockIdx.x < 1184 && COOP_LTRACE)
                 LTRACE_RB2(cs.level - 1);
         } else {
-            __syncthreads();
+            cta_sync();
         }
     }
 }
@@ -713,7 +727,7 @@ __device__ __noinline__ void run_task_block(const KParams &p, CtaState &cs) {
         if (atomicAdd(&c->task_done, 1u) + 1 == total && cur && cur - 1 < p.events_cap)
             p.events[cur - 1].t_end = globaltimer();
     }
-    __syncthreads();
+    cta_sync();
 }
 
 // ---------------------------------------------------------------- scheduler CTA
@@ -827,7 +841,7 @@ __device__ __noinline__ void park_loop(const KParams &p, CtaState &cs, App &app)
             }
             cs.action = action;
         }
-        __syncthreads();
+        cta_sync();
         const uint32_t act = cs.action;
         if (act == ACT_EXIT) return;
         if (act == ACT_RUN_TASK) {
@@ -845,7 +859,7 @@ __device__ __noinline__ void park_loop(const KParams &p, CtaState &cs, App &app)
             cs.M = mhist_get(p, cs.gen);
             __threadfence();
         }
-        __syncthreads();
+        cta_sync();
         if (cs.action == ACT_ABORT) return;
         uint32_t r = run_body<App, BLOCK>(p, cs, app, cs.entry);
         flush_stats(p, cs);
@@ -859,7 +873,7 @@ __device__ __noinline__ void park_loop(const KParams &p, CtaState &cs, App &app)
         // killed (offer_kill accepted) or finished: back to the worker pool, where the
         // CTA can run task blocks and be forked again
         if (threadIdx.x == 0) { __threadfence(); atomicOr(&c->pool[wi], bit); }
-        __syncthreads();
+        cta_sync();
     }
 }
 
@@ -880,7 +894,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(KParams p) {
         cs.lid = blockIdx.x; cs.M = p.M0; cs.gen = 0; cs.level = 0; cs.in_sel = 0;
         if (blockIdx.x == 0) p.ctl->t_start = t0;
     }
-    __syncthreads();
+    cta_sync();
     if (p.has_sched && blockIdx.x == p.P) { scheduler_loop(p, cs); return; }
     if (blockIdx.x < p.M0) {
         uint32_t r = run_body<App, BLOCK>(p, cs, app, ENTRY_START);
@@ -896,7 +910,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(KParams p) {
             __threadfence();
             atomicOr(&p.ctl->pool[blockIdx.x >> 5], 1u << (blockIdx.x & 31));
         }
-        __syncthreads();
+        cta_sync();
     }
     if (p.barrier_mode != COOP_BARRIER_PLAIN) park_loop<App, BLOCK>(p, cs, app);
 #if COOP_TRACE

@@ -84,7 +84,7 @@ struct PartBfsApp {
             cs.app_u32[0] = p.ctl->gcount ? 1u : 0u;
             cs.app_u32[5] = p.ctl->pmode;
         }
-        __syncthreads();
+        cta_sync();
         return cs.app_u32[0] == 0;
     }
 
