@@ -406,6 +406,36 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags):
                     "episodes": st.episodes, "relaxed_edges": st.edges_scanned,
                     "us_per_episode": ms * 1e3 / max(1, st.episodes)}
     ex["sssp_grid2048"] = ss
+    # device API (include/coop_device.cuh): the paper's Fig. 4 kernel written literally on
+    # resizing_global_barrier (thread-strided, CAS claims), same RMAT-24 sources, and Fig. 2
+    # work stealing with offer_kill / request_fork at the loop head (§3.2)
+    m_graph = float(g.num_edges) / 2
+    f4 = []
+    with coop.DevHandle(policy=coop.POLICY_NEVER) as h:
+        for i in range(3):
+            t, (lv, st) = timed(lambda: coop.fig4_bfs(h, g, srcs[i], out, threads_per_wg=256))
+            f4.append(t)
+    ex["fig4_device_api_bfs"] = {"ms": statistics.median(f4), "episodes": st["episodes"],
+                                 "note": "Fig. 4 literally on the device API (2 resizing barriers/level, "
+                                         "thread-strided frontier, CAS claims); levels identical"}
+    ws_line = {}
+    tree = dict(seed=3, depth=18, max_fanout=4, rounds=16)
+    for name, kw in (("never", dict(policy=coop.POLICY_NEVER)),
+                     ("random_kill_fork", dict(policy=coop.POLICY_RANDOM, kill_prob=0.002, fork_prob=0.002,
+                                               max_fork=8, seed=5))):
+        ts, res = [], None
+        with coop.DevHandle(**kw) as h:
+            for i in range(3):
+                t, (r, st) = timed(lambda: coop.work_steal(h, **tree))
+                ts.append(t)
+                res = r if res is None else res
+                assert (r["count"], r["total"]) == (res["count"], res["total"])   # schedule independent
+        ms = statistics.median(ts)
+        ws_line[name] = {"ms": ms, "tasks": res["count"], "mtasks_per_s": res["count"] / ms / 1e3,
+                         "steals": r["steals"], "kills": st["kills"], "forks": st["forks"], "wgs": st["n_wgs"]}
+    ws_line["tree"] = tree
+    ex["work_stealing_device_api"] = ws_line
+    del m_graph
     return ex
 
 
