@@ -83,6 +83,10 @@ typedef struct {
     const int32_t *col_idx;     /* device, E entries in [0, V) */
     const uint32_t *weights;    /* device, E entries >= 1 (SSSP), NULL for BFS */
     uint32_t max_weight;        /* SSSP: max of weights (0 = unknown: the library computes it) */
+    const uint64_t *probe;      /* optional device array of V probe records {degree << 32 | first neighbour}
+                                   (first neighbour 0xFFFFFFFF if degree 0) built once per graph by
+                                   coop_csr_probe; bottom-up BFS levels then decide degree-0 vertices and
+                                   first-neighbour hits with one coalesced load.  NULL = not used. */
 } coop_csr;
 
 typedef struct {
@@ -172,6 +176,11 @@ typedef struct {
 int coop_abi_version(void);
 const char *coop_status_string(coop_status s);
 const char *coop_last_error(void);   /* thread-local description of the last failure */
+
+/* Build the probe records of g (probe_out: device uint64[V], caller-owned) on `stream`
+ * (cudaStream_t, NULL = legacy default) and wait for them.  A graph-layout step, done once per
+ * graph like building the CSR; results of coop_bfs are identical with or without it. */
+coop_status coop_csr_probe(const coop_csr *g, uint64_t *probe_out, void *stream);
 
 /* Co-residency capacity of the BFS/SSSP kernel for threads_per_wg on `device`. */
 coop_status coop_device_query(int device, uint32_t threads_per_wg, coop_device_info *out);

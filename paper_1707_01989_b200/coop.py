@@ -36,7 +36,7 @@ class CooperativeCSR(ctypes.Structure):
     _fields_ = [("num_vertices", ctypes.c_int64), ("num_edges", ctypes.c_int64),
                 ("row_offsets", ctypes.c_void_p), ("offset_bits", ctypes.c_int32),
                 ("col_idx", ctypes.c_void_p), ("weights", ctypes.c_void_p),
-                ("max_weight", ctypes.c_uint32)]
+                ("max_weight", ctypes.c_uint32), ("probe", ctypes.c_void_p)]
 
 
 class Opts(ctypes.Structure):
@@ -127,11 +127,14 @@ class WsResult(ctypes.Structure):
 
 # every function declared in include/coop.h: name -> (restype, argtypes)
 _P = ctypes.c_void_p
+# bottom-up BFS probe records (coop_csr.probe), built once per graph; COOP_PROBE=0 disables (A/B)
+USE_PROBE = os.environ.get("COOP_PROBE", "1") != "0"
 SIGNATURES = {
     "coop_abi_version": (ctypes.c_int, []),
     "coop_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "coop_last_error": (ctypes.c_char_p, []),
     "coop_device_query": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint32, ctypes.POINTER(DeviceInfo)]),
+    "coop_csr_probe": (ctypes.c_int, [ctypes.POINTER(CooperativeCSR), _P, _P]),
     "coop_bfs": (ctypes.c_int, [ctypes.POINTER(CooperativeCSR), ctypes.c_int64, _P, ctypes.POINTER(Opts),
                                 ctypes.POINTER(Stats)]),
     "coop_sssp": (ctypes.c_int, [ctypes.POINTER(CooperativeCSR), ctypes.c_int64, _P, ctypes.POINTER(Opts),
@@ -251,12 +254,20 @@ def _device_csr(g, need_weights: bool):
         w = g.weights.to(torch.int32).contiguous()
     c = CooperativeCSR(g.num_vertices, E, ro.data_ptr(), bits, col.data_ptr() if E else None,
                        w.data_ptr() if (w is not None and E) else None,
-                       int(getattr(g, "max_weight", 0) or 0))
+                       int(getattr(g, "max_weight", 0) or 0), None)
+    probe = None
+    if USE_PROBE and g.num_vertices > 0:
+        # graph layout step (once per graph, like the CSR conversion above): per-vertex
+        # {degree | first neighbour} records for the bottom-up BFS levels
+        probe = torch.empty(g.num_vertices, dtype=torch.int64, device=col.device)
+        _check(load().coop_csr_probe(ctypes.byref(c), probe.data_ptr(), None))
+        c.probe = probe.data_ptr()
+    keep = (ro, col, w, probe)
     try:
-        g._coop_cache = (c, (ro, col, w), w)   # converted arrays are reused by later calls
+        g._coop_cache = (c, keep, w)   # converted arrays are reused by later calls
     except AttributeError:
         pass
-    return c, (ro, col, w)
+    return c, keep
 
 
 def make_opts(*, max_wgs=0, init_wgs=0, threads_per_wg=0, barrier_mode=BARRIER_QUERY, barriers_per_level=1,

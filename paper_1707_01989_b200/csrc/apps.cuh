@@ -592,17 +592,48 @@ struct BfsApp {
                 b[k] = 0;
                 e[k] = 0;
                 found[k] = false;
-                if (bit[k] < 32) {
+                if (bit[k] < 32 && !p.probe) {
                     const uint64_t v = (w0 + o) * 32 + bit[k];
                     b[k] = __ldg(ro + v);
                     e[k] = __ldg(ro + v + 1);
                 }
             }
             uint32_t deg[K];
+            if (p.probe) {
+                // probe records {degree | first neighbour}: one coalesced 8-B load decides
+                // degree-0 vertices and first-neighbour hits (most candidates of a dense
+                // level) without the row offsets or a random column sector
+                unsigned long long rec[K];
+                OffT b0[K];
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                deg[k] = (uint32_t)(e[k] - b[k]);
-                if (bit[k] < 32 && deg[k] == 0) atomicOr(&s_dead[own[k]], 1u << bit[k]);   // never a neighbour
+                for (int k = 0; k < K; ++k) {   // the offset is loaded alongside (coalesced, independent)
+                    const uint64_t v = (w0 + own[k]) * 32 + bit[k];
+                    rec[k] = bit[k] < 32 ? __ldg(p.probe + v) : 0ull;
+                    b0[k] = bit[k] < 32 ? __ldg(ro + v) : (OffT)0;
+                }
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    deg[k] = (uint32_t)(rec[k] >> 32);
+                    const uint32_t f = (uint32_t)rec[k];
+                    if (bit[k] < 32 && deg[k] == 0) atomicOr(&s_dead[own[k]], 1u << bit[k]);   // never a neighbour
+                    if (deg[k]) {
+                        found[k] = (fcur[f >> 5] >> (f & 31)) & 1u;
+                        scanned += 1;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    if (deg[k] > 1 && !found[k]) {   // the rest of the list from the second entry
+                        b[k] = b0[k] + 1;
+                        e[k] = b0[k] + deg[k];
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    deg[k] = (uint32_t)(e[k] - b[k]);
+                    if (bit[k] < 32 && deg[k] == 0) atomicOr(&s_dead[own[k]], 1u << bit[k]);   // never a neighbour
+                }
             }
             for (int step = 0; step < COOP_BU_SOLO; ++step) {   // per-lane: the first hits dominate
                 bool more = false;

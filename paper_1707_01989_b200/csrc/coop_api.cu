@@ -103,6 +103,18 @@ __global__ void max_u32_kernel(const uint32_t *w, int64_t n, uint32_t *out) {
     if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
+// probe records {degree << 32 | first neighbour} (coop_csr_probe): coalesced offsets in,
+// one column per vertex, coalesced records out
+template <typename OffT>
+__global__ void probe_kernel(const OffT *ro, const int32_t *col, int64_t V, unsigned long long *out) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+        const OffT b = ro[v], e = ro[v + 1];
+        const uint32_t d = (uint32_t)(e - b);
+        const uint32_t f = d ? (uint32_t)__ldg(col + b) : 0xFFFFFFFFu;
+        out[v] = ((unsigned long long)d << 32) | f;
+    }
+}
+
 __global__ void l2_rtt_kernel(unsigned long long *word, uint64_t iters, unsigned long long *out_ns) {
     unsigned long long v = 0;
     const uint64_t t0 = globaltimer();
@@ -169,6 +181,26 @@ static coop_status occupancy(void *kern, uint32_t threads, int *sm_count, int *p
     CUDA_TRY(cudaGetDevice(&dev));
     CUDA_TRY(cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev));
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, (int)threads, 0));
+    return COOP_OK;
+}
+
+extern "C" coop_status coop_csr_probe(const coop_csr *g, uint64_t *probe_out, void *stream) {
+    if (!g || !probe_out || !g->row_offsets || (!g->col_idx && g->num_edges > 0))
+        return fail(COOP_ERR_INVALID_ARG, "NULL graph / output");
+    if (g->num_vertices < 1 || g->num_vertices > (int64_t)INT32_MAX) return fail(COOP_ERR_INVALID_ARG, "bad V");
+    if (g->offset_bits != 32 && g->offset_bits != 64) return fail(COOP_ERR_INVALID_ARG, "offset_bits must be 32 or 64");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    unsigned long long *out = reinterpret_cast<unsigned long long *>(probe_out);
+    int dev = 0, sms = 148;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (g->offset_bits == 32)
+        probe_kernel<<<sms * 8, 256, 0, s>>>(static_cast<const uint32_t *>(g->row_offsets), g->col_idx, g->num_vertices, out);
+    else
+        probe_kernel<<<sms * 8, 256, 0, s>>>(static_cast<const unsigned long long *>(g->row_offsets), g->col_idx,
+                                             g->num_vertices, out);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(s));
     return COOP_OK;
 }
 
@@ -369,6 +401,7 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
         kp.off64 = off64;
         kp.col = g->col_idx;
         kp.w = g->weights;
+        kp.probe = reinterpret_cast<const unsigned long long *>(g->probe);
         kp.source = r.source;
         kp.E = g->num_edges;
         if (r.app == APP_BFS) kp.level_out = static_cast<int32_t *>(r.out);

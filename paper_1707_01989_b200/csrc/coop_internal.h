@@ -160,6 +160,7 @@ struct KParams {
     int off64;
     const int32_t *col;
     const uint32_t *w;
+    const unsigned long long *probe;   // optional per-vertex {degree:32 | first neighbour:32} (coop_csr.probe)
     int64_t source;
     // outputs
     int32_t *level_out;
