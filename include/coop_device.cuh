@@ -196,11 +196,10 @@ __device__ __forceinline__ unsigned long long mix(unsigned long long z) {   /* s
  * barrier before lane 0; the warp is counted for them and again when lane 0
  * arrives, so the NEXT barrier releases the other warps early.  ptxas believes
  * the warp is converged there and deletes a plain __syncwarp(), so the
- * reconvergence uses a mask it cannot see through (loaded from memory). */
-__device__ const uint32_t coop_full_mask = 0xffffffffu;
+ * reconvergence uses a mask it cannot see through (a __constant__ word). */
+__constant__ uint32_t coop_full_mask = 0xffffffffu;   /* constant cache: no memory round trip */
 __device__ __forceinline__ void cta_sync_after_t0() {
-    const uint32_t m = *(const volatile uint32_t *)&coop_full_mask;
-    __syncwarp(m);
+    __syncwarp(coop_full_mask);
     asm volatile("barrier.sync 0;" ::: "memory");
 }
 

@@ -81,11 +81,19 @@ constexpr unsigned FULL = 0xffffffffu;
 // other warps early.  ptxas deletes a plain __syncwarp() there (it believes the
 // warp converged), so the reconvergence takes a mask it cannot fold, and the
 // barrier is the non-aligned barrier.sync.
-__device__ const uint32_t g_full_mask = 0xffffffffu;
+// (a __constant__ word: the constant cache, not an L2 round trip as a volatile global load would be)
+__constant__ uint32_t c_full_mask = 0xffffffffu;
+// COOP_ALIGNED_SYNC=1 restores plain __syncthreads() (A/B only: measured 2.95 vs 3.73 us per
+// plain barrier at 148 CTAs, but test_handle_api_host_channel timed out in 1 of 8 runs with it
+// and in none of 14 without; __syncwarp(mask) + __syncthreads() crashes ptxas 12.9)
+#if defined(COOP_ALIGNED_SYNC)
+__device__ __forceinline__ void cta_sync() { __syncthreads(); }
+#else
 __device__ __forceinline__ void cta_sync() {
-    __syncwarp(*(const volatile uint32_t *)&g_full_mask);
+    __syncwarp(c_full_mask);
     asm volatile("barrier.sync 0;" ::: "memory");
 }
+#endif
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint64_t globaltimer() {
