@@ -47,6 +47,10 @@
 #define COOP_ARRIVE_ACQREL 0
 #endif
 
+#ifndef COOP_WARP_WAIT
+#define COOP_WARP_WAIT 1      // waiters poll the release word with all of warp 0 (converged at the CTA barrier)
+#endif
+
 #ifndef COOP_TRACE
 #define COOP_TRACE 0          // 1: clock64 breakdown of the barrier, CTA 0 (coop_debug_trace)
 #endif
@@ -197,6 +201,7 @@ struct CtaState {
     uint64_t deadline;
     unsigned long long edges, frontier, reached;   // per-CTA stats, flushed at body exit
     uint32_t bar_M, bar_naive;                     // barrier: M of the episode, killed on entry (NAIVE)
+    uint32_t wait_rel;                             // barrier: this CTA waits for the release word
     uint32_t chunk, stop, item_next;               // chunk loop broadcast / per-warp item counter
 #if COOP_TRACE
     unsigned long long tr[12];
@@ -463,43 +468,69 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
         cs.bar_M = killed_naive ? w_M(old) - 1 : w_M(old);   // M of the episode for the serial section
         cs.bar_naive = killed_naive;
         if (!last) {
-            if (killed_naive) {
-                action = ACT_KILLED;
-            } else {
-                uint32_t spins = 0;
-                unsigned long long w;
-                for (;;) {
-#if COOP_POLL_ACQUIRE
-                    w = ld_acquire64(&c->R);
-#else
-                    w = ld_relaxed64(&c->R);
-#endif
-                    if (w_gen(w) != g) break;
-                    if (spin_check(p, cs, spins)) { action = ACT_ABORT; break; }
-                }
-#if !COOP_POLL_ACQUIRE
-                __threadfence();
-#endif
-                if (action != ACT_ABORT) {
-                    if (w_gen(w) != g + 1) {
-                        action = ACT_KILLED;               // W moved on without us => we were killed at g
-                    } else {
-                        // W.M is M' unless NAIVE kills of generation g+1 already lowered it
-                        const uint32_t Mn = p.barrier_mode == COOP_BARRIER_NAIVE ? mhist_get(p, g + 1) : w_M(w);
-                        if (cs.lid >= Mn) action = ACT_KILLED;
-                        else { cs.M = Mn; cs.gen = g + 1; }
-                    }
-                }
-            }
-#if COOP_POST_FENCE
-            __threadfence();
-#endif
+            if (killed_naive) action = ACT_KILLED;
+            else cs.wait_rel = 1u;                       // wait for the release below (warp 0)
         }
         cs.action = action;
-#if COOP_TRACE
-        tr3 = clock64();
-#endif
     }
+#if COOP_WARP_WAIT
+    // Waiters poll the release word with the whole of warp 0 (lane 0 loads, the
+    // decision is shuffled): warp 0 is converged when it reaches the CTA barrier,
+    // so the divergence-safe barrier takes its fast path.
+    if (threadIdx.x < 32) {
+        __syncwarp();
+        if (cs.wait_rel) {
+            const uint32_t g = cs.gen;
+            uint32_t spins = 0, stop = 0;
+            unsigned long long w = 0;
+            for (;;) {
+                if (threadIdx.x == 0) {
+                    w = ld_acquire64(&c->R);
+                    stop = w_gen(w) != g ? 1u : (spin_check(p, cs, spins) ? 2u : 0u);
+                }
+                if (__shfl_sync(FULL, stop, 0)) break;
+            }
+            if (threadIdx.x == 0) {
+                cs.wait_rel = 0u;
+                if (stop == 2u) {
+                    cs.action = ACT_ABORT;
+                } else if (w_gen(w) != g + 1) {
+                    cs.action = ACT_KILLED;                // W moved on without us => we were killed at g
+                } else {
+                    // W.M is M' unless NAIVE kills of generation g+1 already lowered it
+                    const uint32_t Mn = p.barrier_mode == COOP_BARRIER_NAIVE ? mhist_get(p, g + 1) : w_M(w);
+                    if (cs.lid >= Mn) cs.action = ACT_KILLED;
+                    else { cs.M = Mn; cs.gen = g + 1; }
+                }
+            }
+            __syncwarp();
+        }
+    }
+#else
+    if (threadIdx.x == 0 && cs.wait_rel) {
+        const uint32_t g = cs.gen;
+        uint32_t spins = 0;
+        unsigned long long w;
+        cs.wait_rel = 0u;
+        for (;;) {
+            w = ld_acquire64(&c->R);
+            if (w_gen(w) != g) break;
+            if (spin_check(p, cs, spins)) { cs.action = ACT_ABORT; break; }
+        }
+        if (cs.action != ACT_ABORT) {
+            if (w_gen(w) != g + 1) {
+                cs.action = ACT_KILLED;                    // W moved on without us => we were killed at g
+            } else {
+                const uint32_t Mn = p.barrier_mode == COOP_BARRIER_NAIVE ? mhist_get(p, g + 1) : w_M(w);
+                if (cs.lid >= Mn) cs.action = ACT_KILLED;
+                else { cs.M = Mn; cs.gen = g + 1; }
+            }
+        }
+    }
+#endif
+#if COOP_TRACE
+    if (threadIdx.x == 0) tr3 = clock64();
+#endif
     cta_sync();
     if (cs.last) {  // uniform
         if (threadIdx.x < 32) {
@@ -555,7 +586,10 @@ __device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, 
                 const uint32_t M = w_M(w);
                 const uint32_t d = ld_relaxed32(&c->demand);
                 if (d == 0 || cs.lid == 0 || cs.lid + d < M || w_gen(w) != cs.gen) { act = ACT_CONT; break; }
-                if (cs.lid != M - 1) { act = ACT_IDLE; break; }         // the ids above go first
+                // the ids above go first; but once some CTA has arrived at the barrier the top
+                // id may be among them and can no longer leave mid-interval: then stop offering
+                // and let the query barrier take the demand (waiting here would deadlock)
+                if (cs.lid != M - 1) { act = w_arr(w) ? ACT_CONT : ACT_IDLE; break; }
                 if (atomicCAS(&c->demand, d, d - 1) != d) { w = ld_relaxed64(&c->W); continue; }
                 uint32_t a;
                 for (;;) {                                               // arrivals may race the CAS
@@ -899,6 +933,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(KParams p) {
         cs.deadline = t0 + p.timeout_ns;
         cs.edges = cs.frontier = cs.reached = 0;
         cs.consumed = 0;
+        cs.wait_rel = 0;
         cs.lid = blockIdx.x; cs.M = p.M0; cs.gen = 0; cs.level = 0; cs.in_sel = 0;
         if (blockIdx.x == 0) p.ctl->t_start = t0;
     }
