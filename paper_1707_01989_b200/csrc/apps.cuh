@@ -33,7 +33,7 @@
 #define COOP_BU_K 4           // bottom-up (compacted): candidates per lane per round
 #endif
 #ifndef COOP_BU_SOLO
-#define COOP_BU_SOLO 8        // bottom-up (compacted): per-lane steps before the warp takes a list over
+#define COOP_BU_SOLO 12       // bottom-up (compacted): per-lane steps before the warp takes a list over (sweep: profiles/r01b_bu_probe_variants.log)
 #endif
 #ifndef COOP_BU_DENSE_W
 #define COOP_BU_DENSE_W 16    // bottom-up (compacted): words per item in the first (dense) level
