@@ -167,8 +167,12 @@ static coop_status get_scratch(Scratch **out, uint32_t ws) {
     Scratch *s = &g_scratch[dev][ws];
     if (!s->host_ctl) {   // all workspaces of the device at once (no allocation while a kernel runs)
         for (uint32_t k = 0; k < kWorkspaces; ++k)
-            if (!g_scratch[dev][k].host_ctl)
-                CUDA_TRY(cudaHostAlloc((void **)&g_scratch[dev][k].host_ctl, sizeof(Ctl), cudaHostAllocDefault));
+            if (!g_scratch[dev][k].host_ctl) {
+                // control block + zeroed mailboxes: one pinned staging buffer, one H2D copy per call
+                const size_t bytes = sizeof(Ctl) + sizeof(Mailbox) * kMaxCtas;
+                CUDA_TRY(cudaHostAlloc((void **)&g_scratch[dev][k].host_ctl, bytes, cudaHostAllocDefault));
+                memset((void *)g_scratch[dev][k].host_ctl, 0, bytes);
+            }
     }
     s->device = dev;
     *out = s;
@@ -176,11 +180,27 @@ static coop_status get_scratch(Scratch **out, uint32_t ws) {
 }
 
 // ------------------------------------------------------------------ device info
+// co-residency capacity, cached per (device, kernel, block size): the occupancy query is a
+// host-side cost on every call otherwise (the GPU idles while the next call prepares)
 static coop_status occupancy(void *kern, uint32_t threads, int *sm_count, int *per_sm) {
+    struct Entry { int dev; void *kern; uint32_t threads; int sms, per; };
+    static std::mutex mu;
+    static std::vector<Entry> cache;
     int dev = 0;
     CUDA_TRY(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (const Entry &e : cache)
+            if (e.dev == dev && e.kern == kern && e.threads == threads) {
+                *sm_count = e.sms;
+                *per_sm = e.per;
+                return COOP_OK;
+            }
+    }
     CUDA_TRY(cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev));
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, (int)threads, 0));
+    std::lock_guard<std::mutex> lk(mu);
+    cache.push_back(Entry{dev, kern, threads, *sm_count, *per_sm});
     return COOP_OK;
 }
 
@@ -451,8 +471,7 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
     // ---- scratch
     const uint64_t V = r.app == APP_BARRIER ? 0 : (uint64_t)kp.V;
     const uint64_t E = (r.app == APP_BARRIER || r.app == APP_PBFS) ? 0 : (uint64_t)r.g->num_edges;
-    CUDA_TRY(s->ctl.ensure(sizeof(Ctl)));
-    CUDA_TRY(s->mb.ensure(sizeof(Mailbox) * P));
+    CUDA_TRY(s->ctl.ensure(sizeof(Ctl) + sizeof(Mailbox) * kMaxCtas));   // mailboxes follow the control block
     CUDA_TRY(s->stamp.ensure(4ull * kMaxCtas));
     const uint32_t mcap = 1u << 16, lcap = 1u << 16, ecap = 4096;
     CUDA_TRY(s->mtrace.ensure(4ull * mcap));
@@ -505,7 +524,7 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
     kp.qlight[0] = s->ql0.p;
     kp.qlight[1] = s->ql1.p;
     kp.ctl = static_cast<Ctl *>(s->ctl.p);
-    kp.mb = static_cast<Mailbox *>(s->mb.p);
+    kp.mb = reinterpret_cast<Mailbox *>(static_cast<char *>(s->ctl.p) + sizeof(Ctl));
     kp.stamp = static_cast<uint32_t *>(s->stamp.p);
     kp.m_trace = static_cast<uint32_t *>(s->mtrace.p);
     kp.m_trace_cap = mcap;
@@ -552,8 +571,9 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
     h->max_m = M0;
     h->task_next = 0xFFFFFFFFu;
     for (uint32_t b = M0; b < P; ++b) h->pool[b >> 5] |= 1u << (b & 31);
-    CUDA_TRY(cudaMemcpyAsync(kp.ctl, h, sizeof(Ctl), cudaMemcpyHostToDevice, stream));
-    CUDA_TRY(cudaMemsetAsync(kp.mb, 0, sizeof(Mailbox) * P, stream));
+    // one copy: the control block and the P mailboxes behind it (the staging buffer's mailbox
+    // part is zero and never written on the host)
+    CUDA_TRY(cudaMemcpyAsync(kp.ctl, h, sizeof(Ctl) + sizeof(Mailbox) * P, cudaMemcpyHostToDevice, stream));
     if (sched) CUDA_TRY(cudaMemsetAsync(kp.events, 0, sizeof(TaskEventDev) * ecap, stream));
     pr->kp = kp;
     pr->kern = kern;
