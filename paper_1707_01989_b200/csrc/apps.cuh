@@ -35,6 +35,9 @@
 #ifndef COOP_BU_SOLO
 #define COOP_BU_SOLO 12       // bottom-up (compacted): per-lane steps before the warp takes a list over (sweep: profiles/r01b_bu_probe_variants.log)
 #endif
+#ifndef COOP_SSSP_PRECHECK
+#define COOP_SSSP_PRECHECK 0  // SSSP: read dist[v] before the atomicMin (fewer atomics, one more dependent round trip: 73.4 vs 68.4 ms on the 2048^2 grid without it)
+#endif
 #ifndef COOP_BU_DENSE_W
 #define COOP_BU_DENSE_W 16    // bottom-up (compacted): words per item in the first (dense) level
 #endif
@@ -848,6 +851,7 @@ struct BfsApp {
 // entries with dist < T + delta to near (T += delta) and compacts the rest.
 // The fixpoint -- and so every distance -- is the same as plain Bellman-Ford.
 enum : uint32_t { SSSP_RELAX = 0, SSSP_DRAIN = 1, SSSP_DONE = 2 };
+constexpr uint32_t kNoRound = 0xFFFFFFFFu;   // low word of an SSSP key not pushed to a near worklist
 
 template <typename OffT>
 struct SsspApp {
@@ -860,10 +864,11 @@ struct SsspApp {
         const uint64_t tid = (uint64_t)cs.lid * BLOCK + threadIdx.x;
         const uint64_t nth = (uint64_t)cs.M * BLOCK;
         const int64_t V = p.V, s = p.source;
-        for (uint64_t i = tid; i < (uint64_t)V; i += nth) {
-            p.dist_out[i] = (int64_t)i == s ? 0u : 0xFFFFFFFFu;
-            p.qlev[i] = 0u;
-        }
+        // key[v] = {dist:32 | ~round:32}: one 64-bit atomicMin both relaxes dist[v] and tells
+        // whether v was already pushed to the near worklist of this round (low word ~r1; far
+        // improvements and the initial state carry ~0 = "no round"); dist_out is written at the end
+        for (uint64_t i = tid; i < (uint64_t)V; i += nth)
+            p.dq[i] = (int64_t)i == s ? (unsigned long long)kNoRound : ~0ull;
         if (cs.lid == 0 && threadIdx.x == 0) {
             Ctl *c = p.ctl;
             static_cast<uint32_t *>(p.qlight[0])[0] = (uint32_t)s;
@@ -893,7 +898,13 @@ struct SsspApp {
             cs.app_u32[7] = (uint32_t)(Tlo >> 32);
         }
         cta_sync();
-        return cs.app_u32[5] == SSSP_DONE;
+        const bool done = cs.app_u32[5] == SSSP_DONE;
+        if (done) {   // every active CTA copies its stride of the distances out (the kernel's output)
+            const uint64_t nth = (uint64_t)cs.M * blockDim.x;
+            for (uint64_t i = (uint64_t)cs.lid * blockDim.x + threadIdx.x; i < (uint64_t)p.V; i += nth)
+                p.dist_out[i] = (uint32_t)(ldcg(p.dq + i) >> 32);
+        }
+        return done;
     }
 
     uint32_t r1_cur;
@@ -901,8 +912,8 @@ struct SsspApp {
 
     // push v into the next near worklist (once per round) or into the far pile;
     // warp-collective, `who` = lane pushes somewhere, `near` selects the pile
-    __device__ __forceinline__ void push(const KParams &p, bool who, bool near, uint32_t v, uint32_t out,
-                                         uint32_t fout) {
+    __device__ __forceinline__ void push(const KParams &p, bool who, bool near, uint32_t v, uint32_t dval,
+                                         uint32_t out, uint32_t fout) {
         const uint32_t lane = threadIdx.x & 31;
         const uint32_t lt = lanemask_lt();
         const uint32_t mn = __ballot_sync(FULL, who && near);
@@ -921,8 +932,11 @@ struct SsspApp {
                 const uint32_t slot = pos + __popc(mf & lt);
                 if (slot < p.far_cap) {
                     p.far[fout][slot] = v;
-                } else if (atomicMax(p.qlev + v, r1_of(p)) < r1_of(p)) {   // far pile full: relax it early
-                    static_cast<uint32_t *>(p.qlight[out])[atomicAdd(&p.ctl->qsize[out], 1u)] = v;
+                } else {                                                   // far pile full: relax it early
+                    const uint32_t mark = ~r1_of(p);
+                    const unsigned long long o = atomicMin(p.dq + v, ((unsigned long long)dval << 32) | mark);
+                    if ((uint32_t)o != mark && (uint32_t)(o >> 32) >= dval)
+                        static_cast<uint32_t *>(p.qlight[out])[atomicAdd(&p.ctl->qsize[out], 1u)] = v;
                 }
             }
         }
@@ -947,7 +961,7 @@ struct SsspApp {
             const uint32_t v = ldcg(inq + i);
             beg = __ldg(ro + v);
             deg = (uint32_t)(__ldg(ro + v + 1) - beg);
-            du = ldcg(p.dist_out + v);                         // current dist[u] (reading R8)
+            du = (uint32_t)(ldcg(p.dq + v) >> 32);             // current dist[u] (reading R8)
         }
         const uint32_t incl = warp_incl_scan(deg), excl = incl - deg;
         const uint32_t total = __shfl_sync(FULL, incl, 31);
@@ -966,19 +980,26 @@ struct SsspApp {
             const uint32_t dsrc = __shfl_sync(FULL, du, j);
             bool who = false, near = true;
             int32_t v = -1;
+            uint32_t nd = 0;
             if (e < total) {
                 const OffT k = b + (e - ex);
                 v = __ldg(col + k);
-                const uint32_t nd = dsrc + __ldg(wt + k);
-                if (nd < ldcg(p.dist_out + v)) {                      // pre-check
-                    const uint32_t old = atomicMin(p.dist_out + v, nd);   // relax
-                    if (nd < old) {
-                        near = nd < T;
-                        who = near ? atomicMax(p.qlev + v, r1) < r1 : true;
-                    }
+                nd = dsrc + __ldg(wt + k);
+                if (!COOP_SSSP_PRECHECK || nd < (uint32_t)(ldcg(p.dq + v) >> 32)) {   // pre-check
+                    near = nd < T;
+                    const uint32_t mark = near ? ~r1 : kNoRound;
+                    const unsigned long long old = atomicMin(p.dq + v, ((unsigned long long)nd << 32) | mark);
+                    const uint32_t od = (uint32_t)(old >> 32);
+                    if (nd < od)                                        // relaxed; near: once per round
+                        who = near ? (uint32_t)old != mark : true;
+                    else if (near && nd == od && (uint32_t)old != mark)
+                        // an equal distance replaced an older round mark with this round's:
+                        // v now looks queued for this round, so queue it (a harmless extra
+                        // expansion; otherwise a later improvement this round would skip it)
+                        who = true;
                 }
             }
-            push(p, who, near, (uint32_t)v, out, fsel);
+            push(p, who, near, (uint32_t)v, nd, out, fsel);
         }
     }
 
@@ -1000,14 +1021,17 @@ struct SsspApp {
         bool have = i < nf;
         if (have) {
             v = ldcg(fin + i);
-            d = ldcg(p.dist_out + v);
+            d = (uint32_t)(ldcg(p.dq + v) >> 32);
         }
         have = have && d >= Tlo;
         const bool near = have && d < T;
         bool who = have && !near;
-        if (near) who = atomicMax(p.qlev + v, r1) < r1;    // once per round
+        if (near) {                                          // once per round
+            const unsigned long long o = atomicMin(p.dq + v, ((unsigned long long)d << 32) | ~r1);
+            who = (uint32_t)o != ~r1;
+        }
         if (have && !near) atomicMin(&p.ctl->far_min, d);
-        push(p, who, near, v, out, fsel ^ 1u);
+        push(p, who, near, v, d, out, fsel ^ 1u);
         __threadfence();   // far_min (RED) is read by the serial section
     }
 

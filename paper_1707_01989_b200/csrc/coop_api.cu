@@ -508,10 +508,10 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
         CUDA_TRY(s->visited.ensure(4 * ((nown + 31) / 32) + 4));
         kp.visited = static_cast<uint32_t *>(s->visited.p);
     } else if (r.app == APP_SSSP) {
-        CUDA_TRY(s->qlev.ensure(4 * V));
+        CUDA_TRY(s->qlev.ensure(8 * V));
         CUDA_TRY(s->ql0.ensure(4 * V));
         CUDA_TRY(s->ql1.ensure(4 * V));
-        kp.qlev = static_cast<uint32_t *>(s->qlev.p);
+        kp.dq = static_cast<unsigned long long *>(s->qlev.p);
         if (o.sssp_delta) {   // far piles: every entry is one distance improvement, so <= E + V
             CUDA_TRY(s->far0.ensure(4 * (E + V)));
             CUDA_TRY(s->far1.ensure(4 * (E + V)));

@@ -169,7 +169,8 @@ struct KParams {
     Ctl *ctl;
     Mailbox *mb;
     uint32_t *visited;          // BFS bitmap [ceil(V/32)]
-    uint32_t *qlev;             // SSSP dedupe [V]
+    uint32_t *qlev;             // (unused by the current SSSP)
+    unsigned long long *dq;     // SSSP keys {dist:32 | ~round:32} [V]
     void *qlight[2];            // BFS light entries / SSSP vertex ids
     HeavyEntry *qheavy[2];
     uint32_t *stamp;            // barrier bench message passing [kMaxCtas]
