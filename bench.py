@@ -16,9 +16,9 @@ L2 atomic round trip, and SSSP on the 2048x2048 grid (configs[1]).
 
 --impl reference times the oracle (oracle/textbook.c, 1 host core) on the same
 workload: the base contract's reference arm for this tier.
-Under torchrun (N>1): rank 0 prints; per-rank independent replicas of the
-single-GPU step are timed (max over ranks) until the partitioned path is the
-default.
+Under torchrun (N>1): the 1-D vertex-partitioned BFS (configs[4]),
+weak scaling with 2^24 vertices per GPU, frontier exchanged inside the kernel
+over NVLink peer memory; time = max over ranks, rank 0 prints.
 """
 from __future__ import annotations
 
@@ -421,7 +421,7 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags):
     ws_line = {}
     tree = dict(seed=3, depth=18, max_fanout=4, rounds=16)
     for name, kw in (("never", dict(policy=coop.POLICY_NEVER)),
-                     ("random_kill_fork", dict(policy=coop.POLICY_RANDOM, kill_prob=0.002, fork_prob=0.002,
+                     ("random_kill_fork", dict(policy=coop.POLICY_RANDOM, kill_prob=0.02, fork_prob=0.02,
                                                max_fork=8, seed=5))):
         ts, res = [], None
         with coop.DevHandle(**kw) as h:
