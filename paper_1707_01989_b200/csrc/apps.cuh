@@ -35,6 +35,9 @@
 #ifndef COOP_BU_SOLO
 #define COOP_BU_SOLO 12       // bottom-up (compacted): per-lane steps before the warp takes a list over (sweep: profiles/r01b_bu_probe_variants.log)
 #endif
+#ifndef COOP_BU_CHUNK
+#define COOP_BU_CHUNK 16u     // bottom-up items per mid-interval claim (scheduler policy only)
+#endif
 #ifndef COOP_SSSP_PRECHECK
 #define COOP_SSSP_PRECHECK 0  // SSSP: read dist[v] before the atomicMin (fewer atomics, one more dependent round trip: 73.4 vs 68.4 ms on the 2048^2 grid without it)
 #endif
@@ -775,7 +778,9 @@ struct BfsApp {
             // the first bottom-up level is dense (most vertices still open): smaller
             // items so the static split stays balanced; later levels: 32 words
             const uint32_t W = cs.app_u32[6] <= 1 ? COOP_BU_DENSE_W : 32u;
-            r = claim_items<BLOCK>(p, cs, *this, &p.ctl->chunk[in], (nw + W - 1) / W, 16u, [&](uint64_t it) {
+            // chunk = items claimed per CTA claim; only used when a scheduler can ask for workgroups
+            // mid-interval (static split otherwise): it bounds the offer_kill latency
+            r = claim_items<BLOCK>(p, cs, *this, &p.ctl->chunk[in], (nw + W - 1) / W, COOP_BU_CHUNK, [&](uint64_t it) {
                 bu_compact<COOP_BU_K>(p, cs, it * W, nw, W, &s_bits[0][wb], &s_bits[1][wb], edges, reached, mfsum);
             }, flush);
         } else if (mode == BFS_BU) {                          // item = BU_KW 32-vertex words
