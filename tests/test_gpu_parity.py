@@ -242,6 +242,24 @@ def test_handle_api_host_channel(coop):
     np.testing.assert_array_equal(lv.cpu().numpy(), tb.bfs(g, 0))
 
 
+def test_handle_api_repeated_mid_interval_demand(coop):
+    """Regression for the mid-interval offer_kill deadlock: demand
+    posted while CTAs are already arriving at the barrier must not leave a demanded
+    non-top CTA waiting for a top id that can no longer leave.  The original bug hung
+    about 1 run in 8 of this scenario; 12 runs here."""
+    g = gg.grid(300, 300)
+    gd = _dev(g)
+    ref = tb.bfs(g, 0)
+    out = torch.empty(g.num_vertices, dtype=torch.int32, device="cuda")
+    for i in range(12):
+        with coop.Handle("bfs", gd, 0, out, threads_per_wg=256, max_wgs=32, timeout_ns=5_000_000_000) as h:
+            h.submit_task(8, 16, 10_000)
+            h.demand(2 + i % 3)
+            h.grant(2)
+            h.wait(event_cap=16)
+        np.testing.assert_array_equal(out.cpu().numpy(), ref)
+
+
 # ---------------------------------------------------------------- barrier
 @pytest.mark.parametrize("n", [148, 296, 592])
 def test_barrier_bench_invariants(coop, n):
