@@ -66,6 +66,22 @@ if what in ("all", "bfs"):
                 ts.append(t)
             print(json.dumps({"bfs": True, "flags": flags, "threads": threads, "ms": sorted(ts)[len(ts) // 2],
                               "levels": st.levels, "bu": st.bottom_up_levels}), flush=True)
+if what == "c4":   # BASELINE.json configs[3]: 148-1184 CTAs, 1e6 barriers, random resizes p in {0, 1/64, 1/8}
+    rtt = coop.l2_atomic_rtt(200000)
+    print(json.dumps({"l2_atomic_rtt_ns": rtt}), flush=True)
+    iters = int(os.environ.get("ITERS", "1000000"))
+    for n in (148, 296, 444, 592, 740, 888, 1036, 1184):
+        r = coop.barrier_bench(n, iters, threads=128, plain=True)
+        print(json.dumps({"c4": True, "ctas": n, "p": "plain", "ns_per_barrier": r["ns_per_barrier"],
+                          "ratio_to_rtt": r["ns_per_barrier"] / rtt}), flush=True)
+        for pr in (0.0, 1 / 64, 1 / 8):
+            r = coop.barrier_bench(n, iters, threads=128, resize_prob=pr, seed=3)
+            print(json.dumps({"c4": True, "ctas": n, "p": pr, "ns_per_barrier": r["ns_per_barrier"],
+                              "ratio_to_rtt": r["ns_per_barrier"] / rtt, "kills": r["kills"], "forks": r["forks"]}),
+                  flush=True)
+        r = coop.barrier_bench(n, iters // 10, threads=128, resize_prob=1 / 8, seed=4, check=True)
+        print(json.dumps({"c4_check": True, "ctas": n, "p": 1 / 8, "iters": iters // 10, "kills": r["kills"],
+                          "forks": r["forks"], "violations": r["violations"]}), flush=True)
 if what in ("all", "barrier_small"):
     for n in (1, 2, 4, 8, 16, 32, 64, 148):
         r = coop.barrier_bench(n, 100000, threads=128, plain=True)
