@@ -196,6 +196,13 @@ def run_ours(args, ws, rank, local):
     V, E = g.num_vertices, g.num_edges
     deg = g.degrees()
     srcs = gg.sample_sources(g, 64, seed=2)
+    # graph layout for BFS (once per graph, untimed like the graph generation): hub-first
+    # neighbour order + probe records, built by libcoop kernels (coop_csr_hub_first / _probe)
+    torch.cuda.synchronize(dev)
+    t_lay = time.time()
+    coop._bfs_csr(g)
+    torch.cuda.synchronize(dev)
+    layout_s = time.time() - t_lay
     out = torch.empty(V, dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -301,7 +308,10 @@ def run_ours(args, ws, rank, local):
                        "wgs": info["max_coresident"], "threads_per_wg": args.threads,
                        "l2": "flushed (256 MB write) before every step; CSR 2.2 GB > L2",
                        "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
-                       "graph_gen_s": round(gen_s, 2)},
+                       "graph_gen_s": round(gen_s, 2),
+                       "layout": ("hub-first neighbour order + probe records" if coop.USE_HUB_FIRST else
+                                  "generator order + probe records" if coop.USE_PROBE else "generator order"),
+                       "layout_s": round(layout_s, 3)},
             "kernel_ms_per_step": sum(ktimes) / len(ktimes),
             "levels": stats[-1].levels, "bottom_up_levels": stats[-1].bottom_up_levels,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

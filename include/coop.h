@@ -182,6 +182,13 @@ const char *coop_last_error(void);   /* thread-local description of the last fai
  * graph like building the CSR; results of coop_bfs are identical with or without it. */
 coop_status coop_csr_probe(const coop_csr *g, uint64_t *probe_out, void *stream);
 
+/* Hub-first neighbour order for BFS (graph-layout step, once per graph): writes g's neighbour
+ * lists to col_out (device int32[E], caller-owned) with each list sorted by descending neighbour
+ * degree, so bottom-up levels probe hubs first.  BFS results are identical for any neighbour order
+ * (levels are unique); use col_out as col_idx (and build the probe records from it).  Not for SSSP
+ * (weights are not permuted).  COOP_ERR_INVALID_ARG if E >= 2^31 (the segmented sort's limit). */
+coop_status coop_csr_hub_first(const coop_csr *g, int32_t *col_out, void *stream);
+
 /* Co-residency capacity of the BFS/SSSP kernel for threads_per_wg on `device`. */
 coop_status coop_device_query(int device, uint32_t threads_per_wg, coop_device_info *out);
 

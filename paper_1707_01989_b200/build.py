@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcoop.so")
-SOURCES = [os.path.join(CSRC, "coop_api.cu"), os.path.join(CSRC, "coop_dev_api.cu")]
+SOURCES = [os.path.join(CSRC, f) for f in ("coop_api.cu", "coop_dev_api.cu", "coop_layout.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("coop_rt.cuh", "apps.cuh", "coop_internal.h")] + \
     [os.path.join(ROOT, "include", f) for f in ("coop.h", "coop_device.cuh")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -129,12 +129,15 @@ class WsResult(ctypes.Structure):
 _P = ctypes.c_void_p
 # bottom-up BFS probe records (coop_csr.probe), built once per graph; COOP_PROBE=0 disables (A/B)
 USE_PROBE = os.environ.get("COOP_PROBE", "1") != "0"
+# BFS graphs get a hub-first copy of their neighbour lists (coop_csr_hub_first); COOP_HUB_FIRST=0 disables
+USE_HUB_FIRST = os.environ.get("COOP_HUB_FIRST", "1") != "0"
 SIGNATURES = {
     "coop_abi_version": (ctypes.c_int, []),
     "coop_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "coop_last_error": (ctypes.c_char_p, []),
     "coop_device_query": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint32, ctypes.POINTER(DeviceInfo)]),
     "coop_csr_probe": (ctypes.c_int, [ctypes.POINTER(CooperativeCSR), _P, _P]),
+    "coop_csr_hub_first": (ctypes.c_int, [ctypes.POINTER(CooperativeCSR), _P, _P]),
     "coop_bfs": (ctypes.c_int, [ctypes.POINTER(CooperativeCSR), ctypes.c_int64, _P, ctypes.POINTER(Opts),
                                 ctypes.POINTER(Stats)]),
     "coop_sssp": (ctypes.c_int, [ctypes.POINTER(CooperativeCSR), ctypes.c_int64, _P, ctypes.POINTER(Opts),
@@ -230,7 +233,35 @@ class RunStats:
     task_events: list = field(default_factory=list)
 
 
-def _device_csr(g, need_weights: bool):
+def _bfs_csr(g):
+    """The BFS layout of a graph: hub-first neighbour lists (coop_csr_hub_first) and the probe
+    records built from them -- graph-layout steps done once per graph and cached on it."""
+    import torch
+    cache = getattr(g, "_coop_bfs_cache", None)
+    if cache is not None:
+        return cache
+    c0, keep0 = _device_csr(g, need_weights=False, probe=not USE_HUB_FIRST)
+    if not USE_HUB_FIRST or g.num_edges == 0 or g.num_edges >= (1 << 31) - 1:
+        res = (c0, keep0)
+    else:
+        col2 = torch.empty_like(keep0[1])
+        _check(load().coop_csr_hub_first(ctypes.byref(c0), col2.data_ptr(), None))
+        c = CooperativeCSR(c0.num_vertices, c0.num_edges, c0.row_offsets, c0.offset_bits, col2.data_ptr(), None,
+                           0, None)
+        probe = None
+        if USE_PROBE:
+            probe = torch.empty(g.num_vertices, dtype=torch.int64, device=col2.device)
+            _check(load().coop_csr_probe(ctypes.byref(c), probe.data_ptr(), None))
+            c.probe = probe.data_ptr()
+        res = (c, (keep0[0], col2, None, probe))
+    try:
+        g._coop_bfs_cache = res
+    except AttributeError:
+        pass
+    return res
+
+
+def _device_csr(g, need_weights: bool, probe: bool = True):
     """graphgen.CSR on a CUDA device -> (CooperativeCSR, keepalive tensors)."""
     import torch
     if not g.col_idx.is_cuda:
@@ -255,14 +286,14 @@ def _device_csr(g, need_weights: bool):
     c = CooperativeCSR(g.num_vertices, E, ro.data_ptr(), bits, col.data_ptr() if E else None,
                        w.data_ptr() if (w is not None and E) else None,
                        int(getattr(g, "max_weight", 0) or 0), None)
-    probe = None
-    if USE_PROBE and g.num_vertices > 0:
+    probe_t = None
+    if probe and USE_PROBE and g.num_vertices > 0:
         # graph layout step (once per graph, like the CSR conversion above): per-vertex
         # {degree | first neighbour} records for the bottom-up BFS levels
-        probe = torch.empty(g.num_vertices, dtype=torch.int64, device=col.device)
-        _check(load().coop_csr_probe(ctypes.byref(c), probe.data_ptr(), None))
-        c.probe = probe.data_ptr()
-    keep = (ro, col, w, probe)
+        probe_t = torch.empty(g.num_vertices, dtype=torch.int64, device=col.device)
+        _check(load().coop_csr_probe(ctypes.byref(c), probe_t.data_ptr(), None))
+        c.probe = probe_t.data_ptr()
+    keep = (ro, col, w, probe_t)
     try:
         g._coop_cache = (c, keep, w)   # converted arrays are reused by later calls
     except AttributeError:
@@ -338,7 +369,7 @@ def bfs(g, source: int, levels_out=None, *, trace_cap=0, level_cap=0, event_cap=
     """Cooperative BFS on the current CUDA device.  Returns (levels int32 tensor, RunStats)."""
     import torch
     lib = load()
-    c, keep = _device_csr(g, need_weights=False)
+    c, keep = _bfs_csr(g)
     if levels_out is None:
         levels_out = torch.empty(g.num_vertices, dtype=torch.int32, device=g.col_idx.device)
     o, k2 = make_opts(**opts)
