@@ -30,10 +30,10 @@
 #define COOP_BU_COMPACT 1     // bottom-up: compacted candidates over 32-word items (else lane per vertex)
 #endif
 #ifndef COOP_BU_K
-#define COOP_BU_K 4           // bottom-up (compacted): candidates per lane per round
+#define COOP_BU_K 3           // bottom-up (compacted): candidates per lane per round (hub-first layout sweep: profiles/r01c_bu_hubfirst_variants.log)
 #endif
 #ifndef COOP_BU_SOLO
-#define COOP_BU_SOLO 12       // bottom-up (compacted): per-lane steps before the warp takes a list over (sweep: profiles/r01b_bu_probe_variants.log)
+#define COOP_BU_SOLO 8        // bottom-up (compacted): per-lane steps before the warp takes a list over (same sweep)
 #endif
 #ifndef COOP_BU_CHUNK
 #define COOP_BU_CHUNK 16u     // bottom-up items per mid-interval claim (scheduler policy only)
