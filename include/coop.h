@@ -87,6 +87,9 @@ typedef struct {
                                    (first neighbour 0xFFFFFFFF if degree 0) built once per graph by
                                    coop_csr_probe; bottom-up BFS levels then decide degree-0 vertices and
                                    first-neighbour hits with one coalesced load.  NULL = not used. */
+    const uint32_t *isolated;   /* optional device bitmap, ceil(V/32) words: bit v set iff degree(v) == 0
+                                   (coop_csr_isolated); direction-optimising BFS copies it into the
+                                   visited bitmap at init instead of reading the row offsets.  NULL = not used. */
 } coop_csr;
 
 typedef struct {
@@ -181,6 +184,9 @@ const char *coop_last_error(void);   /* thread-local description of the last fai
  * (cudaStream_t, NULL = legacy default) and wait for them.  A graph-layout step, done once per
  * graph like building the CSR; results of coop_bfs are identical with or without it. */
 coop_status coop_csr_probe(const coop_csr *g, uint64_t *probe_out, void *stream);
+
+/* Degree-zero bitmap of g (bits_out: device uint32[ceil(V/32)], caller-owned), once per graph. */
+coop_status coop_csr_isolated(const coop_csr *g, uint32_t *bits_out, void *stream);
 
 /* Hub-first neighbour order for BFS (graph-layout step, once per graph): writes g's neighbour
  * lists to col_out (device int32[E], caller-owned) with each list sorted by descending neighbour

@@ -36,7 +36,7 @@ class CooperativeCSR(ctypes.Structure):
     _fields_ = [("num_vertices", ctypes.c_int64), ("num_edges", ctypes.c_int64),
                 ("row_offsets", ctypes.c_void_p), ("offset_bits", ctypes.c_int32),
                 ("col_idx", ctypes.c_void_p), ("weights", ctypes.c_void_p),
-                ("max_weight", ctypes.c_uint32), ("probe", ctypes.c_void_p)]
+                ("max_weight", ctypes.c_uint32), ("probe", ctypes.c_void_p), ("isolated", ctypes.c_void_p)]
 
 
 class Opts(ctypes.Structure):
@@ -138,6 +138,7 @@ SIGNATURES = {
     "coop_device_query": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint32, ctypes.POINTER(DeviceInfo)]),
     "coop_csr_probe": (ctypes.c_int, [ctypes.POINTER(CooperativeCSR), _P, _P]),
     "coop_csr_hub_first": (ctypes.c_int, [ctypes.POINTER(CooperativeCSR), _P, _P]),
+    "coop_csr_isolated": (ctypes.c_int, [ctypes.POINTER(CooperativeCSR), _P, _P]),
     "coop_bfs": (ctypes.c_int, [ctypes.POINTER(CooperativeCSR), ctypes.c_int64, _P, ctypes.POINTER(Opts),
                                 ctypes.POINTER(Stats)]),
     "coop_sssp": (ctypes.c_int, [ctypes.POINTER(CooperativeCSR), ctypes.c_int64, _P, ctypes.POINTER(Opts),
@@ -247,13 +248,16 @@ def _bfs_csr(g):
         col2 = torch.empty_like(keep0[1])
         _check(load().coop_csr_hub_first(ctypes.byref(c0), col2.data_ptr(), None))
         c = CooperativeCSR(c0.num_vertices, c0.num_edges, c0.row_offsets, c0.offset_bits, col2.data_ptr(), None,
-                           0, None)
+                           0, None, None)
         probe = None
         if USE_PROBE:
             probe = torch.empty(g.num_vertices, dtype=torch.int64, device=col2.device)
             _check(load().coop_csr_probe(ctypes.byref(c), probe.data_ptr(), None))
             c.probe = probe.data_ptr()
-        res = (c, (keep0[0], col2, None, probe))
+        iso = torch.empty((g.num_vertices + 31) // 32, dtype=torch.int32, device=col2.device)
+        _check(load().coop_csr_isolated(ctypes.byref(c), iso.data_ptr(), None))
+        c.isolated = iso.data_ptr()
+        res = (c, (keep0[0], col2, None, probe, iso))
     try:
         g._coop_bfs_cache = res
     except AttributeError:
@@ -285,7 +289,7 @@ def _device_csr(g, need_weights: bool, probe: bool = True):
         w = g.weights.to(torch.int32).contiguous()
     c = CooperativeCSR(g.num_vertices, E, ro.data_ptr(), bits, col.data_ptr() if E else None,
                        w.data_ptr() if (w is not None and E) else None,
-                       int(getattr(g, "max_weight", 0) or 0), None)
+                       int(getattr(g, "max_weight", 0) or 0), None, None)
     probe_t = None
     if probe and USE_PROBE and g.num_vertices > 0:
         # graph layout step (once per graph, like the CSR conversion above): per-vertex

@@ -90,7 +90,15 @@ struct BfsApp {
         for (uint64_t i = h + 4 * nvec + tid; i < (uint64_t)V; i += nth) lv[i] = (int64_t)i == s ? 0 : -1;
         const uint64_t nw = ((uint64_t)V + 31) / 32;
         const uint32_t sw = (uint32_t)(s >> 5), sb = 1u << (s & 31);
-        if (p.dopt && COOP_INIT_DEAD && sizeof(OffT) == 4 && ((uintptr_t)p.ro & 15) == 0) {
+        const bool dead_from_iso = p.dopt && COOP_INIT_DEAD && p.iso != nullptr;
+        if (dead_from_iso) {
+            // the graph's degree-zero bitmap (a layout step done once per graph): 2 MB copied
+            // instead of the 67 MB of row offsets read below
+            for (uint64_t i = tid; i < nw; i += nth) {
+                const uint32_t m = __ldg(p.iso + i) & ~(i == sw ? sb : 0u);
+                p.visited[i] = m | (i == sw ? sb : 0u);
+            }
+        } else if (p.dopt && COOP_INIT_DEAD && sizeof(OffT) == 4 && ((uintptr_t)p.ro & 15) == 0) {
             // symmetric CSR: a degree-0 vertex is never a neighbour, so it starts
             // closed and the bottom-up levels do not enumerate it (about half of
             // an R-MAT graph's vertices).  Thread per word: the 33 offsets of its
@@ -121,7 +129,7 @@ struct BfsApp {
             }
         }
         for (uint64_t i = tid; i < nw; i += nth) {
-            if (!(p.dopt && COOP_INIT_DEAD && sizeof(OffT) == 4 && ((uintptr_t)p.ro & 15) == 0))
+            if (!dead_from_iso && !(p.dopt && COOP_INIT_DEAD && sizeof(OffT) == 4 && ((uintptr_t)p.ro & 15) == 0))
                 p.visited[i] = i == sw ? sb : 0u;
             if (p.dopt) {
                 p.fbits[0][i] = i == sw ? sb : 0u;

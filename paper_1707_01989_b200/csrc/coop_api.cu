@@ -115,6 +115,20 @@ __global__ void probe_kernel(const OffT *ro, const int32_t *col, int64_t V, unsi
     }
 }
 
+// degree-zero bitmap (coop_csr_isolated): warp per 32-vertex word, one coalesced offsets load
+template <typename OffT>
+__global__ void isolated_kernel(const OffT *ro, int64_t V, uint32_t *bits) {
+    const uint32_t lane = threadIdx.x & 31;
+    const int64_t nw = (V + 31) / 32;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; w < nw;
+         w += (int64_t)gridDim.x * blockDim.x / 32) {
+        const int64_t v = w * 32 + lane;
+        const bool iso = v < V && ro[v + 1] == ro[v];
+        const uint32_t m = __ballot_sync(0xffffffffu, iso);
+        if (lane == 0) bits[w] = m;
+    }
+}
+
 __global__ void l2_rtt_kernel(unsigned long long *word, uint64_t iters, unsigned long long *out_ns) {
     unsigned long long v = 0;
     const uint64_t t0 = globaltimer();
@@ -219,6 +233,24 @@ extern "C" coop_status coop_csr_probe(const coop_csr *g, uint64_t *probe_out, vo
     else
         probe_kernel<<<sms * 8, 256, 0, s>>>(static_cast<const unsigned long long *>(g->row_offsets), g->col_idx,
                                              g->num_vertices, out);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return COOP_OK;
+}
+
+extern "C" coop_status coop_csr_isolated(const coop_csr *g, uint32_t *bits_out, void *stream) {
+    if (!g || !bits_out || !g->row_offsets) return fail(COOP_ERR_INVALID_ARG, "NULL graph / output");
+    if (g->num_vertices < 1 || g->num_vertices > (int64_t)INT32_MAX) return fail(COOP_ERR_INVALID_ARG, "bad V");
+    if (g->offset_bits != 32 && g->offset_bits != 64) return fail(COOP_ERR_INVALID_ARG, "offset_bits must be 32 or 64");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int dev = 0, sms = 148;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (g->offset_bits == 32)
+        isolated_kernel<<<sms * 8, 256, 0, s>>>(static_cast<const uint32_t *>(g->row_offsets), g->num_vertices, bits_out);
+    else
+        isolated_kernel<<<sms * 8, 256, 0, s>>>(static_cast<const unsigned long long *>(g->row_offsets),
+                                                g->num_vertices, bits_out);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaStreamSynchronize(s));
     return COOP_OK;
@@ -422,6 +454,7 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
         kp.col = g->col_idx;
         kp.w = g->weights;
         kp.probe = reinterpret_cast<const unsigned long long *>(g->probe);
+        kp.iso = g->isolated;
         kp.source = r.source;
         kp.E = g->num_edges;
         if (r.app == APP_BFS) kp.level_out = static_cast<int32_t *>(r.out);

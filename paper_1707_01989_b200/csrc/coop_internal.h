@@ -161,6 +161,7 @@ struct KParams {
     const int32_t *col;
     const uint32_t *w;
     const unsigned long long *probe;   // optional per-vertex {degree:32 | first neighbour:32} (coop_csr.probe)
+    const uint32_t *iso;               // optional degree-zero bitmap (coop_csr.isolated)
     int64_t source;
     // outputs
     int32_t *level_out;

@@ -33,7 +33,7 @@ def test_header_declares_the_north_star_entry_points():
     for n in ["coop_dev_create", "coop_dev_arm", "coop_dev_demand", "coop_dev_grant", "coop_dev_collect",
               "coop_dev_destroy", "coop_fig4_bfs", "coop_work_steal"]:
         assert n in names
-    assert len(names) == 36
+    assert len(names) == 37
 
 
 def test_library_exports_every_declared_symbol(lib_path):
