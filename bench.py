@@ -197,7 +197,8 @@ def run_ours(args, ws, rank, local):
     deg = g.degrees()
     srcs = gg.sample_sources(g, 64, seed=2)
     # graph layout for BFS (once per graph, untimed like the graph generation): hub-first
-    # neighbour order + probe records, built by libcoop kernels (coop_csr_hub_first / _probe)
+    # neighbour order, probe records, degree-zero bitmap -- built by libcoop kernels
+    # (coop_csr_hub_first / coop_csr_probe / coop_csr_isolated)
     torch.cuda.synchronize(dev)
     t_lay = time.time()
     coop._bfs_csr(g)
@@ -309,7 +310,8 @@ def run_ours(args, ws, rank, local):
                        "l2": "flushed (256 MB write) before every step; CSR 2.2 GB > L2",
                        "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
                        "graph_gen_s": round(gen_s, 2),
-                       "layout": ("hub-first neighbour order + probe records" if coop.USE_HUB_FIRST else
+                       "layout": ("hub-first neighbour order + probe records + degree-zero bitmap"
+                                  if coop.USE_HUB_FIRST else
                                   "generator order + probe records" if coop.USE_PROBE else "generator order"),
                        "layout_s": round(layout_s, 3)},
             "kernel_ms_per_step": sum(ktimes) / len(ktimes),
