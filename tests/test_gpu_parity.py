@@ -360,3 +360,37 @@ def test_mid_interval_offer_kill_keeps_results_exact(coop):
     d, st = coop.sssp(_dev(gw), 0, sssp_delta=500, threads_per_wg=256, policy=coop.POLICY_SCHEDULER, task_wgs=N // 2,
                       task_blocks=N, task_block_ns=2_000, task_period_ns=10_000, flags=coop.FLAG_CHECK)
     np.testing.assert_array_equal(_u32(d), tb.dijkstra(gw, 0))
+
+
+# ---------------------------------------------------------------- graph layout steps
+def test_layout_kernels_match_numpy(coop):
+    """coop_csr_probe / coop_csr_isolated / coop_csr_hub_first against their plain
+    definitions on the host: probe = {degree | first neighbour}, isolated = degree-0
+    bits, hub-first = each list a permutation of the original, by descending neighbour
+    degree."""
+    import ctypes
+    lib = coop.load()
+    for g in (gg.rmat(12, seed=5), gg.disjoint_union(gg.rmat(10, seed=3), gg.star(40)), gg.grid(9, 7)):
+        gd = _dev(g)
+        c, keep = coop._device_csr(gd, need_weights=False, probe=False)
+        V, E = g.num_vertices, g.num_edges
+        ro = g.row_offsets.numpy().astype(np.int64)
+        col = g.col_idx.numpy().astype(np.int64)
+        deg = np.diff(ro)
+        probe = torch.empty(V, dtype=torch.int64, device="cuda")
+        assert lib.coop_csr_probe(ctypes.byref(c), probe.data_ptr(), None) == 0
+        p = probe.cpu().numpy().view(np.uint64)
+        np.testing.assert_array_equal((p >> np.uint64(32)).astype(np.int64), deg)
+        first = np.where(deg > 0, col[np.minimum(ro[:-1], max(E - 1, 0))], 0xFFFFFFFF)
+        np.testing.assert_array_equal((p & np.uint64(0xFFFFFFFF)).astype(np.int64), first)
+        iso = torch.empty((V + 31) // 32, dtype=torch.int32, device="cuda")
+        assert lib.coop_csr_isolated(ctypes.byref(c), iso.data_ptr(), None) == 0
+        bits = np.unpackbits(iso.cpu().numpy().view(np.uint8), bitorder="little")[:V]
+        np.testing.assert_array_equal(bits.astype(bool), deg == 0)
+        col2 = torch.empty(E, dtype=torch.int32, device="cuda")
+        assert lib.coop_csr_hub_first(ctypes.byref(c), col2.data_ptr(), None) == 0
+        h = col2.cpu().numpy().astype(np.int64)
+        for v in range(V):
+            a, b = ro[v], ro[v + 1]
+            assert sorted(h[a:b]) == sorted(col[a:b])               # same neighbour set
+            assert np.all(np.diff(deg[h[a:b]]) <= 0)                # descending neighbour degree
