@@ -120,11 +120,12 @@ if what == "srcs":   # mean DIROPT kernel time on RMAT-24 over 8 sources (L2 flu
     out = torch.empty(g.num_vertices, dtype=torch.int32, device="cuda")
     l2 = torch.empty(1 << 26, dtype=torch.int32, device="cuda")
     ks = []
+    thr = int(os.environ.get("THREADS", "512"))
     for s in gg.sample_sources(g, 8, seed=2):
         best = None
         for rep in range(3):
             l2.fill_(rep)
-            _, st = coop.bfs(g, s, out, threads_per_wg=512, flags=coop.FLAG_DIROPT)
+            _, st = coop.bfs(g, s, out, threads_per_wg=thr, flags=coop.FLAG_DIROPT)
             best = st.kernel_ns if best is None else min(best, st.kernel_ns)
         ks.append(best / 1e3)
     print(json.dumps({"lib": os.environ.get("COOP_LIB", "default"), "mean_kernel_us": round(sum(ks) / len(ks), 1),
