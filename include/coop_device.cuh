@@ -290,8 +290,12 @@ __device__ __noinline__ uint32_t claim_pool(coop_ctx *c, uint32_t k, bool wait, 
 }
 
 /* Serial section of episode g (warp 0 of the CTA completing it; all M active
- * CTAs wait).  Returns M' (broadcast to the warp). */
-__device__ __noinline__ uint32_t serial_section(coop_ctx *c, uint32_t g, uint32_t M) {
+ * CTAs wait).  Returns M' (broadcast to the warp).  `behalf`: the caller is a
+ * CTA that just left by offer_kill and completes the episode for the waiters;
+ * it is not in the pool yet, so at most N-M-1 CTAs can be forked (a waiting
+ * fork of N-M would never finish: oracle/barrier_model.py bug
+ * "no_cap_on_behalf"). */
+__device__ __noinline__ uint32_t serial_section(coop_ctx *c, uint32_t g, uint32_t M, bool behalf = false) {
     coop_dev *d = c->d;
     const uint32_t lane = threadIdx.x & 31u;
     const bool resizing = d->tx0_kind != 0u;
@@ -333,6 +337,7 @@ __device__ __noinline__ uint32_t serial_section(coop_ctx *c, uint32_t g, uint32_
             }
         }
         Mp = max(1u, min(Mp, d->N));
+        if (behalf && wait) Mp = min(Mp, d->N - 1u);
         fork_want = Mp > M ? Mp - M : 0u;
     }
     fork_want = __shfl_sync(0xffffffffu, fork_want, 0);
@@ -522,7 +527,7 @@ __device__ __noinline__ bool coop_offer_kill(coop_ctx *c) {
     }
     cta_sync_after_t0();
     if (c->state == COOP_ST_KILLED && c->last) {
-        if (threadIdx.x < 32) (void)serial_section(c, c->gen, c->bar_M);
+        if (threadIdx.x < 32) (void)serial_section(c, c->gen, c->bar_M, /*behalf=*/true);
         coop_detail::cta_sync_after_t0();
     }
     return c->state != COOP_ST_ACTIVE;

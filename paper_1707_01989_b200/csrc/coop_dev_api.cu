@@ -55,6 +55,7 @@ struct coop_dev_handle {
     uint32_t *trace_d = nullptr;
     uint32_t *posted_h = nullptr;       // pinned {demand_posted, grant_posted}
     cudaStream_t side = nullptr;        // resource messages while a kernel runs
+    cudaEvent_t armed = nullptr;        // recorded after arm's control-block copy
     std::mutex mu;
     uint32_t n_wgs = 0;
     int device = 0;
@@ -91,6 +92,7 @@ extern "C" coop_status coop_dev_create(const coop_dev_opts *opts, coop_dev_handl
     if ((e = cudaHostAlloc((void **)&h->posted_h, 64, cudaHostAllocDefault)) != cudaSuccess) return bail(e, "cudaHostAlloc");
     memset(h->posted_h, 0, 64);
     if ((e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking)) != cudaSuccess) return bail(e, "cudaStreamCreate");
+    if ((e = cudaEventCreateWithFlags(&h->armed, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "cudaEventCreate");
     *handle = h;
     return COOP_OK;
 }
@@ -101,6 +103,7 @@ extern "C" void coop_dev_destroy(coop_dev_handle *h) {
     cudaGetDevice(&cur);
     cudaSetDevice(h->device);
     if (h->side) cudaStreamSynchronize(h->side), cudaStreamDestroy(h->side);
+    if (h->armed) cudaEventDestroy(h->armed);
     cudaFree(h->d);
     cudaFree(h->mb);
     cudaFree(h->script_d);
@@ -148,6 +151,9 @@ extern "C" coop_status coop_dev_arm(coop_dev_handle *h, uint32_t n_wgs, void *st
     // pageable source: cudaMemcpyAsync stages it before returning, so `hd` may go out of scope
     DCUDA(cudaMemcpyAsync(h->d, &hd, sizeof hd, cudaMemcpyHostToDevice, s));
     DCUDA(cudaMemsetAsync(h->mb, 0, sizeof(coop_dev_mailbox) * n_wgs, s));
+    // a resource message posted after arm returns must land after this copy, or the
+    // copy's older posted counts would overwrite it (post() waits on this event)
+    DCUDA(cudaEventRecord(h->armed, s));
     h->n_wgs = n_wgs;
     *dev_out = h->d;
     return COOP_OK;
@@ -163,7 +169,8 @@ static coop_status post(coop_dev_handle *h, int which, uint32_t n) {
     // one monotone 32-bit store into the running kernel's control block (copy engine,
     // non-blocking stream: it does not wait for the persistent kernel)
     uint32_t *dst = which == 0 ? &h->d->demand_posted : &h->d->grant_posted;
-    cudaError_t e = cudaMemcpyAsync(dst, &h->posted_h[which], 4, cudaMemcpyHostToDevice, h->side);
+    cudaError_t e = cudaStreamWaitEvent(h->side, h->armed, 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dst, &h->posted_h[which], 4, cudaMemcpyHostToDevice, h->side);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->side);
     if (cur != h->device) cudaSetDevice(cur);
     if (e != cudaSuccess) {

@@ -873,8 +873,16 @@ __device__ __noinline__ void park_loop(const KParams &p, CtaState &cs, App &app)
                 if (ld_relaxed32(&c->task_next) < ld_relaxed32(&c->task_total)) {
                     uint32_t old = atomicAnd(&c->pool[wi], ~bit);     // leave the forkable set
                     if (old & bit) {
-                        uint32_t b = atomicAdd(&c->task_next, 1u);
-                        if (b < c->task_total) { cs.block = b; action = ACT_RUN_TASK; break; }
+                        // claim a block by CAS: never advance task_next past task_total (the
+                        // scheduler's 0xFFFFFFFF "finished" mark must not wrap to 0 and
+                        // re-open the finished instance's blocks)
+                        uint32_t b = ld_relaxed32(&c->task_next), got = 0;
+                        while (b < ld_relaxed32(&c->task_total)) {
+                            const uint32_t prev = atomicCAS(&c->task_next, b, b + 1u);
+                            if (prev == b) { got = 1; break; }
+                            b = prev;
+                        }
+                        if (got) { cs.block = b; action = ACT_RUN_TASK; break; }
                         atomicOr(&c->pool[wi], bit);
                     }
                 }
