@@ -172,6 +172,59 @@ class RandomScheduler(Scheduler):
         return M if t is None else t
 
 
+class ChannelScheduler(Scheduler):
+    """The scheduler of §4.2 driven by resource messages:
+    ``demand`` workgroups wanted back, ``grant`` workgroups that may join.
+    Kill is accepted while demand is outstanding (one unit per kill); a fork
+    takes min(grant, N-M).  ``query`` returns the outstanding demand capped at
+    M-1.  Messages arrive at nondeterministic times: ``posts`` maps
+    an engine transition count to (demand, grant) added at that point, and with
+    ``rate`` > 0 a seeded RNG adds one unit of demand (or, half as often, grant)
+    before a transition with that probability, up to ``budget`` units."""
+
+    def __init__(self, posts: Optional[dict] = None, seed: int = 0, rate: float = 0.0, budget: int = 0,
+                 demand: int = 0, grant: int = 0):
+        self.posts = dict(posts or {})
+        self.rng = random.Random(seed)
+        self.rate = rate
+        self.budget = budget
+        self.demand = demand
+        self.grant = grant
+        self.reserved = 0            # query barrier: W frozen at the release (reading R17)
+
+    def tick(self, t: int):
+        if t in self.posts:
+            dd, gg = self.posts[t]
+            self.demand += dd
+            self.grant += gg
+        if self.budget and self.rate and self.rng.random() < self.rate:
+            self.budget -= 1
+            if self.rng.random() < 2 / 3:
+                self.demand += 1
+            else:
+                self.grant += 1
+
+    def target(self, episode, M, N):
+        return M
+
+    def accept_kill(self, episode, M, N):
+        if self.reserved:
+            self.reserved -= 1
+            return True
+        if self.demand:
+            self.demand -= 1
+            return True
+        return False
+
+    def fork_count(self, episode, M, N):
+        k = min(self.grant, N - M)
+        self.grant -= k
+        return k
+
+    def query(self, M):
+        return min(self.demand, M - 1)
+
+
 # --------------------------------------------------------------------------
 # Interleaver: which enabled transition fires next
 # --------------------------------------------------------------------------
@@ -203,6 +256,27 @@ class RandomChooser(Chooser):
                 return max(prims, key=lambda i: options[i][1])
             return 0
         return self.rng.randrange(len(options))
+
+
+class OrderedChooser(Chooser):
+    """Deterministic: an enabled workgroup primitive fires at once (highest id
+    first, so the scheduler can take the top workgroup); otherwise the thread
+    step of the lowest (``ascending``) or highest workgroup id; a barrier when
+    nothing else is enabled.  Makes workgroups reach a barrier in id order (the
+    arrival orders of P:931-934)."""
+
+    def __init__(self, ascending: bool = True):
+        self.sign = 1 if ascending else -1
+
+    def choose(self, options):
+        def key(i):
+            kind, pl = options[i]
+            if kind == "barrier":
+                return (2, 0)
+            if kind == "step":
+                return (1, self.sign * pl.wg)
+            return (0, -pl)
+        return min(range(len(options)), key=key)
 
 
 class ReplayChooser(Chooser):
@@ -270,6 +344,8 @@ class EpisodeRecord:
     kills: int = 0
     forks: int = 0
     fork_transmit: list = field(default_factory=list)   # transmit env of each forked WG
+    query_W: int = 0                                    # query barrier: W broadcast at the release
+    mid_kills: int = 0                                  # kills at chunk boundaries after this barrier
     wg0_transmit: Optional[dict] = None                 # thread 0 of WG 0 at its request_fork
 
 
@@ -281,6 +357,7 @@ class SimResult:
     steps: int
     kills: int
     forks: int
+    mid_kills: int = 0           # kills at chunk boundaries inside an interval
 
     @property
     def m_trace(self) -> list[int]:
@@ -292,7 +369,8 @@ class CoopSim:
 
     def __init__(self, V, ro, col, source, *, weights=None, N=4, d=4, M0=None,
                  scheduler: Optional[Scheduler] = None, chooser: Optional[Chooser] = None,
-                 mode: str = "bfs", max_steps: int = 10_000_000):
+                 mode: str = "bfs", max_steps: int = 10_000_000, barrier: str = "desugared",
+                 work: str = "stride", chunk: int = 1, live_num_groups: bool = False):
         if not (0 <= source < V):
             raise ValueError("source out of range")
         if mode not in ("bfs", "sssp"):
@@ -304,6 +382,25 @@ class CoopSim:
         if not (1 <= self.M <= N):
             raise ValueError("need 1 <= M0 <= N (P:513-514)")
         self.mode = mode
+        if barrier not in ("desugared", "naive", "query"):
+            raise ValueError(barrier)
+        if work not in ("stride", "chunk"):
+            raise ValueError(work)
+        if work == "chunk" and d != 1:
+            raise ValueError("the chunk-counter variant is modelled at workgroup granularity (d=1): "
+                             "the GPU claims a chunk CTA-collectively")
+        if (barrier in ("naive", "query") or work == "chunk") and not isinstance(scheduler, ChannelScheduler):
+            raise ValueError("naive/query barriers and mid-interval kills are driven by a ChannelScheduler")
+        self.barrier = barrier
+        self.gbs = 3 if barrier == "desugared" else 2     # global barriers per resizing barrier
+        self.work = work
+        self.chunk = chunk
+        self.counter = [0, 0]                             # chunk counters of n0/n1
+        self.spin_W = 0                                   # query barrier: W broadcast at the release
+        self.M_committed = None                           # query barrier: M - W until the spinners left
+        self.mid_kills = 0
+        self.live_num_groups = live_num_groups
+        self.M_pub = self.M if M0 is None else M0                 # M published at the last release
         self.sched = scheduler or NeverResize()
         self.chooser = chooser or RandomChooser(0)
         self.max_steps = max_steps
@@ -335,7 +432,16 @@ class CoopSim:
         return t
 
     def get_num_groups(self):
-        M = self.M
+        # Reading R21: with the naive / query implementations get_num_groups is the count
+        # published at the last release (M' of the query barrier excludes the W workgroups
+        # committed to leave), not the live M: a fast workgroup's entry kill at the next
+        # naive barrier, or a spinner not yet claimed, would otherwise change the value a
+        # slow workgroup reads in the same interval (P:655-661 requires it constant).
+        # ``live_num_groups`` reads the live M instead, to show that hazard.
+        if self.barrier == "desugared" or self.live_num_groups:
+            M = self.M
+        else:
+            M = self.M_pub
         if self.interval_M is None:
             self.interval_M = M
         elif self.interval_M != M:
@@ -343,7 +449,39 @@ class CoopSim:
         return M
 
     def _resizing_barrier(self, t: Thread, which: int):
-        """Desugared Resizing-Barrier rule (reading R2: master = WG 0)."""
+        """Desugared Resizing-Barrier rule (reading R2: master = WG 0),
+        or the paper's two implementations of it (§4.2):
+
+        naive  -- slaves offer_kill once on entry, then wait; the master waits for
+                  the (possibly shrunk) M, calls request_fork (new WGs join the
+                  waiting slaves), then releases (P:918-929);
+        query  -- the master waits for everybody, calls request_fork, then query
+                  (W), releases broadcasting W; ids >= M-W spin on offer_kill
+                  until the scheduler claims them."""
+        if self.barrier == "naive":
+            if t.wg != 0:
+                yield (OFFER_KILL, which)
+                yield (GB, 0)
+            else:
+                yield (GB, 0)
+                yield (REQUEST_FORK, which)
+            yield (GB, 1)
+            return
+        if self.barrier == "query":
+            yield (GB, 0)
+            if t.wg == 0:
+                yield (REQUEST_FORK, which)
+                if t.lid == 0:
+                    W = self.sched.query(self.M)
+                    self.sched.demand -= W             # frozen for this episode (reading R17)
+                    self.sched.reserved += W
+                    self.spin_W = W
+                    self.M_committed = self.M - W if W else None
+                    self.episodes[-1].query_W = W
+                yield "step"
+            yield (GB, 1)
+            yield from self._query_spin(t, which)
+            return
         if t.wg == 0:
             yield (GB, 0)
             yield (REQUEST_FORK, which)
@@ -394,6 +532,48 @@ class CoopSim:
                             out["size"] += 1
                     yield "step"
 
+    def _query_spin(self, t: Thread, which):
+        # spin until claimed.  A non-top spinner's offers are Kill-No-Ops that
+        # change nothing (stuttering), so it stays blocked until it is the top id.
+        while t.wg != 0 and self.M_committed is not None and t.wg >= self.M_committed:
+            yield (OFFER_KILL, which, "spin")
+
+    def _chunk_loop(self, t: Thread):
+        """Chunk-counter distribution of one interval (d=1): the workgroup claims
+        ``chunk`` items at a time from the in-queue's atomic counter, so work is
+        never tied to (id, M) and a workgroup may offer_kill between chunks
+         without stranding items -- the remedy for wide graphs whose
+        resizing barriers are rare.  Query style: a
+        workgroup with id >= M - demand stops after its chunk and offers until
+        claimed; only the top id can go; once some workgroup waits at the barrier
+        the rest resume claiming and leave the demand to the barrier."""
+        s = self.sigma
+        env = t.env
+        while True:
+            c = self.counter[env["in_sel"]]             # atomicAdd(counter, chunk)
+            self.counter[env["in_sel"]] = c + self.chunk
+            sched = self.sched
+            stop = t.wg != 0 and sched.demand > 0 and t.wg + sched.demand >= self.M
+            yield "step"
+            size = s.nodes[env["in_sel"]]["size"]
+            for i in range(c, min(c + self.chunk, size)):
+                node = s.nodes[env["in_sel"]]["items"][i]
+                yield "step"
+                yield from self._process_node(t, node)
+            while stop:
+                sched = self.sched
+                if sched.demand == 0 or t.wg + sched.demand < self.M:
+                    break
+                if t.wg == self.M - 1:
+                    yield (OFFER_KILL, "mid")              # accepted: this generator is dropped
+                    break
+                if any(th.blocked is not None and th.blocked[0] == GB
+                       for th in self._active()):
+                    break                                 # someone arrived: resume claiming
+                yield "step"                              # spin
+            if c >= size:
+                return False
+
     def _fig4(self, t: Thread, resume):
         s = self.sigma
         env = t.env
@@ -406,13 +586,18 @@ class CoopSim:
             state = "head"
         else:
             # forked inside resizing barrier `resume`: continuation after request_fork
-            # is "global_barrier(); global_barrier(); ss"
+            # is "global_barrier(); global_barrier(); ss"; in the naive/query
+            # implementations new WGs join the waiting slaves
             yield (GB, 1)
-            yield (GB, 2)
+            if self.barrier == "desugared":
+                yield (GB, 2)
+            elif self.barrier == "query":
+                yield from self._query_spin(t, resume)   # new WGs are slaves too
             state = "after_rb1" if resume == 1 else "head"
         while True:
             if state == "after_rb1":
                 s.nodes[env["out_sel"]]["size"] = 0        # reset(out_nodes)  (reading R9: idempotent)
+                self.counter[env["in_sel"]] = 0            # chunk counter of the next in-queue (idem)
                 yield "step"
                 env["level"] += 1                            # level++
                 yield "step"
@@ -425,6 +610,15 @@ class CoopSim:
             yield "step"
             if size == 0:
                 return
+            if self.work == "chunk":
+                killed = yield from self._chunk_loop(t)
+                if killed:
+                    return
+                env["in_sel"], env["out_sel"] = env["out_sel"], env["in_sel"]
+                yield "step"
+                yield from self._resizing_barrier(t, 1)
+                state = "after_rb1"
+                continue
             # re-chunk: tid = get_global_id(); stride = get_global_size()
             M = self.get_num_groups()
             tid = t.wg * self.d + t.lid
@@ -481,7 +675,8 @@ class CoopSim:
             if len(toks) == 1:
                 tok = next(iter(toks))
                 if tok is not None and tok[0] == OFFER_KILL:
-                    opts.append(("kill", i))
+                    if len(tok) < 3 or i == self.M - 1:
+                        opts.append(("kill", i))
                 elif tok is not None and tok[0] == REQUEST_FORK:
                     opts.append(("fork", i))
         # global barrier: every thread of every active WG at a GB
@@ -491,7 +686,7 @@ class CoopSim:
         return opts
 
     def _episode(self):
-        return self.gb_fired // 3
+        return self.gb_fired // self.gbs
 
     def _apply_barrier(self):
         active = self._active()
@@ -499,33 +694,47 @@ class CoopSim:
         if len(toks) != 1:
             raise SemanticsViolation(f"barrier divergence: {toks} (S:83)")
         idx = next(iter(toks))[1]
-        if idx != self.gb_fired % 3:
+        if idx != self.gb_fired % self.gbs:
             raise SemanticsViolation("barrier instance mismatch (reading R3)")
         passed = {t.gb_passed for t in active}
         # forked threads join at GB index 1; they did not pass GB 0 of this episode
         e = self._episode()
         if idx == 0:
-            self.episodes.append(EpisodeRecord(e, self.M))
+            self._record(e)
             self.interval_M = None
         for t in active:
             t.blocked = None
             t.gb_passed += 1
         self.gb_fired += 1
-        if idx == 2:
+        if idx == self.gbs - 1:
             rec = self.episodes[-1]
-            rec.M_after = self.M
+            rec.M_after = self.M if self.M_committed is None else self.M_committed
+            self.M_pub = rec.M_after
             self.interval_M = None
         del passed
+
+    def _record(self, e):
+        if len(self.episodes) <= e:
+            self.episodes.append(EpisodeRecord(e, self.M))
+        return self.episodes[e]
 
     def _apply_kill(self, i):
         e = self._episode()
         M = self.M
         wg = self.slots[i]
+        which = wg[0].blocked[1]
         accept = i == M - 1 and self.sched.accept_kill(e, M, self.N)
         self.M, killed = rule_offer_kill(self.slots, M, i, accept)
         if killed:
             self.kills += 1
-            self.episodes[-1].kills += 1
+            if which == "mid":
+                self.mid_kills += 1
+            elif self.barrier == "naive":                 # on entry, before the episode's barrier
+                self._record(e).kills += 1
+            else:                                         # inside the episode / query spinners after it
+                self.episodes[-1].kills += 1
+            if self.M_committed is not None and self.M == self.M_committed:
+                self.M_committed = None                   # every spinner has left
         else:
             for t in wg:                           # Kill-No-Op: advance past offer_kill
                 t.blocked = None
@@ -565,6 +774,9 @@ class CoopSim:
                 if any(not t.done for t in self._active()):
                     raise Deadlock("no enabled transition (S:289)")
                 break
+            if isinstance(self.sched, ChannelScheduler):
+                self.sched.tick(self.steps + self.gb_fired)
+                opts = self._enabled()
             c = self.chooser.choose(opts)
             kind, payload = opts[c]
             if kind == "step":
@@ -579,14 +791,17 @@ class CoopSim:
         vals = list(self.sigma.val)
         if self.mode == "bfs":
             vals = [-1 if x == INF else x for x in vals]
-        return SimResult(vals, self.frontier_sizes, self.episodes, self.steps, self.kills, self.forks)
+        return SimResult(vals, self.frontier_sizes, self.episodes, self.steps, self.kills, self.forks,
+                         self.mid_kills)
 
 
 def simulate(g, source, *, mode="bfs", N=4, d=4, M0=None, scheduler=None, chooser=None,
-             max_steps=10_000_000) -> SimResult:
+             max_steps=10_000_000, barrier="desugared", work="stride", chunk=1,
+             live_num_groups=False) -> SimResult:
     """Convenience wrapper over a graphgen.CSR."""
     ro = g.row_offsets.cpu().tolist()
     col = g.col_idx.cpu().tolist()
     w = None if g.weights is None else [int(x) & 0xFFFFFFFF for x in g.weights.cpu().tolist()]
     return CoopSim(g.num_vertices, ro, col, source, weights=w, N=N, d=d, M0=M0,
-                   scheduler=scheduler, chooser=chooser, mode=mode, max_steps=max_steps).run()
+                   scheduler=scheduler, chooser=chooser, mode=mode, max_steps=max_steps,
+                   barrier=barrier, work=work, chunk=chunk, live_num_groups=live_num_groups).run()

@@ -183,3 +183,99 @@ def test_enumeration_detects_a_broken_kernel(monkeypatch):
     for seq, r in itertools.islice(en.all_resize_sequences(g, 0, N=2, d=1), 200):
         bad += not np.array_equal(r.values, ref)
     assert bad > 0
+
+
+# ---------------- the paper's two barrier implementations and chunked intervals ----------------
+VARIANTS = [(b, w) for b in ("desugared", "naive", "query") for w in ("stride", "chunk")]
+
+
+@pytest.mark.parametrize("barrier,work", VARIANTS)
+def test_barrier_variants_random_channel_bfs(barrier, work):
+    """Naive and query resizing barriers and the chunk-counter
+    distribution with offer_kill at chunk boundaries: levels equal O1 and the
+    frontier sizes equal O1's per-level counts under random interleavings and resource
+    messages posted at random times."""
+    g = gg.rmat(8, seed=5)
+    for s in gg.sample_sources(g, 2):
+        ref = tb.bfs(g, s)
+        for seed in range(6):
+            d = 1 if work == "chunk" else 2
+            sch = cs.ChannelScheduler(seed=seed, rate=0.03, budget=8)
+            r = cs.simulate(g, s, N=4, d=d, M0=4, scheduler=sch, barrier=barrier, work=work, chunk=2,
+                            chooser=cs.RandomChooser(seed, prims_last=seed % 2 == 0))
+            np.testing.assert_array_equal(r.values, ref)
+            assert r.frontier_sizes == tb.level_sizes(ref)
+
+
+@pytest.mark.parametrize("barrier,work", VARIANTS)
+def test_barrier_variants_random_channel_sssp(barrier, work):
+    g = gg.with_weights(gg.grid(6, 5), seed=2)
+    ref = tb.dijkstra(g, 0)
+    for seed in range(4):
+        d = 1 if work == "chunk" else 2
+        sch = cs.ChannelScheduler(seed=seed, rate=0.03, budget=8)
+        r = cs.simulate(g, 0, mode="sssp", N=4, d=d, M0=3, scheduler=sch, barrier=barrier, work=work,
+                        chunk=3, chooser=cs.RandomChooser(seed))
+        np.testing.assert_array_equal(np.array(r.values, dtype=np.uint64), ref.astype(np.uint64))
+
+
+def test_naive_barrier_gathers_one_workgroup_per_call_in_ascending_arrival():
+    """with the naive barrier, 'depending on order of arrival, it is possible that
+    only one workgroup is killed per barrier call'.  Arrival in ascending id order: the slaves
+    below the top offer while they are not the largest id (Kill-No-Op), so exactly one WG
+    leaves per episode; arrival in descending order lets all of them go at once."""
+    g = gg.path(12)
+    asc = cs.simulate(g, 0, N=4, d=1, M0=4, scheduler=cs.ChannelScheduler(demand=3), barrier="naive",
+                      chooser=cs.OrderedChooser(ascending=True))
+    assert [e.kills for e in asc.episodes[:4]] == [1, 1, 1, 0]
+    assert [e.M_after for e in asc.episodes[:3]] == [3, 2, 1]
+    desc = cs.simulate(g, 0, N=4, d=1, M0=4, scheduler=cs.ChannelScheduler(demand=3), barrier="naive",
+                       chooser=cs.OrderedChooser(ascending=False))
+    assert desc.episodes[0].kills == 3 and desc.episodes[0].M_after == 1
+    for r in (asc, desc):
+        assert r.values == list(range(12)) and r.kills == 3
+
+
+@pytest.mark.parametrize("ascending", [True, False])
+def test_query_barrier_gathers_W_workgroups_in_one_call(ascending):
+    """P:936-947: the master's query returns W = outstanding demand (capped at M-1, reading R5);
+    ids >= M-W spin on offer_kill until claimed, so the whole demand is met at the first
+    barrier whatever the arrival order."""
+    g = gg.path(12)
+    for D, expect in ((3, 3), (5, 3), (2, 2)):
+        r = cs.simulate(g, 0, N=4, d=1, M0=4, scheduler=cs.ChannelScheduler(demand=D), barrier="query",
+                        chooser=cs.OrderedChooser(ascending=ascending))
+        assert r.episodes[0].query_W == expect and r.episodes[0].kills == expect
+        assert r.episodes[0].M_after == 4 - expect
+        assert r.values == list(range(12))
+
+
+def test_chunked_interval_kill_between_chunks():
+    """offer_kill at a chunk boundary takes a workgroup out in the middle of an
+    interval, before any barrier; the chunk counter hands its remaining items to the others."""
+    g = gg.grid(5, 5)
+    r = cs.simulate(g, 0, N=4, d=1, M0=4, scheduler=cs.ChannelScheduler(demand=1), barrier="query",
+                    work="chunk", chunk=1, chooser=cs.RandomChooser(3))
+    assert r.mid_kills == 1 and r.kills == 1
+    rr, cc = np.divmod(np.arange(25), 5)
+    np.testing.assert_array_equal(r.values, rr + cc)
+
+
+def test_naive_barrier_needs_the_published_group_count():
+    """Reading R21: the naive barrier kills on entry, i.e. while slower workgroups may
+    still be in the interval; if get_num_groups returned the live M, a slow workgroup could read a
+    different value than its peers in the same interval (violating P:655-661, and its stride would
+    skip or repeat items).  The simulator finds that interleaving; with the count published at the
+    last release (what the GPU's per-CTA M is) every interleaving is exact (tests above)."""
+    g = gg.rmat(8, seed=5)
+    s = gg.sample_sources(g, 1)[0]
+    hit = False
+    for seed in range(30):
+        try:
+            cs.simulate(g, s, N=4, d=2, M0=4, scheduler=cs.ChannelScheduler(seed=seed, rate=0.05, budget=8),
+                        barrier="naive", chooser=cs.RandomChooser(seed, prims_last=False), live_num_groups=True)
+        except cs.SemanticsViolation as e:
+            assert "get_num_groups changed" in str(e)
+            hit = True
+            break
+    assert hit
