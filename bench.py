@@ -141,6 +141,27 @@ def oracle_gteps(g_host, sources, budget_s, deg):
     return edges / secs / 1e9, n, secs
 
 
+def verify_levels(g_host, results):
+    """Parity at the benchmarked size: every level array the GPU produced
+    for a timed source is compared element by element with the oracle (C textbook
+    BFS) on the same graph; the oracle runs are spread over the host's cores (ctypes
+    releases the GIL).  Returns {"verified": bool, "sources_checked": n, ...}."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import textbook as tb
+    ro = g_host.row_offsets.numpy().astype(np.int64)
+    col = g_host.col_idx.numpy()
+    V = g_host.num_vertices
+    srcs = sorted({s for s, _ in results})
+    t = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+        ref = dict(zip(srcs, ex.map(lambda s: tb.bfs_arrays(V, ro, col, s), srcs)))
+    bad = [int(s) for s, lv in results if not np.array_equal(lv, ref[s])]
+    return {"verified": not bad, "outputs_checked": len(results), "sources_checked": len(srcs),
+            "mismatched_sources": bad[:8], "oracle_s": round(time.perf_counter() - t, 1),
+            "how": "levels of every timed traversal == oracle/textbook.c, element by element"}
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return
@@ -208,6 +229,7 @@ def run_ours(args, ws, rank, local):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     n_steps = args.warmup + args.steps
+    checked = []
 
     def one(i, **kw):
         s = srcs[(i + rank * 7) % len(srcs)]
@@ -221,6 +243,8 @@ def run_ours(args, ws, rank, local):
                          event_cap=kw.pop("event_cap", 0), **kw)
         e1.record(stream)
         torch.cuda.synchronize(dev)
+        if rank == 0 and ws == 1 and not args.no_verify:
+            checked.append((s, out.cpu().numpy()))          # untimed: verified against the oracle below
         return e0.elapsed_time(e1), k0.elapsed_time(k1), st
 
     # ---- main: standalone cooperative BFS (NeverResize)
@@ -265,7 +289,7 @@ def run_ours(args, ws, rank, local):
 
     extras = {}
     if rank == 0 and not args.quick:
-        extras = run_extras(args, g, srcs, out, flush, stream, dev, info, times, flags)
+        extras = run_extras(args, g, srcs, out, flush, stream, dev, info, times, flags, checked)
 
     # ---- end to end through the C ABI with HOST buffers (H2D graph + D2H levels inside)
     e2e = None
@@ -288,6 +312,11 @@ def run_ours(args, ws, rank, local):
                "h2d_bytes_per_step": int(ro_h.numel() * 4 + col_h.numel() * 4),
                "d2h_bytes_per_step": int(V * 4), "steps": len(et)}
         del ro_h, col_h
+    # ---- parity of every timed output (and the multitasked runs) against the oracle
+    verify = None
+    if rank == 0 and ws == 1 and not args.no_verify:
+        verify = verify_levels(g.to("cpu"), checked)
+        checked.clear()
     # ---- CPU oracle baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -321,17 +350,20 @@ def run_ours(args, ws, rank, local):
                          "kernel": "coop_kernel<BfsApp<uint32_t>,%d>" % args.threads,
                          "alg_bytes_per_launch": sum(alg_bytes) / len(alg_bytes)},
             "cpu_baseline": cpu,
+            "parity": verify,
             "e2e": e2e,
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
             **extras,
         }
         print(json.dumps(line), flush=True)
+        if verify is not None and not verify["verified"]:
+            sys.exit(f"bench: GPU levels differ from the oracle for sources {verify['mismatched_sources']}")
     if ws > 1:
         torch.distributed.destroy_process_group()
 
 
-def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags):
+def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags, checked):
     import torch
     import graphgen as gg
     from paper_1707_01989_b200 import coop
@@ -348,17 +380,38 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags):
         return e0.elapsed_time(e1), r
 
     k = min(args.steps, 8)
-    # non-cooperative persistent baseline (plain global barrier), same N and block size
-    t_plain, t_coop = [], []
-    for i in range(k + 1):
-        tp, (_, stp) = timed(lambda: coop.bfs(g, srcs[i], out, threads_per_wg=args.threads,
-                                                barrier_mode=coop.BARRIER_PLAIN, flags=flags))
-        tc, (_, stc) = timed(lambda: coop.bfs(g, srcs[i], out, threads_per_wg=args.threads, flags=flags))
-        if i:
-            t_plain.append(tp)
-            t_coop.append(tc)
-    ex["noncoop_baseline"] = {"ms_coop": statistics.median(t_coop), "ms_noncoop": statistics.median(t_plain),
-                              "slowdown": statistics.median(t_coop) / statistics.median(t_plain)}
+    # T2 analogue: the cooperative kernel with no competing task against the
+    # separately compiled non-cooperative persistent kernel (kCoop = false: plain barrier,
+    # static split, no scheduler/pool/mailbox code), all at the same N worker CTAs.  Two
+    # cooperative arms: the scheduler never resizes (NEVER) and the scheduler armed with no
+    # task (SCHEDULER: scheduler CTA running, chunk claims + demand reads in every interval,
+    # the kernel "still interacts with the scheduler").  Ratios are geometric
+    # means over sources of per-source medians (the paper's aggregation).
+    n_w = N - 1
+    arms = {"noncoop": dict(barrier_mode=coop.BARRIER_PLAIN),
+            "coop_never": dict(),
+            "coop_scheduler_armed": dict(policy=coop.POLICY_SCHEDULER)}
+    per = {a: [] for a in arms}
+    n_src = max(8, k)
+    for i in range(n_src):
+        samples = {a: [] for a in arms}
+        for rep in range(3):
+            for a, kw in arms.items():
+                t, _ = timed(lambda: coop.bfs(g, srcs[i], out, threads_per_wg=args.threads, max_wgs=n_w,
+                                              flags=flags, **kw))
+                samples[a].append(t)
+        for a in arms:
+            per[a].append(statistics.median(samples[a]))
+
+    def geo(xs):
+        import math
+        return math.exp(sum(math.log(x) for x in xs) / len(xs))
+    ex["noncoop_baseline"] = {
+        "workers": n_w, "sources": n_src, "ms_median": {a: statistics.median(v) for a, v in per.items()},
+        "slowdown_never_vs_noncoop": geo([c / b for c, b in zip(per["coop_never"], per["noncoop"])]),
+        "slowdown_armed_vs_noncoop": geo([c / b for c, b in zip(per["coop_scheduler_armed"], per["noncoop"])]),
+        "aggregation": "geomean over sources of per-source medians of 3 interleaved runs"}
+    t_coop = per["coop_never"]
     # multitasked: scheduler CTA posts a task every P with Q = N/4 WGs (scaled light preset)
     mt = {}
     for name, (P_us, E_us) in {"stress": (200, 20)}.items():
@@ -374,6 +427,8 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags):
             if i:
                 tt.append(t)
                 tasks += st.tasks_completed
+                if not args.no_verify:
+                    checked.append((srcs[i], out.cpu().numpy()))   # multitasked levels: same oracle
                 for e in st.task_events:
                     if e["t_first_start"]:
                         lat.append((e["t_first_start"] - e["t_arrive"]) / 1e3)
@@ -535,6 +590,7 @@ def main():
     ap.add_argument("--topdown", action="store_true", help="main line without direction optimisation")
     ap.add_argument("--quick", action="store_true", help="skip the extra objects")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-verify", action="store_true", help="skip the oracle comparison of the outputs")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

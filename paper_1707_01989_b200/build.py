@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcoop.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("coop_api.cu", "coop_dev_api.cu", "coop_layout.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("coop_rt.cuh", "apps.cuh", "coop_internal.h")] + \
+DEPS = SOURCES + sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))) + \
     [os.path.join(ROOT, "include", f) for f in ("coop.h", "coop_device.cuh")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -234,6 +234,19 @@ class RunStats:
     task_events: list = field(default_factory=list)
 
 
+def with_offset_bits(g, bits: int):
+    """A view of graphgen.CSR ``g`` whose row offsets go to the library as ``bits``-bit
+    integers (64 is chosen automatically only when E >= 2^32, e.g. RMAT-27 on one GPU;
+    forcing it on small graphs exercises that path)."""
+    if bits not in (32, 64):
+        raise ValueError("offset_bits must be 32 or 64")
+    h = type(g)(g.num_vertices, g.row_offsets, g.col_idx, g.weights, g.name)
+    if getattr(g, "max_weight", None) is not None:
+        h.max_weight = g.max_weight
+    h.offset_bits = bits
+    return h
+
+
 def _bfs_csr(g):
     """The BFS layout of a graph: hub-first neighbour lists (coop_csr_hub_first) and the probe
     records built from them -- graph-layout steps done once per graph and cached on it."""
@@ -274,7 +287,7 @@ def _device_csr(g, need_weights: bool, probe: bool = True):
     if cache is not None and (cache[2] is not None or not need_weights):
         return cache[0], cache[1]
     E = g.num_edges
-    if E < (1 << 32):
+    if E < (1 << 32) and getattr(g, "offset_bits", None) != 64:
         ro = g.row_offsets.to(torch.int32) if g.row_offsets.dtype != torch.int32 else g.row_offsets
         bits = 32
     else:

@@ -58,8 +58,12 @@ __device__ __forceinline__ T ldcg(const T *p) { return __ldcg(p); }
 //   BU   bottom-up: every unvisited vertex looks for a parent in the frontier
 //        bitmap (direction optimisation; only with COOP_FLAG_DIROPT)
 // Every mode produces the same level values (BFS levels are unique).
-template <typename OffT>
+// kCoop = false compiles the non-cooperative persistent baseline of the same
+// traversal (the paper's T2 comparison): plain generation barrier,
+// static work split, no scheduler, pool, mailboxes or kill/fork code.
+template <typename OffT, bool KCOOP = true>
 struct BfsApp {
+    static constexpr bool kCoop = KCOOP;
     using LE = typename std::conditional<sizeof(OffT) == 4, LightEntry, LightEntry64>::type;
     static constexpr int KB = 4;   // 32-edge windows per warp iteration (32*KB <= kHeavyDeg)
 
@@ -866,8 +870,9 @@ struct BfsApp {
 enum : uint32_t { SSSP_RELAX = 0, SSSP_DRAIN = 1, SSSP_DONE = 2 };
 constexpr uint32_t kNoRound = 0xFFFFFFFFu;   // low word of an SSSP key not pushed to a near worklist
 
-template <typename OffT>
+template <typename OffT, bool KCOOP = true>
 struct SsspApp {
+    static constexpr bool kCoop = KCOOP;
     __device__ void enter(const KParams &, CtaState &) {}
     template <int BLOCK>
     __device__ void between(const KParams &, CtaState &) {}
@@ -1119,6 +1124,7 @@ struct SsspApp {
 // stamp of a peer from the previous interval is visible (message passing
 // across the barrier).  iters resizing barriers in total.
 struct BarrierApp {
+    static constexpr bool kCoop = true;
     __device__ void enter(const KParams &, CtaState &cs) {
         if (threadIdx.x == 0) cs.app_u32[4] = 0;   // no previous interval for a (re)entered CTA
     }

@@ -82,10 +82,19 @@ static void *pick_block(uint32_t threads) {
     }
 }
 
-static void *select_kernel(uint32_t app, int off64, uint32_t threads) {
+// plain (COOP_BARRIER_PLAIN): the separately compiled non-cooperative persistent
+// kernel of the same traversal (kCoop = false: no scheduler, pool, mailboxes,
+// kill/fork or chunk-claim code), the T2 baseline
+static void *select_kernel(uint32_t app, int off64, uint32_t threads, bool plain) {
     if (app == APP_PBFS) return off64 ? pick_block<PartBfsApp<int64_t>>(threads) : pick_block<PartBfsApp<uint32_t>>(threads);
-    if (app == APP_BFS) return off64 ? pick_block<BfsApp<int64_t>>(threads) : pick_block<BfsApp<uint32_t>>(threads);
-    if (app == APP_SSSP) return off64 ? pick_block<SsspApp<int64_t>>(threads) : pick_block<SsspApp<uint32_t>>(threads);
+    if (app == APP_BFS) {
+        if (plain) return off64 ? pick_block<BfsApp<int64_t, false>>(threads) : pick_block<BfsApp<uint32_t, false>>(threads);
+        return off64 ? pick_block<BfsApp<int64_t>>(threads) : pick_block<BfsApp<uint32_t>>(threads);
+    }
+    if (app == APP_SSSP) {
+        if (plain) return off64 ? pick_block<SsspApp<int64_t, false>>(threads) : pick_block<SsspApp<uint32_t, false>>(threads);
+        return off64 ? pick_block<SsspApp<int64_t>>(threads) : pick_block<SsspApp<uint32_t>>(threads);
+    }
     switch (threads) {
         case 128: return kernel_ptr<BarrierApp, 128>();
         case 256: return kernel_ptr<BarrierApp, 256>();
@@ -259,7 +268,7 @@ extern "C" coop_status coop_csr_isolated(const coop_csr *g, uint32_t *bits_out, 
 extern "C" coop_status coop_device_query(int device, uint32_t threads_per_wg, coop_device_info *out) {
     if (!out) return fail(COOP_ERR_INVALID_ARG, "out is NULL");
     if (threads_per_wg == 0) threads_per_wg = 512;
-    void *k = select_kernel(APP_BFS, 0, threads_per_wg);
+    void *k = select_kernel(APP_BFS, 0, threads_per_wg, false);
     if (!k) return fail(COOP_ERR_INVALID_ARG, "threads_per_wg %u not supported (256/512/1024)", threads_per_wg);
     int cur = 0;
     CUDA_TRY(cudaGetDevice(&cur));
@@ -460,7 +469,7 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
         if (r.app == APP_BFS) kp.level_out = static_cast<int32_t *>(r.out);
         else kp.dist_out = static_cast<uint32_t *>(r.out);
     }
-    void *kern = select_kernel(r.app, off64, threads);
+    void *kern = select_kernel(r.app, off64, threads, o.barrier_mode == COOP_BARRIER_PLAIN);
     if (!kern) return fail(COOP_ERR_INVALID_ARG, "threads_per_wg %u not supported", threads);
     int sms = 0, per = 0;
     st = occupancy(kern, threads, &sms, &per);

@@ -285,7 +285,7 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
     const uint32_t ep = g - 1;
     uint32_t Mp = M, take = 0;
     bool sched_fork = false, wait_fork = false;
-    if (lane == 0) {
+    if (App::kCoop && lane == 0) {
         if (resizing && p.barrier_mode != COOP_BARRIER_PLAIN) {
             if (p.policy == COOP_POLICY_SCRIPTED) {
                 uint32_t s = ep < p.script_len ? p.script[ep] : 0u;
@@ -319,7 +319,7 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
     Mp = __shfl_sync(FULL, Mp, 0);
     wait_fork = __shfl_sync(FULL, (uint32_t)wait_fork, 0) != 0;
     uint32_t got = 0;
-    if (Mp > M) {
+    if (App::kCoop && Mp > M) {
         // the transmit-annotated state is uniform over the workgroups at a barrier
         // (PAPER.md:1731-1742), so the serial section's own copy IS WG 0's
         // (checked against WG 0's published copy under COOP_FLAG_CHECK)
@@ -330,6 +330,7 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
         Mp = M + got;
     }
     if (lane == 0) {
+        if constexpr (App::kCoop) {
         const uint64_t now = globaltimer();
         if (sched_fork && got) atomicSub(&c->grant, got);
         if (take > 0) {   // gather bookkeeping of the task instance in flight
@@ -341,15 +342,16 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
                 if (before + take >= e->demanded) e->t_last_surrender = now;
             }
         }
+        }   // kCoop
         app.serial(p, cs, entry, resizing);
         if (resizing) {
             if (ep < p.m_trace_cap) p.m_trace[ep] = Mp;
             c->episode = ep + 1;                       // plain store: statistics only
         }
         // statistics as fire-and-forget reductions (no round trip on the critical path)
-        if (Mp < M) atomicAdd(&c->kills, M - Mp);
-        if (got) atomicAdd(&c->forks, got);
-        if (Mp != M) {
+        if (App::kCoop && Mp < M) atomicAdd(&c->kills, M - Mp);
+        if (App::kCoop && got) atomicAdd(&c->forks, got);
+        if (App::kCoop && Mp != M) {
             atomicMin(&c->min_m, Mp);
             atomicMax(&c->max_m, Mp);
         }
@@ -369,7 +371,7 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
         }
         // M' of generation g+1 for NAIVE mode and forked CTAs (NAIVE kills may lower
         // W.M during g+1); the release store publishes it with everything above
-        st_relaxed32(&c->mhist[(g + 1) & 7], Mp);
+        if (App::kCoop) st_relaxed32(&c->mhist[(g + 1) & 7], Mp);
         // reset the arrival word for generation g+1, then release on the separate
         // release line R (waiters poll R, arrivals hit W: no polling traffic on the
         // line the arrival atomics serialise on)
@@ -407,7 +409,7 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
         }
         uint32_t action = ACT_CONT, last = 0, killed_naive = 0;
         unsigned long long old;
-        if (resizing && p.barrier_mode == COOP_BARRIER_NAIVE && p.policy == COOP_POLICY_SCHEDULER &&
+        if (App::kCoop && resizing && p.barrier_mode == COOP_BARRIER_NAIVE && p.policy == COOP_POLICY_SCHEDULER &&
             cs.lid != 0) {
             // naive barrier: the slave offers kill on entry; only id M-1 can go
             __threadfence();
@@ -479,8 +481,10 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
     // so the divergence-safe barrier takes its fast path.
     if (threadIdx.x < 32) {
         __syncwarp();
-        if (cs.wait_rel) {
-            const uint32_t g = cs.gen;
+        // every lane reads the shared flags before lane 0 rewrites them (racecheck-clean)
+        const uint32_t waiting = cs.wait_rel, g = cs.gen;
+        __syncwarp();
+        if (waiting) {
             uint32_t spins = 0, stop = 0;
             unsigned long long w = 0;
             for (;;) {
@@ -498,8 +502,8 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
                     cs.action = ACT_KILLED;                // W moved on without us => we were killed at g
                 } else {
                     // W.M is M' unless NAIVE kills of generation g+1 already lowered it
-                    const uint32_t Mn = p.barrier_mode == COOP_BARRIER_NAIVE ? mhist_get(p, g + 1) : w_M(w);
-                    if (cs.lid >= Mn) cs.action = ACT_KILLED;
+                    const uint32_t Mn = App::kCoop && p.barrier_mode == COOP_BARRIER_NAIVE ? mhist_get(p, g + 1) : w_M(w);
+                    if (App::kCoop && cs.lid >= Mn) cs.action = ACT_KILLED;
                     else { cs.M = Mn; cs.gen = g + 1; }
                 }
             }
@@ -651,7 +655,7 @@ __device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, 
 template <int BLOCK, class App, class Fn, class Flush>
 __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32_t *counter, uint64_t n_items,
                                 uint32_t per_chunk, Fn &&fn, Flush &&flush) {
-    const bool midkill = p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY;
+    const bool midkill = App::kCoop && p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY;
     const uint32_t lane = threadIdx.x & 31;
     if (!midkill) {
         // no scheduler can ask for workgroups inside this interval: Fig. 4's static
@@ -691,9 +695,11 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
             }
         }
         cta_sync();                                   // chunk done; cs.chunk reusable
-        if (stop) {
-            const uint32_t r = offer_kill_mid(p, cs, app, flush);
-            if (r != ACT_CONT) return r;
+        if constexpr (App::kCoop) {
+            if (stop) {
+                const uint32_t r = offer_kill_mid(p, cs, app, flush);
+                if (r != ACT_CONT) return r;
+            }
         }
         if (ch >= nchunks) return ACT_CONT;
     }
@@ -900,17 +906,19 @@ __device__ __noinline__ void park_loop(const KParams &p, CtaState &cs, App &app)
             continue;
         }
         // forked: join generation cs.gen once W reaches it (the release of the fork episode)
+        // (the result goes to cs.stop, not cs.action: other warps may still be reading
+        // cs.action above -- racecheck)
         if (threadIdx.x == 0) {
             uint32_t spins = 0;
-            cs.action = ACT_CONT;
+            cs.stop = 0;
             while (w_gen(ld_acquire64(&c->R)) != cs.gen) {
-                if (spin_check(p, cs, spins)) { cs.action = ACT_ABORT; break; }
+                if (spin_check(p, cs, spins)) { cs.stop = 1; break; }
             }
             cs.M = mhist_get(p, cs.gen);
             __threadfence();
         }
         cta_sync();
-        if (cs.action == ACT_ABORT) return;
+        if (cs.stop) return;
         uint32_t r = run_body<App, BLOCK>(p, cs, app, cs.entry);
         flush_stats(p, cs);
         if (r == ACT_DONE) {
@@ -946,7 +954,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(KParams p) {
         if (blockIdx.x == 0) p.ctl->t_start = t0;
     }
     cta_sync();
-    if (p.has_sched && blockIdx.x == p.P) { scheduler_loop(p, cs); return; }
+    if constexpr (App::kCoop) {
+        if (p.has_sched && blockIdx.x == p.P) { scheduler_loop(p, cs); return; }
+    }
     if (blockIdx.x < p.M0) {
         uint32_t r = run_body<App, BLOCK>(p, cs, app, ENTRY_START);
         flush_stats(p, cs);
@@ -957,13 +967,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(KParams p) {
             }
         }
         if (r == ACT_ABORT) return;
-        if (p.barrier_mode != COOP_BARRIER_PLAIN && threadIdx.x == 0) {   // killed or finished: join the pool
+        if (App::kCoop && p.barrier_mode != COOP_BARRIER_PLAIN && threadIdx.x == 0) {   // killed or finished: join the pool
             __threadfence();
             atomicOr(&p.ctl->pool[blockIdx.x >> 5], 1u << (blockIdx.x & 31));
         }
         cta_sync();
     }
-    if (p.barrier_mode != COOP_BARRIER_PLAIN) park_loop<App, BLOCK>(p, cs, app);
+    if constexpr (App::kCoop) {
+        if (p.barrier_mode != COOP_BARRIER_PLAIN) park_loop<App, BLOCK>(p, cs, app);
+    }
 #if COOP_TRACE
     if (threadIdx.x == 0 && blockIdx.x == 0)
         for (int i = 0; i < 12; ++i) p.ctl->trace[i + (i >= 6 ? 2 : 0)] = cs.tr[i];

@@ -31,6 +31,7 @@ namespace coop {
 
 template <typename OffT>
 struct PartBfsApp {
+    static constexpr bool kCoop = true;
     static constexpr int KB = 4;
 
     __device__ void enter(const KParams &, CtaState &) {}

@@ -105,12 +105,23 @@ def test_bfs_random_resize_schedules(coop, bpl):
             assert all(1 <= m <= 40 for m in st.m_trace)
 
 
-def test_bfs_plain_noncoop_baseline(coop):
+@pytest.mark.parametrize("flags", [0, "diropt"])
+def test_bfs_plain_noncoop_baseline(coop, flags):
+    """The separately compiled non-cooperative kernel (kCoop=false, selected by BARRIER_PLAIN)."""
     g = gg.rmat(14, seed=4)
-    s = gg.sample_sources(g, 1)[0]
-    lv, st = coop.bfs(_dev(g), s, barrier_mode=coop.BARRIER_PLAIN)
-    np.testing.assert_array_equal(lv.cpu().numpy(), tb.bfs(g, s))
-    assert st.kills == 0 and st.forks == 0
+    fl = coop.FLAG_DIROPT if flags else 0
+    for s in gg.sample_sources(g, 3):
+        for thr in (256, 512, 1024):
+            lv, st = coop.bfs(_dev(g), s, barrier_mode=coop.BARRIER_PLAIN, threads_per_wg=thr, flags=fl)
+            np.testing.assert_array_equal(lv.cpu().numpy(), tb.bfs(g, s))
+            assert st.kills == 0 and st.forks == 0
+
+
+def test_sssp_plain_noncoop_baseline(coop):
+    g = gg.with_weights(gg.grid(40, 31), seed=5)
+    for delta in (0, 3000):
+        d, st = coop.sssp(_dev(g), 7, barrier_mode=coop.BARRIER_PLAIN, sssp_delta=delta)
+        np.testing.assert_array_equal(_u32(d), tb.dijkstra(g, 7))
 
 
 def test_bfs_edge_cases(coop):
