@@ -156,7 +156,7 @@ def verify_levels(g_host, results):
     t = time.perf_counter()
     with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
         ref = dict(zip(srcs, ex.map(lambda s: tb.bfs_arrays(V, ro, col, s), srcs)))
-    bad = [int(s) for s, lv in results if not np.array_equal(lv, ref[s])]
+    bad = [int(s) for s, lv in results if not np.array_equal(lv.cpu().numpy(), ref[s])]
     return {"verified": not bad, "outputs_checked": len(results), "sources_checked": len(srcs),
             "mismatched_sources": bad[:8], "oracle_s": round(time.perf_counter() - t, 1),
             "how": "levels of every timed traversal == oracle/textbook.c, element by element"}
@@ -244,7 +244,7 @@ def run_ours(args, ws, rank, local):
         e1.record(stream)
         torch.cuda.synchronize(dev)
         if rank == 0 and ws == 1 and not args.no_verify:
-            checked.append((s, out.cpu().numpy()))          # untimed: verified against the oracle below
+            checked.append((s, out.clone()))                # untimed (device copy): verified below
         return e0.elapsed_time(e1), k0.elapsed_time(k1), st
 
     # ---- main: standalone cooperative BFS (NeverResize)
@@ -428,7 +428,7 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags, 
                 tt.append(t)
                 tasks += st.tasks_completed
                 if not args.no_verify:
-                    checked.append((srcs[i], out.cpu().numpy()))   # multitasked levels: same oracle
+                    checked.append((srcs[i], out.clone()))          # multitasked levels: same oracle
                 for e in st.task_events:
                     if e["t_first_start"]:
                         lat.append((e["t_first_start"] - e["t_arrive"]) / 1e3)
@@ -445,6 +445,23 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags, 
                     "gather_us_p50": pct(gat, 0.5), "gather_us_p99": pct(gat, 0.99),
                     "tasks_completed": tasks, "gteps": None}
     ex["multitask"] = mt
+    # the paper's presets at Q = N/4 (query barrier), BFS looped over sources inside ONE
+    # launch for >= 10 s per cell; the full preset x Q x barrier grid is
+    # tools/multitask_paper.py (profiles/)
+    if not args.no_paper_multitask:
+        import importlib.util
+        spec = importlib.util.spec_from_file_location("multitask_paper",
+                                                      os.path.join(ROOT, "tools", "multitask_paper.py"))
+        mp = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mp)
+        runner = mp.MultitaskRunner(coop, g, srcs, args.threads,
+                                    verify_host=None if args.no_verify else g.to("cpu"))
+        base = runner.standalone(args.loop_s)
+        cells = [runner.cell(p, runner.N // 4, "query", args.loop_s) for p in mp.PRESETS_MS]
+        ex["multitask_paper"] = {"standalone_loop": base, "workers": runner.N, "cells": cells,
+                                 "parity": runner.verify() if not args.no_verify else None,
+                                 "note": "BFS looped over 64 sources inside one launch, loop_s each; task = "
+                                         "E ms of work on all N workgroups every P ms, Q = N/4 demanded"}
     # barrier ns vs L2 atomic RTT (configs[3] points)
     rtt = coop.l2_atomic_rtt(200000)
     bar = {}
@@ -591,6 +608,8 @@ def main():
     ap.add_argument("--quick", action="store_true", help="skip the extra objects")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-verify", action="store_true", help="skip the oracle comparison of the outputs")
+    ap.add_argument("--no-paper-multitask", action="store_true", help="skip the 10 s paper-preset loops")
+    ap.add_argument("--loop-s", type=float, default=10.0, help="seconds per multitask loop (>= 10: P:1045)")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -303,9 +303,12 @@ def part_rows(part: PartCSR) -> tuple[torch.Tensor, torch.Tensor]:
 
 
 def part_bounds(V: int, P: int) -> list[int]:
-    """Owned-range boundaries, multiples of 32 (whole bitmap words per rank)."""
+    """Owned-range boundaries: uniform slices of sw = ceil(ceil(V/32) / P) bitmap
+    words per rank (rank p owns [32*sw*p, min(V, 32*sw*(p+1)))), so the slice
+    all-gather of the frontier bitmap is one in-place NCCL all-gather."""
     nw = (V + 31) // 32
-    b = [min(V, (p * nw // P) * 32) for p in range(P)]
+    sw = (nw + P - 1) // P
+    b = [min(V, p * sw * 32) for p in range(P)]
     return b + [V]
 
 

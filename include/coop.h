@@ -252,6 +252,19 @@ coop_status coop_debug_trace(uint64_t *out16);
 
 typedef struct coop_handle coop_handle;
 
+/* BFS looped over sources inside ONE persistent launch -- the paper's multitasking
+ * workload runs the cooperative kernel continuously while tasks arrive (P:1045,
+ * P:1135-1255).  Run r traverses from sources[r % n_sources] (device int64 array);
+ * a new run starts while less than loop_ns has elapsed since the kernel started
+ * (each restart is a resizing barrier, so the scheduler can resize there too).
+ * levels_out (device int32[V]) holds the LAST run's levels; *runs_out = runs done;
+ * run_end_ns (host, optional, run_cap entries) = end of each run, ns after the
+ * kernel start.  stats->reached/edges_scanned sum over all runs; the per-level
+ * statistics are the last run's.  Default watchdog: loop_ns + 20 s. */
+coop_status coop_bfs_loop(const coop_csr *g, const int64_t *sources, uint32_t n_sources, uint64_t loop_ns,
+                          int32_t *levels_out, uint64_t *run_end_ns, uint32_t run_cap, uint32_t *runs_out,
+                          const coop_opts *opts, coop_stats *stats);
+
 /* ---- 1-D vertex-partitioned BFS across the GPUs of one node (BASELINE.json configs[4]) ----
  * Not in the paper (single iGPU).  One call per rank; every rank runs the
  * cooperative BFS kernel over its partition and the per-level frontier is
@@ -263,7 +276,7 @@ typedef struct coop_handle coop_handle;
 #define COOP_MAX_RANKS 8
 typedef struct {
     int64_t num_vertices;       /* global V */
-    int64_t v_begin, v_end;     /* owned vertices [v_begin, v_end); v_begin % 32 == 0 */
+    int64_t v_begin, v_end;     /* owned vertices [v_begin, v_end); v_begin % 32 == 0 (or == V for an empty rank) */
     int32_t rank, nranks;       /* 1 <= nranks <= COOP_MAX_RANKS */
     uint32_t seq;               /* call sequence number: identical on all ranks, new for every call */
     const void *row_offsets;    /* device, V+1 offsets of the local edges (destination owned), by global source */
@@ -289,6 +302,31 @@ coop_status coop_bfs_part(const coop_part *part, int64_t source, int32_t *levels
  * when each uses its own opts->workspace and stream. */
 coop_status coop_bfs_part_launch(const coop_part *part, int64_t source, int32_t *levels_owned_out,
                                  const coop_opts *opts, coop_handle **handle);
+/* North_star's NCCL data plane: the same persistent
+ * cooperative kernel per rank, with the per-level frontier exchanged by
+ * ncclAllGather over NVLink/NVSwitch on a comm stream instead of in-kernel peer
+ * stores.  Per level L the comm stream runs cuStreamWaitValue32(ready >= L+1)
+ * (released by the kernel's first resizing barrier), an in-place ncclAllGather
+ * of this rank's bitmap slice plus its counts, and cuStreamWriteValue32
+ * (gathered = L+1), which the second resizing barrier waits for; termination is
+ * the gathered global count == 0 on every rank (no extra reduce).
+ *   Layout: slices are uniform -- with sw = ceil(ceil(V/32) / nranks) words,
+ *   rank q owns [32*sw*q, min(V, 32*sw*(q+1))) (graphgen.part_bounds);
+ *   part->frontier[rank][0..1] are THIS rank's two bitmaps of nranks*sw words
+ *   (device, zeroed once); the other frontier / flags entries are unused.
+ *   nccl_comm: an ncclComm_t of nranks ranks (this rank = part->rank), from
+ *   coop_nccl_comm_init or torch's ProcessGroupNCCL; every rank calls with the
+ *   same source.  The default grid leaves 16 CTA slots free for NCCL's kernels.
+ * Blocking; returns COOP_ERR_NCCL if NCCL or the stream memory operations are
+ * unavailable or a collective fails. */
+coop_status coop_bfs_part_nccl(const coop_part *part, int64_t source, int32_t *levels_owned_out,
+                               void *nccl_comm, const coop_opts *opts, coop_stats *stats);
+/* NCCL communicator helpers (the unique id is broadcast by the caller, e.g. over
+ * torch.distributed): 128-byte ncclUniqueId; comm is an ncclComm_t. */
+coop_status coop_nccl_get_unique_id(void *uid128);
+coop_status coop_nccl_comm_init(int32_t nranks, const void *uid128, int32_t rank, void **comm);
+coop_status coop_nccl_comm_destroy(void *comm);
+
 /* Exchange buffers: cudaMalloc'd (so they can be shared by IPC) and zeroed; and
  * CUDA IPC helpers for the peer frontier buffers (64-byte opaque handles). */
 coop_status coop_exchange_alloc(uint64_t bytes, void **dptr);

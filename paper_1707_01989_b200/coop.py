@@ -166,6 +166,14 @@ SIGNATURES = {
                                      ctypes.POINTER(Stats)]),
     "coop_bfs_part_launch": (ctypes.c_int, [ctypes.POINTER(CoopPart), ctypes.c_int64, _P, ctypes.POINTER(Opts),
                                             ctypes.POINTER(_P)]),
+    "coop_bfs_loop": (ctypes.c_int, [ctypes.POINTER(CooperativeCSR), _P, ctypes.c_uint32, ctypes.c_uint64, _P,
+                                     ctypes.POINTER(ctypes.c_uint64), ctypes.c_uint32,
+                                     ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(Opts), ctypes.POINTER(Stats)]),
+    "coop_bfs_part_nccl": (ctypes.c_int, [ctypes.POINTER(CoopPart), ctypes.c_int64, _P, _P, ctypes.POINTER(Opts),
+                                          ctypes.POINTER(Stats)]),
+    "coop_nccl_get_unique_id": (ctypes.c_int, [_P]),
+    "coop_nccl_comm_init": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.c_int32, ctypes.POINTER(_P)]),
+    "coop_nccl_comm_destroy": (ctypes.c_int, [_P]),
     "coop_exchange_alloc": (ctypes.c_int, [ctypes.c_uint64, ctypes.POINTER(_P)]),
     "coop_exchange_free": (ctypes.c_int, [_P]),
     "coop_ipc_get_handle": (ctypes.c_int, [_P, _P]),
@@ -394,6 +402,30 @@ def bfs(g, source: int, levels_out=None, *, trace_cap=0, level_cap=0, event_cap=
     _check(lib.coop_bfs(ctypes.byref(c), int(source), levels_out.data_ptr(), ctypes.byref(o), ctypes.byref(st)))
     del keep, k2
     return levels_out, _to_runstats(st, bufs)
+
+
+def bfs_loop(g, sources, loop_s: float, levels_out=None, *, run_cap=1 << 20, event_cap=0, **opts):
+    """BFS looped over ``sources`` inside one persistent launch for ``loop_s`` seconds
+    (coop_bfs_loop).  Returns (levels of the last run, runs, run end times in s after
+    the kernel start, RunStats)."""
+    import numpy as np
+    import torch
+    lib = load()
+    c, keep = _bfs_csr(g)
+    dev = g.col_idx.device
+    src = torch.as_tensor(list(sources), dtype=torch.int64, device=dev)
+    if levels_out is None:
+        levels_out = torch.empty(g.num_vertices, dtype=torch.int32, device=dev)
+    o, k2 = make_opts(**opts)
+    st, bufs = _stats_struct(0, 0, event_cap)
+    t = np.zeros(run_cap, dtype=np.uint64)
+    runs = ctypes.c_uint32()
+    _check(lib.coop_bfs_loop(ctypes.byref(c), src.data_ptr(), src.numel(), int(loop_s * 1e9), levels_out.data_ptr(),
+                             t.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), run_cap, ctypes.byref(runs),
+                             ctypes.byref(o), ctypes.byref(st)))
+    del keep, k2
+    n = runs.value
+    return levels_out, n, t[: min(n, run_cap)].astype(np.float64) * 1e-9, _to_runstats(st, bufs)
 
 
 def sssp(g, source: int, dist_out=None, *, trace_cap=0, level_cap=0, event_cap=0, **opts):

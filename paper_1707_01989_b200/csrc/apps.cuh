@@ -75,7 +75,7 @@ struct BfsApp {
     __device__ __noinline__ void init(const KParams &p, CtaState &cs) {
         const uint64_t tid = (uint64_t)cs.lid * BLOCK + threadIdx.x;
         const uint64_t nth = (uint64_t)cs.M * BLOCK;
-        const int64_t V = p.V, s = p.source;
+        const int64_t V = p.V, s = run_source(p);
         int32_t *lv = p.level_out;
         // level[v] = -1 (unreached, reading R10), level[s] = 0; 16-B vector stores on the aligned body
         const uint64_t head = ((16 - ((uintptr_t)lv & 15)) & 15) / 4;
@@ -141,7 +141,15 @@ struct BfsApp {
                 p.fbits[2][i] = 0u;
             }
         }
-        if (cs.lid == 0 && threadIdx.x == 0) {
+        // the frontier counters: here for the first run; for a restart of the source loop in
+        // the serial section of the restart barrier (slower CTAs may still be reading the
+        // previous run's counters in empty() until they arrive there)
+        if (cs.lid == 0 && threadIdx.x == 0 && ld_relaxed32(&p.ctl->run) == 0) init_ctl(p, s);
+        if (cs.lid == 0 && threadIdx.x == 0) cs.reached += 1;
+    }
+
+    __device__ void init_ctl(const KParams &p, int64_t s) {
+        {
             const OffT *ro = static_cast<const OffT *>(p.ro);
             const OffT b = ro[s], e = ro[s + 1];
             const uint32_t deg = (uint32_t)(e - b);
@@ -159,11 +167,22 @@ struct BfsApp {
             p.ctl->mf[0] = deg;
             p.ctl->vis_edges = deg;
             p.ctl->bmode[0] = BFS_TDQ;
-            cs.reached += 1;
             if (p.level_cap) p.level_sizes[0] = 1;
             p.ctl->frontier_total = 1;
             p.ctl->levels = 1;
         }
+    }
+
+    // BFS looped over sources (coop_bfs_loop): the source of the current run
+    __device__ __forceinline__ static int64_t run_source(const KParams &p) {
+        return p.n_src ? __ldg(p.sources + (ld_relaxed32(&p.ctl->run) % p.n_src)) : p.source;
+    }
+    // after an empty frontier: does another run start? (uniform: read after the release)
+    __device__ bool next_run(const KParams &p, CtaState &cs) {
+        if (!p.n_src) return false;
+        if (threadIdx.x == 0) cs.app_u32[7] = ld_relaxed32(&p.ctl->run) & 0x80000000u ? 0u : 1u;
+        cta_sync();
+        return cs.app_u32[7] != 0;
     }
 
     __device__ bool empty(const KParams &p, CtaState &cs) {
@@ -825,6 +844,7 @@ struct BfsApp {
     // direction of the next level (Beamer: TD->BU if m_f > m_u/alpha, BU->TD if
     // n_f < V/beta)
     __device__ __noinline__ void serial(const KParams &p, CtaState &cs, uint32_t entry, bool resizing) {
+        if (resizing && entry == ENTRY_RESTART) { init_ctl(p, run_source(p)); return; }
         if (!resizing || entry != ENTRY_AFTER_RB1) return;
         Ctl *c = p.ctl;
         const uint32_t in = cs.in_sel, out = in ^ 1u;        // post-swap selectors
@@ -848,12 +868,29 @@ struct BfsApp {
             if (mode == BFS_BU) c->n_bu_levels = nbu + 1;
         }
         c->bmode[in] = mode;
-        if (cs.level < p.level_cap) p.level_t[cs.level] = globaltimer();   // level L's expand done
+        const unsigned long long now = globaltimer();
+        if (cs.level < p.level_cap) p.level_t[cs.level] = now;   // level L's expand done
         if (nf) {
             const uint32_t L = cs.level + 1;
             if (L < p.level_cap) p.level_sizes[L] = (uint32_t)nf;
             c->frontier_total = ftot + nf;
             c->levels = nlev + 1;
+        } else if (p.n_src) {
+            // end of a run of the source loop: stamp it, and either stop (bit 31) or
+            // reset the per-traversal counters for the next run (its init follows)
+            const uint32_t r = c->run;
+            if (r < p.run_cap) p.run_t[r] = now;
+            const bool more = now - c->t_start < p.loop_ns;
+            c->run = more ? r + 1 : ((r + 1) | 0x80000000u);
+            if (more) {
+                c->qsize[0] = c->qsize[1] = 0;
+                c->heavy[0] = c->heavy[1] = 0;
+                c->chunk[0] = c->chunk[1] = 0;
+                c->nf[0] = c->nf[1] = 0;
+                c->mf[0] = c->mf[1] = 0;
+                c->bmode[0] = c->bmode[1] = BFS_TDQ;
+                c->n_bu_levels = 0;
+            }
         }
     }
 };
@@ -873,6 +910,7 @@ constexpr uint32_t kNoRound = 0xFFFFFFFFu;   // low word of an SSSP key not push
 template <typename OffT, bool KCOOP = true>
 struct SsspApp {
     static constexpr bool kCoop = KCOOP;
+    __device__ bool next_run(const KParams &, CtaState &) { return false; }
     __device__ void enter(const KParams &, CtaState &) {}
     template <int BLOCK>
     __device__ void between(const KParams &, CtaState &) {}
@@ -1125,6 +1163,7 @@ struct SsspApp {
 // across the barrier).  iters resizing barriers in total.
 struct BarrierApp {
     static constexpr bool kCoop = true;
+    __device__ bool next_run(const KParams &, CtaState &) { return false; }
     __device__ void enter(const KParams &, CtaState &cs) {
         if (threadIdx.x == 0) cs.app_u32[4] = 0;   // no previous interval for a (re)entered CTA
     }

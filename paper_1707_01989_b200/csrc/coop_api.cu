@@ -5,7 +5,11 @@
 // cooperative-attribute launch (co-residency is guaranteed or the launch
 // fails; grid.sync is never used) -> read back the control block -> map the
 // device error word to a coop_status.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+#include <sched.h>
 
 #include <algorithm>
 #include <atomic>
@@ -173,11 +177,17 @@ struct Scratch {
     DevBuf ctl, lt, mb, visited, qlev, ql0, ql1, qh0, qh1, stamp, mtrace, lsizes, events, script, wmax, fb0, fb1, fb2,
         far0, far1;
     DevBuf h_ro, h_col, h_w, h_out;   // end-to-end (host-pointer) calls
+    DevBuf nccl_aux;                  // NCCL data plane: ready, gathered, count send/recv slots
+    DevBuf runt;                      // source loop: end time of every run
+    volatile uint32_t *nccl_host = nullptr;     // mapped host mirror of `ready`
+    cudaStream_t nccl_stream = nullptr;         // the comm stream (waits, all-gathers, writes)
+    cudaEvent_t nccl_ev = nullptr;
     Ctl *host_ctl = nullptr;          // pinned staging
     std::mutex mu;
 };
 
 constexpr uint32_t kWorkspaces = 8;
+constexpr uint32_t kNcclReserve = 16;     // CTA slots left to NCCL kernels (coop_bfs_part_nccl)
 constexpr uint32_t kDefaultAlpha = 14;   // Beamer et al.'s direction-switch thresholds (reading R14)
 constexpr uint32_t kDefaultBeta = 24;
 static Scratch g_scratch[16][kWorkspaces];
@@ -292,6 +302,14 @@ extern "C" coop_status coop_device_query(int device, uint32_t threads_per_wg, co
 }
 
 // ------------------------------------------------------------------ launch core
+// buffers of the NCCL data plane (per workspace; see coop_bfs_part_nccl)
+struct NcclExt {
+    uint32_t *ready, *gathered;
+    unsigned long long *cnt_send, *cnt_recv;
+    volatile uint32_t *host_ready;     // device pointer of the mapped host word
+    uint64_t slice_words;
+};
+
 struct RunReq {
     uint32_t app;
     const coop_csr *g;
@@ -303,6 +321,11 @@ struct RunReq {
     uint64_t iters;             // barrier bench
     HostChannel *host;          // handle API (device pointer of mapped host memory)
     bool async;                 // do not synchronise (handle API)
+    const NcclExt *nx;          // APP_PBFS with the NCCL data plane (coop_bfs_part_nccl)
+    const int64_t *sources;     // APP_BFS source loop (coop_bfs_loop): device array
+    uint32_t n_src;
+    uint64_t loop_ns;
+    uint32_t run_cap;
 };
 
 static coop_status fill_stats(const Ctl &c, const KParams &kp, coop_stats *st, cudaStream_t stream) {
@@ -398,15 +421,16 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
             return fail(COOP_ERR_INVALID_ARG, "num_vertices out of range");
         if (pt->nranks < 1 || pt->nranks > COOP_MAX_RANKS || pt->rank < 0 || pt->rank >= pt->nranks)
             return fail(COOP_ERR_INVALID_ARG, "rank %d / nranks %d invalid", pt->rank, pt->nranks);
-        if (pt->v_begin < 0 || pt->v_end > pt->num_vertices || pt->v_begin > pt->v_end || (pt->v_begin & 31))
+        if (pt->v_begin < 0 || pt->v_end > pt->num_vertices || pt->v_begin > pt->v_end ||
+            ((pt->v_begin & 31) && pt->v_begin != pt->num_vertices))   // an empty trailing rank may start at V
             return fail(COOP_ERR_INVALID_ARG, "owned range [%lld, %lld) invalid (v_begin %% 32 == 0 required)",
                         (long long)pt->v_begin, (long long)pt->v_end);
         if (pt->offset_bits != 32 && pt->offset_bits != 64) return fail(COOP_ERR_INVALID_ARG, "offset_bits");
         if (!pt->row_offsets || (!pt->col_local && pt->num_edges > 0)) return fail(COOP_ERR_INVALID_ARG, "CSR NULL");
         if (pt->num_hubs && (!pt->hub_ids || !pt->hub_prefix || !pt->hub_degree))
             return fail(COOP_ERR_INVALID_ARG, "hub arrays NULL");
-        for (int q = 0; q < pt->nranks; ++q)
-            if (!pt->frontier[q][0] || !pt->frontier[q][1] || !pt->flags[q])
+        for (int q = 0; q < pt->nranks; ++q)   // the NCCL data plane uses only this rank's bitmaps
+            if ((!r.nx || q == pt->rank) && (!pt->frontier[q][0] || !pt->frontier[q][1] || (!r.nx && !pt->flags[q])))
                 return fail(COOP_ERR_INVALID_ARG, "exchange buffers of rank %d NULL", q);
         if (r.source < 0 || r.source >= pt->num_vertices) return fail(COOP_ERR_INVALID_ARG, "source out of range");
         if (!r.out) return fail(COOP_ERR_INVALID_ARG, "output buffer is NULL");
@@ -432,6 +456,15 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
             pp.F[q][0] = pt->frontier[q][0];
             pp.F[q][1] = pt->frontier[q][1];
             pp.flags[q] = reinterpret_cast<unsigned long long *>(pt->flags[q]);
+        }
+        if (r.nx) {
+            pp.nccl = 1;
+            pp.ready = r.nx->ready;
+            pp.gathered = r.nx->gathered;
+            pp.cnt_send = r.nx->cnt_send;
+            pp.cnt_recv = r.nx->cnt_recv;
+            pp.host_ready = r.nx->host_ready;
+            pp.slice_words = r.nx->slice_words;
         }
         if (o.flags & COOP_FLAG_DIROPT) {
             if (!pt->rows_offsets || (!pt->rows_col && pt->v_end > pt->v_begin) || pt->num_edges_global <= 0)
@@ -479,7 +512,10 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
     if (o.barrier_mode > COOP_BARRIER_NAIVE) return fail(COOP_ERR_INVALID_ARG, "bad barrier_mode %u", o.barrier_mode);
     if (o.policy > COOP_POLICY_SCHEDULER) return fail(COOP_ERR_INVALID_ARG, "bad policy %u", o.policy);
     const bool sched = !plain && (o.policy == COOP_POLICY_SCHEDULER);
-    uint32_t P = o.max_wgs ? o.max_wgs : cap - (sched ? 1 : 0);
+    // the NCCL data plane needs free CTA slots for NCCL's own kernels while the
+    // persistent kernel waits for the gather (kNcclReserve slots left free by default)
+    const uint32_t reserve = (r.nx && cap > 2 * kNcclReserve) ? kNcclReserve : 0u;
+    uint32_t P = o.max_wgs ? o.max_wgs : cap - (sched ? 1 : 0) - reserve;
     if (P < 1 || P > kMaxCtas) return fail(COOP_ERR_INVALID_ARG, "max_wgs %u out of range [1, %u]", P, kMaxCtas);
     if (P + (sched ? 1 : 0) > cap)
         return fail(COOP_ERR_NOT_CORESIDENT, "%u workgroups%s exceed the co-resident capacity %u (%d SMs x %d)",
@@ -602,6 +638,15 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
     kp.task_block_ns = o.task_block_ns;
     kp.task_period_ns = sched ? o.task_period_ns : 0;
     kp.task_first_ns = o.task_first_ns;
+    if (r.sources) {
+        CUDA_TRY(s->runt.ensure(8ull * std::max(1u, r.run_cap)));
+        kp.sources = r.sources;
+        kp.n_src = r.n_src;
+        kp.loop_ns = r.loop_ns;
+        kp.run_t = static_cast<unsigned long long *>(s->runt.p);
+        kp.run_cap = r.run_cap;
+        if (!o.timeout_ns) kp.timeout_ns = r.loop_ns + 20000000000ull;
+    }
 
     // ---- control block
     Ctl *h = s->host_ctl;
@@ -690,6 +735,42 @@ extern "C" coop_status coop_sssp(const coop_csr *g, int64_t source, uint32_t *di
                                  coop_stats *stats) {
     RunReq r = {APP_SSSP, g, nullptr, source, dist_out, opts, stats, 0, nullptr, false};
     return run_blocking(r);
+}
+
+// BFS looped over sources inside ONE persistent launch (the paper's multitasking
+// workload: "BFS ... in a loop"): run r traverses from sources[r % n_sources];
+// a new run starts while less than loop_ns has elapsed since the kernel started.
+extern "C" coop_status coop_bfs_loop(const coop_csr *g, const int64_t *sources, uint32_t n_sources,
+                                     uint64_t loop_ns, int32_t *levels_out, uint64_t *run_end_ns,
+                                     uint32_t run_cap, uint32_t *runs_out, const coop_opts *opts,
+                                     coop_stats *stats) {
+    if (!g || !sources || !n_sources || !runs_out) return fail(COOP_ERR_INVALID_ARG, "bad arguments");
+    std::vector<int64_t> hs(n_sources);
+    CUDA_TRY(cudaMemcpy(hs.data(), sources, 8ull * n_sources, cudaMemcpyDeviceToHost));
+    for (int64_t v : hs)
+        if (v < 0 || v >= g->num_vertices) return fail(COOP_ERR_INVALID_ARG, "source %lld out of range", (long long)v);
+    RunReq r = {APP_BFS, g, nullptr, hs[0], levels_out, opts, stats, 0, nullptr, false, nullptr,
+                sources, n_sources, loop_ns, run_cap};
+    Prepared pr;
+    Scratch *s = nullptr;
+    coop_status st = get_scratch(&s, opts ? opts->workspace : 0);
+    if (st != COOP_OK) return st;
+    SCRATCH_LOCK(s);
+    st = prepare(r, &pr);
+    if (st != COOP_OK) return st;
+    st = launch(pr);
+    if (st != COOP_OK) return st;
+    st = finish(pr, stats);
+    const Ctl &c = *pr.s->host_ctl;
+    const uint32_t runs = c.run & 0x7FFFFFFFu;
+    *runs_out = runs;
+    if (run_end_ns && run_cap) {
+        const uint32_t n = std::min(runs, run_cap);
+        std::vector<unsigned long long> t(n);
+        if (n) CUDA_TRY(cudaMemcpy(t.data(), pr.kp.run_t, 8ull * n, cudaMemcpyDeviceToHost));
+        for (uint32_t i = 0; i < n; ++i) run_end_ns[i] = t[i] > c.t_start ? t[i] - c.t_start : 0;
+    }
+    return st;
 }
 
 // ------------------------------------------------------------------ end-to-end (host pointers)
@@ -928,6 +1009,202 @@ extern "C" coop_status coop_ipc_open(const void *handle64, void **dptr) {
 extern "C" coop_status coop_ipc_close(void *dptr) {
     if (!dptr) return fail(COOP_ERR_INVALID_ARG, "NULL argument");
     CUDA_TRY(cudaIpcCloseMemHandle(dptr));
+    return COOP_OK;
+}
+
+// ------------------------------------------------------------------ NCCL data plane
+// north_star's bring-up exchange for the partitioned BFS: the
+// persistent cooperative kernel runs on the caller's stream; a comm stream holds,
+// per level L, cuStreamWaitValue32(ready >= L+1) -> ncclAllGather of the own
+// bitmap slice (in place) + the counts -> cuStreamWriteValue32(gathered = L+1).
+// The kernel publishes `ready` in RB1's serial section and waits for `gathered`
+// in RB2's.  The host enqueues levels ahead of the kernel (kNcclAhead) from a
+// mapped mirror of `ready`; every rank enqueues exactly final + kNcclAhead
+// gathers, so the collectives match across ranks.
+struct NcclSyms {
+    bool ok = false;
+    char why[256] = {0};
+    ncclResult_t (*get_unique_id)(ncclUniqueId *);
+    ncclResult_t (*comm_init_rank)(ncclComm_t *, int, ncclUniqueId, int);
+    ncclResult_t (*comm_destroy)(ncclComm_t);
+    ncclResult_t (*all_gather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*group_start)();
+    ncclResult_t (*group_end)();
+    const char *(*error_string)(ncclResult_t);
+    CUresult (*wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+    CUresult (*write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+};
+
+static NcclSyms &nccl_syms() {
+    static NcclSyms S;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        // the process's NCCL if one is loaded already (torch's), else the system library
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) { snprintf(S.why, sizeof S.why, "libnccl.so.2 not found: %s", dlerror()); return; }
+#define NSYM(f, n)                                                                   \
+    *reinterpret_cast<void **>(&S.f) = dlsym(h, n);                                  \
+    if (!S.f) { snprintf(S.why, sizeof S.why, "NCCL symbol %s missing", n); return; }
+        NSYM(get_unique_id, "ncclGetUniqueId");
+        NSYM(comm_init_rank, "ncclCommInitRank");
+        NSYM(comm_destroy, "ncclCommDestroy");
+        NSYM(all_gather, "ncclAllGather");
+        NSYM(group_start, "ncclGroupStart");
+        NSYM(group_end, "ncclGroupEnd");
+        NSYM(error_string, "ncclGetErrorString");
+#undef NSYM
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", reinterpret_cast<void **>(&S.wait32), cudaEnableDefault, &q) !=
+                cudaSuccess || q != cudaDriverEntryPointSuccess ||
+            cudaGetDriverEntryPoint("cuStreamWriteValue32", reinterpret_cast<void **>(&S.write32), cudaEnableDefault, &q) !=
+                cudaSuccess || q != cudaDriverEntryPointSuccess) {
+            snprintf(S.why, sizeof S.why, "stream memory operations unavailable");
+            return;
+        }
+        S.ok = true;
+    });
+    return S;
+}
+
+#define NCCL_TRY(x)                                                                                  \
+    do {                                                                                             \
+        ncclResult_t r_ = (x);                                                                       \
+        if (r_ != ncclSuccess) return fail(COOP_ERR_NCCL, "%s: %s", #x, N.error_string(r_));          \
+    } while (0)
+#define CU_TRY(x)                                                                                    \
+    do {                                                                                             \
+        CUresult r_ = (x);                                                                           \
+        if (r_ != CUDA_SUCCESS) return fail(COOP_ERR_CUDA, "%s: CUresult %d", #x, (int)r_);          \
+    } while (0)
+
+extern "C" coop_status coop_nccl_get_unique_id(void *uid128) {
+    NcclSyms &N = nccl_syms();
+    if (!N.ok) return fail(COOP_ERR_NCCL, "%s", N.why);
+    if (!uid128) return fail(COOP_ERR_INVALID_ARG, "NULL argument");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    NCCL_TRY(N.get_unique_id(&id));
+    memcpy(uid128, &id, sizeof id);
+    return COOP_OK;
+}
+
+extern "C" coop_status coop_nccl_comm_init(int32_t nranks, const void *uid128, int32_t rank, void **comm) {
+    NcclSyms &N = nccl_syms();
+    if (!N.ok) return fail(COOP_ERR_NCCL, "%s", N.why);
+    if (!uid128 || !comm || nranks < 1 || rank < 0 || rank >= nranks) return fail(COOP_ERR_INVALID_ARG, "bad arguments");
+    ncclUniqueId id;
+    memcpy(&id, uid128, sizeof id);
+    ncclComm_t c = nullptr;
+    NCCL_TRY(N.comm_init_rank(&c, nranks, id, rank));
+    *comm = c;
+    return COOP_OK;
+}
+
+extern "C" coop_status coop_nccl_comm_destroy(void *comm) {
+    NcclSyms &N = nccl_syms();
+    if (!N.ok) return fail(COOP_ERR_NCCL, "%s", N.why);
+    if (!comm) return fail(COOP_ERR_INVALID_ARG, "NULL comm");
+    NCCL_TRY(N.comm_destroy(static_cast<ncclComm_t>(comm)));
+    return COOP_OK;
+}
+
+constexpr uint32_t kNcclAhead = 2;            // levels of gathers enqueued ahead of the kernel
+
+extern "C" coop_status coop_bfs_part_nccl(const coop_part *part, int64_t source, int32_t *levels_owned_out,
+                                          void *nccl_comm, const coop_opts *opts, coop_stats *stats) {
+    NcclSyms &N = nccl_syms();
+    if (!N.ok) return fail(COOP_ERR_NCCL, "%s", N.why);
+    if (!part || !nccl_comm) return fail(COOP_ERR_INVALID_ARG, "part / nccl_comm NULL");
+    if (part->nranks < 1 || part->nranks > COOP_MAX_RANKS || part->rank < 0 || part->rank >= part->nranks)
+        return fail(COOP_ERR_INVALID_ARG, "rank %d / nranks %d invalid", part->rank, part->nranks);
+    const int P = part->nranks, me = part->rank;
+    const uint64_t nw = ((uint64_t)part->num_vertices + 31) / 32;
+    const uint64_t sw = (nw + P - 1) / P;                       // uniform slice: in-place all-gather
+    const int64_t vb = std::min<int64_t>(part->num_vertices, (int64_t)(32 * sw * me));
+    const int64_t ve = std::min<int64_t>(part->num_vertices, (int64_t)(32 * sw * (me + 1)));
+    if (part->v_begin != vb || part->v_end != ve)
+        return fail(COOP_ERR_INVALID_ARG, "NCCL data plane needs uniform slices: rank %d must own [%lld, %lld)", me,
+                    (long long)vb, (long long)ve);
+    if (!part->frontier[me][0] || !part->frontier[me][1])
+        return fail(COOP_ERR_INVALID_ARG, "frontier[rank][0..1] (nranks * slice words each) NULL");
+    Scratch *s = nullptr;
+    coop_status st = get_scratch(&s, opts ? opts->workspace : 0);
+    if (st != COOP_OK) return st;
+    SCRATCH_LOCK(s);
+    cudaStream_t ks = opts ? static_cast<cudaStream_t>(opts->stream) : nullptr;
+    // per-workspace comm stream, mapped host mirror, small device buffer
+    if (!s->nccl_stream) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&s->nccl_stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&s->nccl_ev, cudaEventDisableTiming));
+        CUDA_TRY(cudaHostAlloc((void **)&s->nccl_host, 64, cudaHostAllocMapped));
+    }
+    const size_t aux = 256 + 8 * 4 * 2 + 8 * 4 * 2 * COOP_MAX_RANKS;
+    CUDA_TRY(s->nccl_aux.ensure(aux));
+    char *base = static_cast<char *>(s->nccl_aux.p);
+    NcclExt nx;
+    nx.ready = reinterpret_cast<uint32_t *>(base);
+    nx.gathered = reinterpret_cast<uint32_t *>(base + 128);
+    nx.cnt_send = reinterpret_cast<unsigned long long *>(base + 256);
+    nx.cnt_recv = nx.cnt_send + 8;
+    volatile uint32_t *hdev = nullptr;
+    CUDA_TRY(cudaHostGetDevicePointer((void **)&hdev, (void *)s->nccl_host, 0));
+    nx.host_ready = hdev;
+    nx.slice_words = sw;
+    s->nccl_host[0] = 0;
+    CUDA_TRY(cudaMemsetAsync(base, 0, 256, ks));                  // ready = gathered = 0
+    CUDA_TRY(cudaEventRecord(s->nccl_ev, ks));
+    CUDA_TRY(cudaStreamWaitEvent(s->nccl_stream, s->nccl_ev, 0));  // no wait may see the previous call's values
+    RunReq r = {APP_PBFS, nullptr, part, source, levels_owned_out, opts, stats, 0, nullptr, false, &nx};
+    Prepared pr;
+    st = prepare(r, &pr);
+    if (st != COOP_OK) return st;
+    st = launch(pr);
+    if (st != COOP_OK) return st;
+    CUDA_TRY(cudaEventRecord(s->nccl_ev, ks));                    // kernel done (abort detection)
+    ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
+    cudaStream_t cs = s->nccl_stream;
+    auto enqueue = [&](uint32_t i) -> coop_status {               // gather i: frontier of level i + 1
+        const uint32_t b = (i + 1) & 1;
+        uint32_t *F = part->frontier[me][b];
+        CU_TRY(N.wait32((CUstream)cs, (CUdeviceptr)nx.ready, i + 1, CU_STREAM_WAIT_VALUE_GEQ));
+        NCCL_TRY(N.group_start());
+        NCCL_TRY(N.all_gather(F + sw * me, F, sw, ncclUint32, comm, cs));
+        NCCL_TRY(N.all_gather(nx.cnt_send + 4 * b, nx.cnt_recv + (size_t)4 * P * b, 4, ncclUint64, comm, cs));
+        NCCL_TRY(N.group_end());
+        CU_TRY(N.write32((CUstream)cs, (CUdeviceptr)nx.gathered, i + 1, CU_STREAM_WRITE_VALUE_DEFAULT));
+        return COOP_OK;
+    };
+    uint32_t enq = 0;
+    coop_status est = COOP_OK;
+    for (; enq < kNcclAhead && est == COOP_OK; ++enq) est = enqueue(enq);
+    bool aborted = false;
+    while (est == COOP_OK) {
+        const uint32_t hr = s->nccl_host[0];
+        if (hr & 0x80000000u) {                                     // final: (hr & ~bit) gathers used
+            const uint32_t target = (hr & 0x7FFFFFFFu) + kNcclAhead;
+            while (enq < target && est == COOP_OK) est = enqueue(enq++);
+            break;
+        }
+        while (enq < hr + kNcclAhead && est == COOP_OK) est = enqueue(enq++);
+        if (cudaEventQuery(s->nccl_ev) == cudaSuccess) {           // kernel ended without the final mark
+            if (s->nccl_host[0] & 0x80000000u) continue;
+            aborted = true;
+            break;
+        }
+        sched_yield();
+    }
+    if (aborted || est != COOP_OK) {
+        // release any wait still enqueued so the comm stream drains (the kernel has ended)
+        static const uint32_t big = 0xFFFFFFFFu;
+        cudaMemcpyAsync(nx.ready, &big, 4, cudaMemcpyHostToDevice, ks);
+        cudaStreamSynchronize(ks);
+    }
+    coop_status fst = finish(pr, stats);
+    cudaError_t ce = cudaStreamSynchronize(cs);
+    if (est != COOP_OK) return est;
+    if (fst != COOP_OK) return fst;
+    if (ce != cudaSuccess) return fail(COOP_ERR_CUDA, "comm stream: %s", cudaGetErrorString(ce));
     return COOP_OK;
 }
 

@@ -14,7 +14,9 @@ constexpr uint64_t kMask40 = (1ull << 40) - 1;
 enum : uint32_t { ACT_CONT = 0, ACT_KILLED = 1, ACT_DONE = 2, ACT_ABORT = 3, ACT_RUN_BODY = 4,
                   ACT_RUN_TASK = 5, ACT_EXIT = 6, ACT_IDLE = 7 };
 // body entry points (the paper's "designated point within the kernel")
-enum : uint32_t { ENTRY_START = 0, ENTRY_AFTER_RB1 = 1, ENTRY_AFTER_RB2 = 2 };
+// ENTRY_RESTART: the resizing barrier after a new run's init (BFS source loop); a CTA
+// forked there starts at the loop head like ENTRY_AFTER_RB2
+enum : uint32_t { ENTRY_START = 0, ENTRY_AFTER_RB1 = 1, ENTRY_AFTER_RB2 = 2, ENTRY_RESTART = 3 };
 // error codes written to Ctl::err (host maps to coop_status)
 enum : uint32_t { DERR_NONE = 0, DERR_TIMEOUT = 1, DERR_INVARIANT = 2, DERR_OVERFLOW = 3 };
 enum : uint32_t { APP_BFS = 0, APP_SSSP = 1, APP_BARRIER = 2, APP_PBFS = 3 };
@@ -121,6 +123,9 @@ struct __align__(128) Ctl {
     uint32_t pad_f[24];
     unsigned long long trace[16];      // COOP_TRACE barrier breakdown (CTA 0, clock64 cycles)
     unsigned long long trace_last;
+    // BFS looped over sources inside one launch (coop_bfs_loop)
+    uint32_t run;                      // runs completed
+    uint32_t pad_l[31];
 };
 
 // Partitioned BFS (1-D vertex partition).  Frontier bitmaps and
@@ -139,6 +144,16 @@ struct PartParams {
     const void *rro;                   // direction optimisation: owned rows (v_end - v_begin + 1 offsets)
     const int32_t *rcol;               //   their neighbours (global ids)
     int64_t E_global;                  //   directed edges of the whole graph (Beamer's m_u)
+    // NCCL data plane (coop_bfs_part_nccl, north_star's per-level all-gather): F[rank][b]
+    // is this rank's full bitmap, its own slice is all-gathered in place by ncclAllGather
+    // on a comm stream that waits for `ready` and signals `gathered` (stream memory ops)
+    uint32_t nccl;
+    uint32_t *ready;                   // RB1 of level L: ready = L + 1 (BIG at termination)
+    const uint32_t *gathered;          // written by the comm stream after gather L: L + 1
+    unsigned long long *cnt_send;      // [2][4] {discovered, m_f, source degree, 0} per parity
+    const unsigned long long *cnt_recv;            // [2][nranks][4], all-gathered with the slice
+    volatile uint32_t *host_ready;     // host-mapped mirror of `ready` (the host enqueues ahead)
+    uint64_t slice_words;              // words per rank slice (uniform: v_begin == rank * 32 * slice_words)
 };
 
 // Host -> GPU packet channel (host-mapped pinned memory; the paper's SVM atomics).
@@ -202,6 +217,11 @@ struct KParams {
     uint32_t dopt;              // BFS: direction-optimising (COOP_FLAG_DIROPT)
     PartParams part;            // APP_PBFS
     uint32_t alpha, beta;       // Beamer's switch thresholds (m_f > m_u/alpha -> BU; n_f < V/beta -> TD)
+    // BFS looped over sources inside one launch (coop_bfs_loop): run r uses
+    // sources[r % n_src]; a new run starts while globaltimer - t_start < loop_ns
+    const int64_t *sources; uint32_t n_src;
+    uint64_t loop_ns;
+    unsigned long long *run_t; uint32_t run_cap;   // globaltimer at the end of each run
     // periodic task generator
     uint32_t task_wgs, task_blocks, task_max;
     uint64_t task_block_ns, task_period_ns, task_first_ns;

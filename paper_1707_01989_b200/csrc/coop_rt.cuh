@@ -47,6 +47,17 @@
 #define COOP_ARRIVE_ACQREL 0
 #endif
 
+#ifndef COOP_CLAIM_UNIFIED
+#define COOP_CLAIM_UNIFIED 1  // one inlined copy of the item body in claim_items (static + chunked)
+#endif
+#ifndef COOP_RUNBODY_NOINLINE
+#define COOP_RUNBODY_NOINLINE 1
+#endif
+#if COOP_RUNBODY_NOINLINE
+#define COOP_RUNBODY_ATTR __noinline__
+#else
+#define COOP_RUNBODY_ATTR
+#endif
 #ifndef COOP_WARP_WAIT
 #define COOP_WARP_WAIT 1      // waiters poll the release word with all of warp 0 (converged at the CTA barrier)
 #endif
@@ -652,6 +663,74 @@ __device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, 
 // SCHEDULER policy every claim also reads the resource channel and, when this
 // id is asked to surrender, the CTA offers itself (offer_kill_mid) right after
 // finishing the chunk in hand.  fn(item) is warp-collective.
+#if COOP_CLAIM_UNIFIED
+template <int BLOCK, class App, class Fn, class Flush>
+__device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32_t *counter, uint64_t n_items,
+                                uint32_t per_chunk, Fn &&fn, Flush &&flush) {
+    const bool midkill = App::kCoop && p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY;
+    const uint32_t lane = threadIdx.x & 31;
+    constexpr uint32_t WPB = BLOCK / 32;
+    // One call site of fn for both distributions (the item body is the hot code: a
+    // second inlined copy doubled the kernel's instruction footprint).
+    //  static  (no scheduler can ask for workgroups inside this interval): Fig. 4's
+    //          distribution, item i to warp i mod (M*W), no atomics or syncs;
+    //  chunked (SCHEDULER + query): the CTA claims per_chunk items from `counter`, its
+    //          warps take them one at a time from a shared counter; between chunks
+    //          (CTA-collective) the CTA may offer itself (offer_kill_mid).
+    const uint64_t TW = (uint64_t)cs.M * WPB;
+    uint64_t it = (uint64_t)cs.lid * WPB + (threadIdx.x >> 5);   // static cursor
+    const uint64_t nchunks = midkill ? (n_items + per_chunk - 1) / per_chunk : 0;
+    bool refill = midkill, first = true;
+    uint64_t base = 0;
+    uint32_t cnt = 0, ch = 0, stop = 0;
+    for (;;) {
+        if (refill) {                                   // CTA-collective (every warp gets here)
+            if (!first) {
+                cta_sync();                             // chunk done; cs.item_next reusable
+                if constexpr (App::kCoop) {
+                    if (stop) {                         // the claim saw demand for this id
+                        const uint32_t r = offer_kill_mid(p, cs, app, flush);
+                        if (r != ACT_CONT) return r;
+                    }
+                }
+                if (ch >= nchunks) return ACT_CONT;
+            }
+            first = false;
+            if (threadIdx.x == 0) {
+                const uint32_t c0 = atomicAdd(counter, 1u);
+                uint32_t st = 0;
+                if (cs.lid != 0) {
+                    const uint32_t d = ld_relaxed32(&p.ctl->demand);
+                    if (d) st = cs.lid + d >= w_M(ld_relaxed64(&p.ctl->W));
+                }
+                cs.chunk = c0;
+                cs.stop = st;
+                cs.item_next = 0;
+            }
+            cta_sync();
+            ch = cs.chunk;
+            stop = cs.stop;
+            base = (uint64_t)ch * per_chunk;
+            cnt = ch < nchunks ? (uint32_t)min((uint64_t)per_chunk, n_items - base) : 0u;
+            refill = false;
+        }
+        uint64_t item;
+        if (midkill) {
+            uint32_t k = 0;
+            if (lane == 0) k = atomicAdd(&cs.item_next, 1u);
+            k = __shfl_sync(FULL, k, 0);
+            if (k >= cnt) { refill = true; continue; }
+            item = base + k;
+        } else {
+            if (it >= n_items) return ACT_CONT;
+            item = it;
+            it += TW;
+        }
+        fn(item);
+    }
+}
+
+#else
 template <int BLOCK, class App, class Fn, class Flush>
 __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32_t *counter, uint64_t n_items,
                                 uint32_t per_chunk, Fn &&fn, Flush &&flush) {
@@ -705,11 +784,13 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
     }
 }
 
+#endif
+
 // ---------------------------------------------------------------- body
 // Fig. 4 with the app's process_node; entry points are the
 // program points after each resizing barrier (forked CTAs start there).
 template <class App, int BLOCK>
-__device__ uint32_t run_body(const KParams &p, CtaState &cs, App &app, uint32_t entry) {
+__device__ COOP_RUNBODY_ATTR uint32_t run_body(const KParams &p, CtaState &cs, App &app, uint32_t entry) {
     uint32_t r;
     app.enter(p, cs);
     if (entry == ENTRY_START) {
@@ -721,7 +802,17 @@ __device__ uint32_t run_body(const KParams &p, CtaState &cs, App &app, uint32_t 
     bool skip_to_rb1 = entry == ENTRY_AFTER_RB1;
     for (;;) {
         if (!skip_to_rb1) {
-            if (app.empty(p, cs)) return ACT_DONE;            // while (in_nodes.size > 0)
+            if (app.empty(p, cs)) {                           // while (in_nodes.size > 0)
+                if (!app.next_run(p, cs)) return ACT_DONE;
+                // BFS looped over sources inside the launch: the next run's init by
+                // the active CTAs, then a resizing barrier (forked CTAs join at the loop head)
+                if (threadIdx.x == 0) { cs.level = 0; cs.in_sel = 0; }
+                cta_sync();
+                app.template init<BLOCK>(p, cs);
+                r = barrier(p, cs, app, /*resizing=*/true, ENTRY_RESTART);
+                if (r != ACT_CONT) return r;
+                continue;
+            }
             LTRACE(0);
             r = app.template expand<BLOCK>(p, cs);             // for (i = tid; ...) process_node
             if (r != ACT_CONT) return r;                       // killed at a chunk boundary (offer_kill)

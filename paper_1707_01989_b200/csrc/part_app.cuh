@@ -32,6 +32,7 @@ namespace coop {
 template <typename OffT>
 struct PartBfsApp {
     static constexpr bool kCoop = true;
+    __device__ bool next_run(const KParams &, CtaState &) { return false; }
     static constexpr int KB = 4;
 
     __device__ void enter(const KParams &, CtaState &) {}
@@ -282,6 +283,13 @@ struct PartBfsApp {
         const uint32_t L = cs.level;
         const uint64_t nw = ((uint64_t)p.V + 31) / 32;
         uint32_t *fcur = pp.F[pp.rank][L & 1];
+        if (pp.nccl) {
+            // NCCL data plane: only the own slice of the consumed bitmap is cleared (it
+            // receives level L+2's bits); the all-gather overwrites every other slice
+            const uint64_t w0 = (uint64_t)pp.vb / 32;
+            for (uint64_t i = tid; i < pp.slice_words; i += nth) fcur[w0 + i] = 0u;
+            return;
+        }
         for (uint64_t i = tid; i < nw; i += nth) fcur[i] = 0u;
         const uint32_t nb = (L + 1) & 1;
         const uint32_t *mine = pp.F[pp.rank][nb];
@@ -334,10 +342,69 @@ struct PartBfsApp {
         return true;
     }
 
+    // NCCL data plane, RB1 of level L: publish this rank's counts for the all-gather and
+    // release the comm stream (its cuStreamWaitValue32(ready >= L+1) precedes the gather)
+    __device__ void nccl_publish(const KParams &p, const CtaState &cs) {
+        const PartParams &pp = p.part;
+        Ctl *c = p.ctl;
+        const uint32_t L = cs.level, b = (L + 1) & 1;
+        unsigned long long *snd = pp.cnt_send + 4 * b;
+        snd[0] = c->pcount[b];
+        snd[1] = c->pmf[b];
+        snd[2] = L == 0 ? c->pmf[0] : 0ull;        // source degree (its owner), summed by every rank
+        snd[3] = 0;
+        c->pcount[b] = 0;
+        c->pmf[b] = 0;
+        if (L == 0) c->pmf[0] = 0;
+        __threadfence_system();                      // bitmap slice + counts before the flag
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pp.ready), "r"(L + 1) : "memory");
+        pp.host_ready[0] = L + 1;
+    }
+
+    // NCCL data plane, RB2 of level L (cs.level == L+1 here): wait for gather L, sum the counts
+    __device__ bool nccl_collect(const KParams &p, const CtaState &cs, unsigned long long *tot,
+                                 unsigned long long *mf, unsigned long long *src) {
+        const PartParams &pp = p.part;
+        const uint32_t L1 = cs.level;
+        uint32_t spins = 0, g;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(g) : "l"(pp.gathered) : "memory");
+            if (g >= L1) break;
+            if (spin_check(p, cs, spins)) return false;
+        }
+        const unsigned long long *rcv = pp.cnt_recv + (uint64_t)(L1 & 1) * 4 * pp.nranks;
+        unsigned long long a = 0, m = 0, s = 0;
+        for (int q = 0; q < pp.nranks; ++q) {
+            a += ldcg(rcv + 4 * q);
+            m += ldcg(rcv + 4 * q + 1);
+            s += ldcg(rcv + 4 * q + 2);
+        }
+        *tot = a;
+        *mf = m;
+        *src = s;
+        return true;
+    }
+
     __device__ void serial(const KParams &p, CtaState &cs, uint32_t entry, bool resizing) {
         Ctl *c = p.ctl;
         const uint32_t base = p.part.seq << 16;
         const uint64_t t0 = globaltimer();
+        if (p.part.nccl) {
+            if (!resizing) return;                   // init: the comm stream orders the first gather
+            if (entry == ENTRY_AFTER_RB1) { nccl_publish(p, cs); return; }
+            if (entry != ENTRY_AFTER_RB2) return;
+            const uint32_t L = cs.level;
+            unsigned long long tot = 0, mf = 0, src = 0;
+            if (!nccl_collect(p, cs, &tot, &mf, &src)) return;
+            if (L == 1) c->vis_edges = src;
+            c->xwait_ns += globaltimer() - t0;
+            next_level(p, tot, mf);
+            if (!tot) {                               // every rank ends here: release any gathers enqueued ahead
+                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.part.ready), "r"(0xFFFFFFFFu) : "memory");
+                p.part.host_ready[0] = 0x80000000u | L;   // final: L gathers were used
+            }
+            return;
+        }
         if (!resizing) {   // the init global barrier: every rank cleared its bitmaps before any peer writes
             unsigned long long tot, mf;
             exchange(p, cs, base | 1u, 0, c->pmf[0], &tot, &mf);
@@ -353,6 +420,14 @@ struct PartBfsApp {
         if (!exchange(p, cs, base | (L + 1), mine, mymf, &tot, &mf)) return;
         c->pcount[L & 1] = 0;
         c->pmf[L & 1] = 0;
+        c->xwait_ns += globaltimer() - t0;
+        next_level(p, tot, mf);
+    }
+
+    // global frontier size `tot` and its m_f: termination, next direction, statistics
+    __device__ void next_level(const KParams &p, unsigned long long tot, unsigned long long mf) {
+        Ctl *c = p.ctl;
+        const uint32_t L = c->levels;                // levels counted so far (level index of `tot`)
         c->gcount = tot;
         // direction of the next level from the global n_f, m_f (same on every rank)
         const uint32_t prev = c->pmode;
@@ -366,7 +441,6 @@ struct PartBfsApp {
             if (mode == BFS_BU) c->n_bu_levels += 1;
         }
         c->pmode = mode;
-        c->xwait_ns += globaltimer() - t0;
         if (tot) {
             if (L < p.level_cap) p.level_sizes[L] = (uint32_t)tot;
             c->frontier_total += tot;

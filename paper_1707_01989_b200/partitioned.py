@@ -50,9 +50,20 @@ def exchange_handles(local: bytes, group=None) -> list[bytes]:
 
 
 class PartitionedBFS:
-    """This rank's partition, exchange buffers and peer mapping."""
+    """This rank's partition, exchange buffers and peer mapping.
 
-    def __init__(self, part, device, hub_degree: int = HUB_DEGREE):
+    exchange="nvlink": the frontier slice is stored into every peer's bitmap by the
+    kernel itself (coop_bfs_part; peers wired by connect_ipc / connect_local).
+    exchange="nccl": north_star's data plane -- ncclAllGather of the slice on a comm
+    stream ordered against the persistent kernel by stream memory operations
+    (coop_bfs_part_nccl; communicator from connect_nccl)."""
+
+    def __init__(self, part, device, hub_degree: int = HUB_DEGREE, exchange: str = "nvlink"):
+        if exchange not in ("nvlink", "nccl"):
+            raise ValueError(exchange)
+        self.exchange = exchange
+        self.comm = None
+        self._own_comm = False
         self.part = part
         self.device = torch.device(device)
         self.V = part.num_vertices
@@ -78,7 +89,11 @@ class PartitionedBFS:
         # two frontier bitmaps of ceil(V/32) words (+16 B slack each) and the flag block
         lib = _lib()
         with torch.cuda.device(self.device):
-            self.nwb = (((self.V + 31) // 32) * 4 + 16 + 255) // 256 * 256
+            nw = (self.V + 31) // 32
+            self.slice_words = (nw + part.nranks - 1) // part.nranks
+            # NCCL: nranks uniform slices (in-place all-gather); NVLink: ceil(V/32) words + slack
+            words = self.slice_words * part.nranks if exchange == "nccl" else nw
+            self.nwb = (words * 4 + 16 + 255) // 256 * 256
             f = ctypes.c_void_p()
             coop._check(lib.coop_exchange_alloc(2 * self.nwb, ctypes.byref(f)))
             g = ctypes.c_void_p()
@@ -121,8 +136,32 @@ class PartitionedBFS:
             self.peer_F[q] = [ptrs[0], ptrs[0] + nwb]
             self.peer_flags[q] = ptrs[1]
 
+    def connect_nccl(self, comm_ptr: Optional[int] = None, group=None):
+        """NCCL communicator of the partitioned BFS: torch's (``comm_ptr``, e.g.
+        ProcessGroupNCCL._comm_ptr()) or a new one whose unique id rank 0 broadcasts
+        over torch.distributed (``group``; a single-rank job needs no group)."""
+        lib = _lib()
+        if comm_ptr:
+            self.comm = comm_ptr
+            return
+        uid = ctypes.create_string_buffer(128)
+        if self.part.rank == 0:
+            coop._check(lib.coop_nccl_get_unique_id(uid))
+        if self.part.nranks > 1:
+            import torch.distributed as dist
+            obj = [uid.raw if self.part.rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            uid = ctypes.create_string_buffer(obj[0], 128)
+        c = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            coop._check(lib.coop_nccl_comm_init(self.part.nranks, uid, self.part.rank, ctypes.byref(c)))
+        self.comm, self._own_comm = c.value, True
+
     def close(self):
         lib = _lib()
+        if self.comm and self._own_comm:
+            lib.coop_nccl_comm_destroy(ctypes.c_void_p(self.comm))
+        self.comm = None
         for p in self._opened:
             lib.coop_ipc_close(ctypes.c_void_p(p))
         self._opened = []
@@ -142,9 +181,13 @@ class PartitionedBFS:
         s.hub_ids = self.hub_ids.data_ptr() if s.num_hubs else None
         s.hub_prefix = self.hub_pref.data_ptr() if s.num_hubs else None
         s.hub_degree = self.hub_degree
-        for q in range(self.part.nranks):
-            s.frontier[q][0], s.frontier[q][1] = self.peer_F[q]
-            s.flags[q] = self.peer_flags[q]
+        if self.exchange == "nccl":
+            r = self.part.rank
+            s.frontier[r][0], s.frontier[r][1] = self.F_ptr, self.F_ptr + self.nwb
+        else:
+            for q in range(self.part.nranks):
+                s.frontier[q][0], s.frontier[q][1] = self.peer_F[q]
+                s.flags[q] = self.peer_flags[q]
         s.rows_offsets = self.rro.data_ptr()
         s.rows_col = self.rcol.data_ptr() if self.rcol.numel() else None
         s.num_edges_global = int(self.E_global) if self.E_global else 0
@@ -178,8 +221,15 @@ class PartitionedBFS:
         s = self._struct(self.seq)
         o, k = coop.make_opts(**opts)
         st, bufs = coop._stats_struct(0, level_cap, 0)
-        coop._check(lib.coop_bfs_part(ctypes.byref(s), int(source), self.levels.data_ptr(), ctypes.byref(o),
-                                      ctypes.byref(st)))
+        if self.exchange == "nccl":
+            if not self.comm:
+                raise RuntimeError("connect_nccl() first")
+            with torch.cuda.device(self.device):
+                coop._check(lib.coop_bfs_part_nccl(ctypes.byref(s), int(source), self.levels.data_ptr(),
+                                                   ctypes.c_void_p(self.comm), ctypes.byref(o), ctypes.byref(st)))
+        else:
+            coop._check(lib.coop_bfs_part(ctypes.byref(s), int(source), self.levels.data_ptr(), ctypes.byref(o),
+                                          ctypes.byref(st)))
         return self.levels, coop._to_runstats(st, bufs)
 
 

@@ -33,7 +33,11 @@ def test_header_declares_the_north_star_entry_points():
     for n in ["coop_dev_create", "coop_dev_arm", "coop_dev_demand", "coop_dev_grant", "coop_dev_collect",
               "coop_dev_destroy", "coop_fig4_bfs", "coop_work_steal"]:
         assert n in names
-    assert len(names) == 37
+    for n in ["coop_bfs_part", "coop_bfs_part_nccl", "coop_nccl_get_unique_id", "coop_nccl_comm_init",
+              "coop_nccl_comm_destroy"]:
+        assert n in names
+    assert "coop_bfs_loop" in names
+    assert len(names) == 42
 
 
 def test_library_exports_every_declared_symbol(lib_path):

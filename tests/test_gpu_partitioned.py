@@ -93,3 +93,83 @@ def test_partitioned_direction_optimising(part, P):
     np.testing.assert_array_equal(lv.cpu().numpy(), tb.bfs(g2, 0))
     for pb in parts + p2:
         pb.close()
+
+
+# ---------------- north_star's NCCL data plane (coop_bfs_part_nccl) ----------------
+@pytest.mark.parametrize("diropt", [False, True])
+def test_partitioned_bfs_nccl_single_rank(part, diropt):
+    """The NCCL exchange path end to end on the one GPU of the box (NCCL refuses two ranks
+    on one device): persistent kernel on the compute stream; per level the comm stream waits
+    for `ready` (cuStreamWaitValue32), runs the in-place ncclAllGather of the slice and the
+    counts, and writes `gathered` (cuStreamWriteValue32), which the kernel's second resizing
+    barrier waits for.  Levels exact, also under random resizes (each rank's kernel resizes
+    independently of the exchange)."""
+    from paper_1707_01989_b200 import coop
+    for g in (gg.rmat(14, seed=2), gg.disjoint_union(gg.grid(40, 30), gg.star(3000))):
+        pb = part.PartitionedBFS(gg.partition(g, 1, 0), "cuda", exchange="nccl")
+        pb.E_global = g.num_edges
+        pb.connect_nccl()
+        flags = coop.FLAG_DIROPT if diropt else 0
+        for i, s in enumerate([0] + gg.sample_sources(g, 3)):
+            kw = dict(policy=coop.POLICY_RANDOM, resize_prob=0.5, seed=i) if i % 2 else {}
+            lv, st = pb.run(s, threads_per_wg=512, flags=flags, level_cap=4096, **kw)
+            ref = tb.bfs(g, s)
+            np.testing.assert_array_equal(lv[: g.num_vertices].cpu().numpy(), ref)
+            assert st.level_sizes == tb.level_sizes(ref)
+        pb.close()
+
+
+_TWO_PROC = r"""
+import os, sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, {root!r})
+import graphgen as gg
+from oracle import textbook as tb
+from paper_1707_01989_b200 import coop, partitioned as pt
+rank = int(sys.argv[1])
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=rank, world_size=2)
+torch.cuda.set_device(0)
+g = gg.rmat(12, seed=7)
+pb = pt.PartitionedBFS(gg.partition(g, 2, rank), "cuda")
+pb.E_global = g.num_edges
+pb.connect_ipc()                       # CUDA IPC handles all-gathered over torch.distributed
+ok = True
+for i, s in enumerate(gg.sample_sources(g, 3)):
+    dist.barrier()
+    lv, st = pb.run(s, threads_per_wg=256, max_wgs=8, timeout_ns=120_000_000_000,
+                    flags=coop.FLAG_DIROPT if i % 2 else 0)
+    ref = tb.bfs(g, s)[pb.part.v_begin:pb.part.v_end]
+    ok &= bool(np.array_equal(lv[: pb.part.v_end - pb.part.v_begin].cpu().numpy(), ref))
+dist.barrier()
+pb.close()
+print("RANK", rank, "OK" if ok else "MISMATCH", flush=True)
+"""
+
+
+def test_partitioned_bfs_two_processes_ipc(part, tmp_path):
+    """Two OS processes (one rank each) on the box's single GPU: the exchange buffers are
+    shared by CUDA IPC handles all-gathered over torch.distributed (connect_ipc), and every
+    level's slice stores and .sys-scope release/acquire flags cross the process boundary --
+    the same code path as across NVLink between GPUs.  The two persistent kernels belong to
+    different contexts, so the GPU time-slices them (slow, but each barrier completes)."""
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    script = tmp_path / "two.py"
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script.write_text(_TWO_PROC.format(root=root, port=port))
+    procs = [subprocess.Popen([sys.executable, str(script), str(r)], stdout=subprocess.PIPE,
+                              stderr=subprocess.STDOUT, text=True) for r in range(2)]
+    outs = []
+    for p in procs:
+        try:
+            outs.append(p.communicate(timeout=600)[0])
+        except subprocess.TimeoutExpired:
+            for q in procs:
+                q.kill()
+            pytest.fail("two-process partitioned BFS timed out")
+    for r, o in enumerate(outs):
+        assert f"RANK {r} OK" in o, o[-3000:]

@@ -143,3 +143,26 @@ def test_compute_sanitizer(coop, tool, tmp_path):
         f.write(log)
     assert r.returncode == 0 and "SANITIZE_OK" in log, log[-4000:]
     assert "ERROR SUMMARY: 0 errors" in log or "0 errors" in log, log[-4000:]
+
+
+@pytest.mark.parametrize("mode", ["standalone", "query", "naive"])
+def test_bfs_source_loop_inside_one_launch(coop, mode):
+    """coop_bfs_loop: BFS looped over sources inside one persistent launch, each
+    restart a resizing barrier; under a periodic competing task (query / naive barrier) the
+    scheduler kills and forks across runs.  The last run's levels are exact, every run
+    completed, run end times increase."""
+    g = gg.rmat(16, seed=3)
+    gd = g.to("cuda")
+    srcs = gg.sample_sources(g, 5, seed=4)
+    kw = {}
+    if mode != "standalone":
+        kw = dict(policy=coop.POLICY_SCHEDULER, barrier_mode=coop.BARRIER_QUERY if mode == "query" else
+                  coop.BARRIER_NAIVE, task_wgs=8, task_blocks=32, task_block_ns=20000, task_period_ns=200000,
+                  task_first_ns=0, event_cap=4096)
+    lv, runs, t_end, st = coop.bfs_loop(gd, srcs, 0.3, threads_per_wg=256, max_wgs=48, flags=coop.FLAG_DIROPT,
+                                        **kw)
+    assert runs > len(srcs)
+    np.testing.assert_array_equal(lv.cpu().numpy(), tb.bfs(g, srcs[(runs - 1) % len(srcs)]))
+    assert np.all(np.diff(t_end) > 0) and t_end[-1] >= 0.3
+    if mode != "standalone":
+        assert st.kills > 0 and st.forks > 0 and st.tasks_completed > 0

@@ -18,7 +18,10 @@ def test_part_bounds_are_word_aligned_and_cover():
     for V, P in [(1, 1), (31, 2), (1000, 3), (1 << 16, 8), (100, 8)]:
         b = gg.part_bounds(V, P)
         assert b[0] == 0 and b[-1] == V and len(b) == P + 1
-        assert all(x % 32 == 0 for x in b[:-1])
+        assert all(x % 32 == 0 or x == V for x in b[:-1])      # empty trailing ranks start at V
+        nw = (V + 31) // 32
+        sw = (nw + P - 1) // P                                  # uniform slices (in-place all-gather)
+        assert all(b[q] == min(V, 32 * sw * q) for q in range(P))
         assert all(b[i] <= b[i + 1] for i in range(P))
 
 
