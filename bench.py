@@ -486,9 +486,36 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags, 
             if i:
                 ts.append(t)
         ms = statistics.median(ts)
+        E_R = gw.num_edges                                  # every vertex is reached on the grid
+        V_R = gw.num_vertices
+        lb = 8 * E_R + 20 * V_R                             # each vertex expanded once
+        est = 20 * st.frontier_total + 16 * st.edges_scanned   # entries x (4 id + 8 key + 8 offsets), edges x (4+4+8)
+        peak, _ = _peaks()
         ss[name] = {"ms": ms, "gteps": m_und / (ms * 1e-3) / 1e9, "delta": delta, "threads_per_wg": thr, "wgs": n,
                     "episodes": st.episodes, "relaxed_edges": st.edges_scanned,
-                    "us_per_episode": ms * 1e3 / max(1, st.episodes)}
+                    "us_per_episode": ms * 1e3 / max(1, st.episodes),
+                    "work_efficiency": st.edges_scanned / E_R,
+                    "hbm_frac_lower_bound_bytes": lb / (ms * 1e-3) / 1e9 / peak,
+                    "hbm_frac_executed_bytes": est / (ms * 1e-3) / 1e9 / peak,
+                    "bound": "barrier latency (episodes x us_per_episode), not HBM"}
+        if not args.no_verify:
+            dlast = dout.cpu().numpy().view("uint32").copy()
+            ss[name]["_dist"] = dlast
+    # same-run oracle: Dijkstra (oracle/textbook.c, 1 host core) on the same grid, and parity
+    import numpy as np
+    from oracle import textbook as tb
+    gh = gw.to("cpu")
+    ro = gh.row_offsets.numpy().astype(np.int64)
+    col = gh.col_idx.numpy()
+    wts = gh.weights.numpy().astype(np.uint32)
+    t0 = time.perf_counter()
+    ref = tb.dijkstra_arrays(gh.num_vertices, ro, col, wts, 0)
+    dj = time.perf_counter() - t0
+    for name in ss:
+        d = ss[name].pop("_dist", None)
+        ss[name]["verified"] = None if d is None else bool(np.array_equal(d, ref))
+    ss["dijkstra_oracle"] = {"s": dj, "gteps": m_und / dj / 1e9, "cores": 1,
+                             "kind": "oracle (binary-heap Dijkstra, oracle/textbook.c)"}
     ex["sssp_grid2048"] = ss
     # device API (include/coop_device.cuh): the paper's Fig. 4 kernel written literally on
     # resizing_global_barrier (thread-strided, CAS claims), same RMAT-24 sources, and Fig. 2

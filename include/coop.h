@@ -252,6 +252,12 @@ coop_status coop_debug_trace(uint64_t *out16);
 
 typedef struct coop_handle coop_handle;
 
+/* The competing task as a standalone non-cooperative kernel (K11):
+ * `blocks` CTAs of `threads` threads, each busy for block_ns; asynchronous on
+ * `stream` (cudaStream_t).  Used for the measured kernel-level preemption
+ * comparison (T3), where the task runs between compute launches. */
+coop_status coop_spin_task(uint32_t blocks, uint32_t threads, uint64_t block_ns, void *stream);
+
 /* BFS looped over sources inside ONE persistent launch -- the paper's multitasking
  * workload runs the cooperative kernel continuously while tasks arrive (P:1045,
  * P:1135-1255).  Run r traverses from sources[r % n_sources] (device int64 array);
@@ -409,6 +415,26 @@ coop_status coop_dev_grant(coop_dev_handle *h, uint32_t forks);    /* fork up to
  * timeout -> COOP_ERR_TIMEOUT, invariant -> COOP_ERR_INVARIANT, overflow -> COOP_ERR_OVERFLOW. */
 coop_status coop_dev_collect(coop_dev_handle *h, void *stream, coop_dev_stats *stats);
 void coop_dev_destroy(coop_dev_handle *h);
+
+/* The Pannotia applications of Table 1 as cooperative kernels on the
+ * device API, with Table 1's resizing-barrier counts (color 2/2, mis 3/3, p-sssp
+ * 3/3); vertex-strided loops re-chunked after every resizing barrier; the
+ * iteration counter is the transmitted state.  Algorithms (R23):
+ *   coop_color  Jones-Plassmann colouring with priorities (splitmix64(seed ^ v), v):
+ *               colors_out[v] = iteration in which v became the highest-priority
+ *               uncoloured vertex of its neighbourhood;
+ *   coop_mis    Luby's maximal independent set with the same priorities (lowest
+ *               undecided joins): state_out[v] = 1 in the set, 2 not;
+ *   coop_psssp  Bellman-Ford over all vertices each iteration (pull form):
+ *               dist_out[v] (u32, 0xFFFFFFFF unreachable).
+ * 32-bit offsets, symmetric graph; device output buffers int32/uint32[V];
+ * *iters_out = iterations executed.  Blocking; errors as coop_fig4_bfs. */
+coop_status coop_color(coop_dev_handle *h, const coop_csr *g, uint64_t seed, int32_t *colors_out, uint32_t threads,
+                       uint32_t *iters_out, coop_dev_stats *stats);
+coop_status coop_mis(coop_dev_handle *h, const coop_csr *g, uint64_t seed, int32_t *state_out, uint32_t threads,
+                     uint32_t *iters_out, coop_dev_stats *stats);
+coop_status coop_psssp(coop_dev_handle *h, const coop_csr *g, int64_t source, uint32_t *dist_out, uint32_t threads,
+                       uint32_t *iters_out, coop_dev_stats *stats);
 
 /* Fig. 4 exactly, written on the device API: thread-strided
  * frontier with tid/stride recomputed after every resizing barrier, claims by

@@ -166,6 +166,7 @@ SIGNATURES = {
                                      ctypes.POINTER(Stats)]),
     "coop_bfs_part_launch": (ctypes.c_int, [ctypes.POINTER(CoopPart), ctypes.c_int64, _P, ctypes.POINTER(Opts),
                                             ctypes.POINTER(_P)]),
+    "coop_spin_task": (ctypes.c_int, [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, _P]),
     "coop_bfs_loop": (ctypes.c_int, [ctypes.POINTER(CooperativeCSR), _P, ctypes.c_uint32, ctypes.c_uint64, _P,
                                      ctypes.POINTER(ctypes.c_uint64), ctypes.c_uint32,
                                      ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(Opts), ctypes.POINTER(Stats)]),
@@ -185,6 +186,12 @@ SIGNATURES = {
     "coop_dev_grant": (ctypes.c_int, [_P, ctypes.c_uint32]),
     "coop_dev_collect": (ctypes.c_int, [_P, _P, ctypes.POINTER(DevStats)]),
     "coop_dev_destroy": (None, [_P]),
+    "coop_color": (ctypes.c_int, [_P, ctypes.POINTER(CooperativeCSR), ctypes.c_uint64, _P, ctypes.c_uint32,
+                                  ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(DevStats)]),
+    "coop_mis": (ctypes.c_int, [_P, ctypes.POINTER(CooperativeCSR), ctypes.c_uint64, _P, ctypes.c_uint32,
+                                ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(DevStats)]),
+    "coop_psssp": (ctypes.c_int, [_P, ctypes.POINTER(CooperativeCSR), ctypes.c_int64, _P, ctypes.c_uint32,
+                                  ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(DevStats)]),
     "coop_fig4_bfs": (ctypes.c_int, [_P, ctypes.POINTER(CooperativeCSR), ctypes.c_int64, _P, ctypes.c_uint32,
                                      ctypes.POINTER(DevStats)]),
     "coop_work_steal": (ctypes.c_int, [_P, ctypes.POINTER(WsTree), ctypes.c_uint32, ctypes.POINTER(WsResult),
@@ -626,6 +633,23 @@ def fig4_bfs(h: DevHandle, g, source: int, levels_out=None, *, threads_per_wg=25
                                 ctypes.byref(st)))
     del keep
     return levels_out, DevHandle._to_dict(st, buf)
+
+
+def pannotia(h: DevHandle, app: str, g, arg: int, out=None, *, threads_per_wg=256):
+    """Table 1's color / mis / p-sssp on the device API (coop_color / coop_mis / coop_psssp).
+    ``arg`` is the priority seed (color, mis) or the source (p-sssp).  Returns (output tensor,
+    iterations, stats dict)."""
+    import torch
+    fn = {"color": "coop_color", "mis": "coop_mis", "psssp": "coop_psssp"}[app]
+    csr, keep = _device_csr(g, app == "psssp")
+    if out is None:
+        out = torch.empty(g.num_vertices, dtype=torch.int32, device=g.col_idx.device)
+    st, buf = h._stats()
+    it = ctypes.c_uint32()
+    _check(getattr(load(), fn)(h.h, ctypes.byref(csr), int(arg), out.data_ptr(), threads_per_wg, ctypes.byref(it),
+                               ctypes.byref(st)))
+    del keep
+    return out, it.value, DevHandle._to_dict(st, buf)
 
 
 def work_steal(h: DevHandle, *, seed: int, depth: int, max_fanout: int, fixed=False, rounds=0, queue_cap=0,

@@ -38,6 +38,9 @@
 #ifndef COOP_BU_CHUNK
 #define COOP_BU_CHUNK 16u     // bottom-up items per mid-interval claim (scheduler policy only)
 #endif
+#ifndef COOP_SSSP_MIN_SZ
+#define COOP_SSSP_MIN_SZ 8    // SSSP: smallest worklist group per warp item (32 = fixed groups)
+#endif
 #ifndef COOP_SSSP_PRECHECK
 #define COOP_SSSP_PRECHECK 0  // SSSP: read dist[v] before the atomicMin (fewer atomics, one more dependent round trip: 73.4 vs 68.4 ms on the 2048^2 grid without it)
 #endif
@@ -61,6 +64,12 @@ __device__ __forceinline__ T ldcg(const T *p) { return __ldcg(p); }
 // kCoop = false compiles the non-cooperative persistent baseline of the same
 // traversal (the paper's T2 comparison): plain generation barrier,
 // static work split, no scheduler, pool, mailboxes or kill/fork code.
+// claim counters of a level parity back to 0 (serial section)
+__device__ __forceinline__ void reset_claims(Ctl *c, uint32_t parity) {
+#pragma unroll
+    for (uint32_t r = 0; r < kClaimShards; ++r) c->claim[parity][r][0] = 0;
+}
+
 template <typename OffT, bool KCOOP = true>
 struct BfsApp {
     static constexpr bool kCoop = KCOOP;
@@ -776,7 +785,7 @@ struct BfsApp {
         mfsum = 0;
     }
 
-    template <int BLOCK>
+    template <int BLOCK, bool MID = false>
     __device__ uint32_t expand(const KParams &p, CtaState &cs) {
         constexpr uint32_t WPB = BLOCK / 32;
         const uint32_t warp = threadIdx.x >> 5;
@@ -811,15 +820,15 @@ struct BfsApp {
             const uint32_t W = cs.app_u32[6] <= 1 ? COOP_BU_DENSE_W : 32u;
             // chunk = items claimed per CTA claim; only used when a scheduler can ask for workgroups
             // mid-interval (static split otherwise): it bounds the offer_kill latency
-            r = claim_items<BLOCK>(p, cs, *this, &p.ctl->chunk[in], (nw + W - 1) / W, COOP_BU_CHUNK, [&](uint64_t it) {
+            r = claim_items<BLOCK, MID>(p, cs, *this, &p.ctl->claim[in][0][0], (nw + W - 1) / W, COOP_BU_CHUNK, [&](uint64_t it) {
                 bu_compact<COOP_BU_K>(p, cs, it * W, nw, W, &s_bits[0][wb], &s_bits[1][wb], edges, reached, mfsum);
             }, flush);
         } else if (mode == BFS_BU) {                          // item = BU_KW 32-vertex words
-            r = claim_items<BLOCK>(p, cs, *this, &p.ctl->chunk[in], (nw + BU_KW - 1) / BU_KW, 128u, [&](uint64_t it) {
+            r = claim_items<BLOCK, MID>(p, cs, *this, &p.ctl->claim[in][0][0], (nw + BU_KW - 1) / BU_KW, 128u, [&](uint64_t it) {
                 bu_words<BU_KW>(p, cs, it * BU_KW, nw, edges, reached, mfsum);
             }, flush);
         } else if (mode == BFS_TDB) {                         // item = 32 frontier words
-            r = claim_items<BLOCK>(p, cs, *this, &p.ctl->chunk[in], (nw + 31) / 32, 4u * WPB, [&](uint64_t g) {
+            r = claim_items<BLOCK, MID>(p, cs, *this, &p.ctl->claim[in][0][0], (nw + 31) / 32, 4u * WPB, [&](uint64_t g) {
                 tdb_group(p, cs, g, fnext, edges, reached, mfsum, res);
             }, flush);
         } else {                                              // item = 32 light frontier entries
@@ -831,7 +840,7 @@ struct BfsApp {
             const uint64_t nl = cs.app_u32[0];
             uint32_t sz = 32;
             while (sz > 1 && (nl + sz - 1) / sz < TW) sz >>= 1;
-            r = claim_items<BLOCK>(p, cs, *this, &p.ctl->chunk[in], (nl + sz - 1) / sz, 4u * WPB,
+            r = claim_items<BLOCK, MID>(p, cs, *this, &p.ctl->claim[in][0][0], (nl + sz - 1) / sz, 4u * WPB,
                             [&](uint64_t g) { tdq_group(p, cs, g, sz, fnext, edges, reached, mfsum, res); }, flush);
         }
         LTRACE(6);
@@ -856,7 +865,7 @@ struct BfsApp {
         const uint32_t nlev = c->levels, nbu = c->n_bu_levels;
         c->qsize[out] = 0;
         c->heavy[out] = 0;
-        c->chunk[out] = 0;
+        reset_claims(c, out);
         c->nf[out] = 0;
         c->mf[out] = 0;
         c->vis_edges = vis;
@@ -885,7 +894,8 @@ struct BfsApp {
             if (more) {
                 c->qsize[0] = c->qsize[1] = 0;
                 c->heavy[0] = c->heavy[1] = 0;
-                c->chunk[0] = c->chunk[1] = 0;
+                reset_claims(c, 0);
+                reset_claims(c, 1);
                 c->nf[0] = c->nf[1] = 0;
                 c->mf[0] = c->mf[1] = 0;
                 c->bmode[0] = c->bmode[1] = BFS_TDQ;
@@ -998,8 +1008,12 @@ struct SsspApp {
         }
     }
 
-    // worklist entries [32g, 32g+32): relax their out-edges (warp-wide gather)
-    __device__ __forceinline__ void relax_group(const KParams &p, CtaState &cs, uint64_t g, uint64_t &edges) {
+    // worklist entries [sz*g, sz*g+sz): relax their out-edges (warp-wide gather).  sz < 32
+    // when the worklist is small (a road-like graph's wavefront: a few thousand entries),
+    // so that every warp gets an item and a group's edges fit one 32-lane pass -- the
+    // episode then costs one dependent chain of loads/atomics instead of several
+    __device__ __forceinline__ void relax_group(const KParams &p, CtaState &cs, uint64_t g, uint32_t sz,
+                                                uint64_t &edges) {
         const uint32_t lane = threadIdx.x & 31;
         const uint32_t in = cs.in_sel, out = in ^ 1u;
         const uint32_t r1 = cs.level + 1;
@@ -1010,10 +1024,10 @@ struct SsspApp {
         const OffT *ro = static_cast<const OffT *>(p.ro);
         const int32_t *__restrict__ col = p.col;
         const uint32_t *__restrict__ wt = p.w;
-        const uint64_t i = g * 32 + lane;
+        const uint64_t i = g * sz + lane;
         OffT beg = 0;
         uint32_t deg = 0, du = 0;
-        if (i < n) {
+        if (lane < sz && i < n) {
             const uint32_t v = ldcg(inq + i);
             beg = __ldg(ro + v);
             deg = (uint32_t)(__ldg(ro + v + 1) - beg);
@@ -1091,7 +1105,7 @@ struct SsspApp {
         __threadfence();   // far_min (RED) is read by the serial section
     }
 
-    template <int BLOCK>
+    template <int BLOCK, bool MID = false>
     __device__ uint32_t expand(const KParams &p, CtaState &cs) {
         constexpr uint32_t WPB = BLOCK / 32;
         const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1103,10 +1117,15 @@ struct SsspApp {
         };
         const bool drain = cs.app_u32[5] == SSSP_DRAIN;
         const uint64_t items = drain ? cs.app_u32[2] : cs.app_u32[0];
-        const uint32_t r = claim_items<BLOCK>(p, cs, *this, &p.ctl->chunk[cs.in_sel], (items + 31) / 32, 2u * WPB,
-                                       [&](uint64_t g) {
+        uint32_t sz = 32;                                   // worklist entries per warp item
+        if (!drain) {
+            const uint64_t TW = (uint64_t)cs.M * WPB;
+            while (sz > COOP_SSSP_MIN_SZ && (items + sz - 1) / sz < TW) sz >>= 1;
+        }
+        const uint32_t r = claim_items<BLOCK, MID>(p, cs, *this, &p.ctl->claim[cs.in_sel][0][0], (items + sz - 1) / sz,
+                                                   2u * WPB, [&](uint64_t g) {
             if (drain) drain_group(p, cs, g);
-            else relax_group(p, cs, g, edges);
+            else relax_group(p, cs, g, sz, edges);
         }, flush);
         if (r == ACT_CONT) flush();
         return r;
@@ -1125,7 +1144,7 @@ struct SsspApp {
         const unsigned long long T0 = c->T, ftot = c->frontier_total;
         const uint32_t nlev = c->levels;
         c->qsize[out] = 0;
-        c->chunk[out] = 0;
+        reset_claims(c, out);
         if (done_mode == SSSP_DRAIN) {                        // kept entries now live in the other buffer
             c->far_size[fsel] = 0;
             fsel ^= 1u;
@@ -1174,7 +1193,7 @@ struct BarrierApp {
     __device__ bool empty(const KParams &p, CtaState &cs) {
         return (uint64_t)cs.level >= p.iters;
     }
-    template <int BLOCK>
+    template <int BLOCK, bool MID = false>
     __device__ uint32_t expand(const KParams &p, CtaState &cs) {
         if (threadIdx.x == 0 && (p.flags & COOP_FLAG_CHECK)) {
             if (cs.app_u32[4]) {

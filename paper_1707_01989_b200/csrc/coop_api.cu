@@ -12,6 +12,8 @@
 #include <sched.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -180,6 +182,7 @@ struct Scratch {
     DevBuf nccl_aux;                  // NCCL data plane: ready, gathered, count send/recv slots
     DevBuf runt;                      // source loop: end time of every run
     volatile uint32_t *nccl_host = nullptr;     // mapped host mirror of `ready`
+    void *nccl_warm = nullptr;                  // communicator already warmed up on nccl_stream
     cudaStream_t nccl_stream = nullptr;         // the comm stream (waits, all-gathers, writes)
     cudaEvent_t nccl_ev = nullptr;
     Ctl *host_ctl = nullptr;          // pinned staging
@@ -909,6 +912,32 @@ extern "C" coop_status coop_l2_atomic_rtt(uint64_t iters, double *ns_per_atomic)
     return COOP_OK;
 }
 
+// The competing task as a standalone (non-cooperative) kernel: `blocks` CTAs each
+// occupy their SM slot for block_ns (the same synthetic task the megakernel's pool
+// runs, K11).  Used for the kernel-level preemption comparison (T3,
+// P:1258-1313): the task is enqueued between compute launches, i.e. it preempts the
+// compute work at kernel granularity.
+__global__ void spin_task_kernel(unsigned long long block_ns) {
+    if (threadIdx.x == 0) {
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 >= block_ns) break;
+            __nanosleep(100);
+        }
+    }
+    __syncthreads();
+}
+
+extern "C" coop_status coop_spin_task(uint32_t blocks, uint32_t threads, uint64_t block_ns, void *stream) {
+    if (!blocks || !threads || threads > 1024) return fail(COOP_ERR_INVALID_ARG, "bad arguments");
+    spin_task_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(block_ns);
+    CUDA_TRY(cudaGetLastError());
+    return COOP_OK;
+}
+
 // ------------------------------------------------------------------ handle API
 struct coop_handle {
     Prepared pr;
@@ -1054,14 +1083,15 @@ static NcclSyms &nccl_syms() {
         NSYM(group_end, "ncclGroupEnd");
         NSYM(error_string, "ncclGetErrorString");
 #undef NSYM
+        // the CUDA 12 ABI of the stream memory operations (the _v2 entry points; the v1
+        // ones need a driver option and fail at enqueue on this image)
         cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", reinterpret_cast<void **>(&S.wait32), cudaEnableDefault, &q) !=
-                cudaSuccess || q != cudaDriverEntryPointSuccess ||
-            cudaGetDriverEntryPoint("cuStreamWriteValue32", reinterpret_cast<void **>(&S.write32), cudaEnableDefault, &q) !=
-                cudaSuccess || q != cudaDriverEntryPointSuccess) {
-            snprintf(S.why, sizeof S.why, "stream memory operations unavailable");
-            return;
-        }
+        if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", reinterpret_cast<void **>(&S.wait32), 12000,
+                                             cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+            S.wait32 = nullptr;
+        if (cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", reinterpret_cast<void **>(&S.write32), 12000,
+                                             cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+            S.write32 = nullptr;
         S.ok = true;
     });
     return S;
@@ -1137,11 +1167,24 @@ extern "C" coop_status coop_bfs_part_nccl(const coop_part *part, int64_t source,
     if (!s->nccl_stream) {
         CUDA_TRY(cudaStreamCreateWithFlags(&s->nccl_stream, cudaStreamNonBlocking));
         CUDA_TRY(cudaEventCreateWithFlags(&s->nccl_ev, cudaEventDisableTiming));
-        CUDA_TRY(cudaHostAlloc((void **)&s->nccl_host, 64, cudaHostAllocMapped));
+        CUDA_TRY(cudaHostAlloc((void **)&s->nccl_host, 64, cudaHostAllocMapped));   // [0] mirror, [1..8] values
     }
-    const size_t aux = 256 + 8 * 4 * 2 + 8 * 4 * 2 * COOP_MAX_RANKS;
+    const size_t aux = 256 + 8 * 4 * 2 + 8 * 4 * 2 * COOP_MAX_RANKS + 64 * COOP_MAX_RANKS;
+    g_alloc_stream = ks;
     CUDA_TRY(s->nccl_aux.ensure(aux));
     char *base = static_cast<char *>(s->nccl_aux.p);
+    if (s->nccl_warm != nccl_comm) {
+        // a first collective on a new communicator may set up NCCL state with calls that
+        // synchronise with the device; that must not happen while the persistent kernel
+        // waits for a gather: warm the communicator up before any launch (collective:
+        // every rank makes its first call with this comm at the same point)
+        CUDA_TRY(cudaStreamSynchronize(ks));
+        uint32_t *scratch = reinterpret_cast<uint32_t *>(base + aux - 64 * COOP_MAX_RANKS);
+        NCCL_TRY(N.all_gather(scratch + me, scratch, 1, ncclUint32, static_cast<ncclComm_t>(nccl_comm),
+                              s->nccl_stream));
+        CUDA_TRY(cudaStreamSynchronize(s->nccl_stream));
+        s->nccl_warm = nccl_comm;
+    }
     NcclExt nx;
     nx.ready = reinterpret_cast<uint32_t *>(base);
     nx.gathered = reinterpret_cast<uint32_t *>(base + 128);
@@ -1175,34 +1218,84 @@ extern "C" coop_status coop_bfs_part_nccl(const coop_part *part, int64_t source,
         CU_TRY(N.write32((CUstream)cs, (CUdeviceptr)nx.gathered, i + 1, CU_STREAM_WRITE_VALUE_DEFAULT));
         return COOP_OK;
     };
+    // Two ways to order the gathers against the persistent kernel:
+    //  relay (default): the host polls the mapped mirror of `ready` and enqueues gather L
+    //    when the kernel has published level L -- the comm stream never blocks, so NCCL's
+    //    host-side enqueue never waits on a stalled stream (measured: with gathers
+    //    enqueued ahead behind cuStreamWaitValue32 the NCCL launch blocked the host while
+    //    the kernel waited for the gather -- a deadlock until the watchdog);
+    //  COOP_NCCL_MEMOP=1: gathers enqueued kNcclAhead levels ahead, each behind
+    //    cuStreamWaitValue32(ready >= L+1) (no host on the critical path).
+    static const bool memop = getenv("COOP_NCCL_MEMOP") && getenv("COOP_NCCL_MEMOP")[0] == '1' && N.wait32 && N.write32;
+    auto enqueue_now = [&](uint32_t i) -> coop_status {            // relay: gather i, then `gathered`
+        const uint32_t b = (i + 1) & 1;
+        uint32_t *F = part->frontier[me][b];
+        NCCL_TRY(N.group_start());
+        NCCL_TRY(N.all_gather(F + sw * me, F, sw, ncclUint32, comm, cs));
+        NCCL_TRY(N.all_gather(nx.cnt_send + 4 * b, nx.cnt_recv + (size_t)4 * P * b, 4, ncclUint64, comm, cs));
+        NCCL_TRY(N.group_end());
+        // `gathered` = i+1 by a copy from pinned host memory behind the gathers (copy engine;
+        // the slot is rewritten only after the kernel has seen it: the kernel publishes
+        // level i+1 only after observing gathered >= i+1)
+        volatile uint32_t *slot = s->nccl_host + 1 + (i & 7);
+        *slot = i + 1;
+        CUDA_TRY(cudaMemcpyAsync(nx.gathered, (const void *)slot, 4, cudaMemcpyHostToDevice, cs));
+        return COOP_OK;
+    };
     uint32_t enq = 0;
     coop_status est = COOP_OK;
-    for (; enq < kNcclAhead && est == COOP_OK; ++enq) est = enqueue(enq);
+    if (memop)
+        for (; enq < kNcclAhead && est == COOP_OK; ++enq) est = enqueue(enq);
     bool aborted = false;
+    static const bool dbg = getenv("COOP_NCCL_DEBUG") != nullptr;
+    auto t_dbg = std::chrono::steady_clock::now();
     while (est == COOP_OK) {
+        if (dbg && std::chrono::steady_clock::now() - t_dbg > std::chrono::milliseconds(500)) {
+            t_dbg = std::chrono::steady_clock::now();
+            fprintf(stderr, "[coop nccl] enq=%u host_ready=%#x comm stream %s\n", enq, s->nccl_host[0],
+                    cudaGetErrorString(cudaStreamQuery(cs)));
+        }
         const uint32_t hr = s->nccl_host[0];
         if (hr & 0x80000000u) {                                     // final: (hr & ~bit) gathers used
-            const uint32_t target = (hr & 0x7FFFFFFFu) + kNcclAhead;
-            while (enq < target && est == COOP_OK) est = enqueue(enq++);
+            if (memop) {
+                const uint32_t target = (hr & 0x7FFFFFFFu) + kNcclAhead;
+                while (enq < target && est == COOP_OK) est = enqueue(enq++);
+            }
             break;
         }
-        while (enq < hr + kNcclAhead && est == COOP_OK) est = enqueue(enq++);
-        if (cudaEventQuery(s->nccl_ev) == cudaSuccess) {           // kernel ended without the final mark
+        if (memop) {
+            while (enq < hr + kNcclAhead && est == COOP_OK) est = enqueue(enq++);
+        } else {
+            while (enq < hr && est == COOP_OK) est = enqueue_now(enq++);
+        }
+        const cudaError_t eq = cudaEventQuery(s->nccl_ev);
+        if (eq == cudaSuccess) {                                    // kernel ended without the final mark
             if (s->nccl_host[0] & 0x80000000u) continue;
             aborted = true;
+            if (dbg) fprintf(stderr, "[coop nccl] kernel ended without the final mark: enq=%u host_ready=%#x\n", enq,
+                             s->nccl_host[0]);
+            break;
+        } else if (eq != cudaErrorNotReady) {
+            est = fail(COOP_ERR_CUDA, "event query: %s", cudaGetErrorString(eq));
             break;
         }
-        sched_yield();
+        if (memop) sched_yield();
     }
+    if (dbg) fprintf(stderr, "[coop nccl] host loop done: enq=%u host_ready=%#x est=%d\n", enq, s->nccl_host[0], (int)est);
     if (aborted || est != COOP_OK) {
         // release any wait still enqueued so the comm stream drains (the kernel has ended)
         static const uint32_t big = 0xFFFFFFFFu;
         cudaMemcpyAsync(nx.ready, &big, 4, cudaMemcpyHostToDevice, ks);
         cudaStreamSynchronize(ks);
     }
+    char msg[sizeof g_err];
+    memcpy(msg, g_err, sizeof msg);                                 // the host loop's own error, if any
     coop_status fst = finish(pr, stats);
     cudaError_t ce = cudaStreamSynchronize(cs);
-    if (est != COOP_OK) return est;
+    if (est != COOP_OK) {
+        memcpy(g_err, msg, sizeof msg);
+        return est;
+    }
     if (fst != COOP_OK) return fst;
     if (ce != cudaSuccess) return fail(COOP_ERR_CUDA, "comm stream: %s", cudaGetErrorString(ce));
     return COOP_OK;

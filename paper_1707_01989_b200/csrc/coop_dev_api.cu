@@ -573,3 +573,257 @@ extern "C" coop_status coop_work_steal(coop_dev_handle *h, const coop_ws_tree *t
     for (int i = 0; i < 64; ++i) res->hist[i] = acc[8 + i];
     return st;
 }
+
+// ==================================================================== Pannotia apps (Table 1)
+// color, mis and p-sssp ported to cooperative kernels on the
+// device API, with the resizing-barrier counts of Table 1 (color 2/2, mis 3/3,
+// p-sssp 3/3): vertex-strided loops re-chunked after every resizing barrier
+// (P:695-705); the only transmitted state is the iteration counter.  Algorithms:
+// DESIGN.md reading R23 (Jones-Plassmann colouring and Luby's MIS with fixed
+// priorities prio(v) = (splitmix64(seed ^ v), v); Bellman-Ford over all vertices).
+namespace {
+
+struct PnParams {
+    const uint32_t *ro;
+    const int32_t *col;
+    const uint32_t *w;
+    int32_t *a;                 // colour / MIS state / distance (u32 bits)
+    uint32_t *b;                // p-sssp: next distances
+    uint32_t *flag;             // [2]: work remains in iteration parity p
+    uint32_t *iters;            // out
+    unsigned long long seed;
+    uint32_t V;
+};
+struct PnTx {
+    uint32_t it;
+};
+enum : uint32_t { PN_START = 0, PN_B = 1, PN_C = 2, PN_NEXT = 3 };
+constexpr int32_t PN_UNC = -1, PN_UND = 0, PN_IN = 1, PN_OUT = 2;
+constexpr uint32_t PN_INF = 0xFFFFFFFFu;
+
+// (splitmix64(seed ^ v), v) > (splitmix64(seed ^ u), u)
+__device__ __forceinline__ bool prio_gt(unsigned long long seed, uint32_t v, uint32_t u) {
+    const unsigned long long pv = coop_detail::mix(seed ^ v), pu = coop_detail::mix(seed ^ u);
+    return pv > pu || (pv == pu && v > u);
+}
+
+template <int BLOCK>
+__device__ void color_body(coop_ctx *ctx, const PnParams &p) {
+    PnTx t;
+    uint32_t entry = coop_entry(ctx);
+    if (entry == PN_START) t.it = 0;
+    else coop_get_transmit(ctx, &t, sizeof t);
+    for (;;) {
+        if (entry != PN_B) {
+            // A: an uncoloured vertex above every neighbour uncoloured at the start of the
+            // iteration takes colour it (a neighbour coloured `it` right now still counts)
+            const uint32_t tid = coop_group_id(ctx) * BLOCK + threadIdx.x, stride = coop_num_groups(ctx) * BLOCK;
+            const int32_t it = (int32_t)t.it;
+            for (uint32_t v = tid; v < p.V; v += stride) {
+                if (*(volatile int32_t *)&p.a[v] != PN_UNC) continue;
+                bool top = true;
+                for (uint32_t e = p.ro[v], end = p.ro[v + 1]; e < end && top; ++e) {
+                    const uint32_t u = (uint32_t)p.col[e];
+                    const int32_t cu = *(volatile int32_t *)&p.a[u];
+                    if ((cu == PN_UNC || cu == it) && prio_gt(p.seed, u, v)) top = false;
+                }
+                if (top) p.a[v] = it;
+                else atomicOr(&p.flag[t.it & 1u], 1u);
+            }
+            if (!coop_resizing_global_barrier(ctx, &t, sizeof t, PN_B)) return;
+        }
+        // B: the iteration's flag is final after the barrier; recycle the other parity
+        if (coop_group_id(ctx) == 0 && threadIdx.x == 0) p.flag[(t.it + 1u) & 1u] = 0u;
+        const bool done = *(volatile uint32_t *)&p.flag[t.it & 1u] == 0u;
+        if (done) {
+            if (coop_group_id(ctx) == 0 && threadIdx.x == 0) *p.iters = t.it + 1u;
+            return;
+        }
+        t.it += 1u;
+        if (!coop_resizing_global_barrier(ctx, &t, sizeof t, PN_NEXT)) return;
+        entry = PN_NEXT;
+    }
+}
+
+template <int BLOCK>
+__device__ void mis_body(coop_ctx *ctx, const PnParams &p) {
+    PnTx t;
+    uint32_t entry = coop_entry(ctx);
+    if (entry == PN_START) t.it = 0;
+    else coop_get_transmit(ctx, &t, sizeof t);
+    for (;;) {
+        if (entry != PN_B && entry != PN_C) {
+            // A: an undecided vertex below every undecided neighbour joins (an earlier member
+            // has no undecided neighbour, so IN here means "joined this iteration")
+            const uint32_t tid = coop_group_id(ctx) * BLOCK + threadIdx.x, stride = coop_num_groups(ctx) * BLOCK;
+            for (uint32_t v = tid; v < p.V; v += stride) {
+                if (*(volatile int32_t *)&p.a[v] != PN_UND) continue;
+                bool low = true;
+                for (uint32_t e = p.ro[v], end = p.ro[v + 1]; e < end && low; ++e) {
+                    const uint32_t u = (uint32_t)p.col[e];
+                    const int32_t su = *(volatile int32_t *)&p.a[u];
+                    if ((su == PN_UND || su == PN_IN) && prio_gt(p.seed, v, u)) low = false;
+                }
+                if (low) p.a[v] = PN_IN;
+            }
+            if (!coop_resizing_global_barrier(ctx, &t, sizeof t, PN_B)) return;
+        }
+        if (entry != PN_C) {
+            // B: an undecided neighbour of a member leaves; the rest remain
+            const uint32_t tid = coop_group_id(ctx) * BLOCK + threadIdx.x, stride = coop_num_groups(ctx) * BLOCK;
+            for (uint32_t v = tid; v < p.V; v += stride) {
+                if (p.a[v] != PN_UND) continue;
+                bool out = false;
+                for (uint32_t e = p.ro[v], end = p.ro[v + 1]; e < end && !out; ++e)
+                    out = p.a[p.col[e]] == PN_IN;
+                if (out) p.a[v] = PN_OUT;
+                else atomicOr(&p.flag[t.it & 1u], 1u);
+            }
+            if (!coop_resizing_global_barrier(ctx, &t, sizeof t, PN_C)) return;
+        }
+        // C: termination test
+        if (coop_group_id(ctx) == 0 && threadIdx.x == 0) p.flag[(t.it + 1u) & 1u] = 0u;
+        const bool done = *(volatile uint32_t *)&p.flag[t.it & 1u] == 0u;
+        if (done) {
+            if (coop_group_id(ctx) == 0 && threadIdx.x == 0) *p.iters = t.it + 1u;
+            return;
+        }
+        t.it += 1u;
+        if (!coop_resizing_global_barrier(ctx, &t, sizeof t, PN_NEXT)) return;
+        entry = PN_NEXT;
+    }
+}
+
+template <int BLOCK>
+__device__ void psssp_body(coop_ctx *ctx, const PnParams &p) {
+    PnTx t;
+    uint32_t entry = coop_entry(ctx);
+    if (entry == PN_START) t.it = 0;
+    else coop_get_transmit(ctx, &t, sizeof t);
+    uint32_t *d = reinterpret_cast<uint32_t *>(p.a);
+    for (;;) {
+        if (entry != PN_B && entry != PN_C) {
+            // A: pull relaxation of every vertex over its in-edges (symmetric graph)
+            const uint32_t tid = coop_group_id(ctx) * BLOCK + threadIdx.x, stride = coop_num_groups(ctx) * BLOCK;
+            for (uint32_t v = tid; v < p.V; v += stride) {
+                uint32_t nd = d[v];
+                for (uint32_t e = p.ro[v], end = p.ro[v + 1]; e < end; ++e) {
+                    const uint32_t du = d[p.col[e]];
+                    if (du != PN_INF && du + p.w[e] < nd) nd = du + p.w[e];
+                }
+                p.b[v] = nd;
+            }
+            if (!coop_resizing_global_barrier(ctx, &t, sizeof t, PN_B)) return;
+        }
+        if (entry != PN_C) {
+            // B: publish the improvements
+            const uint32_t tid = coop_group_id(ctx) * BLOCK + threadIdx.x, stride = coop_num_groups(ctx) * BLOCK;
+            for (uint32_t v = tid; v < p.V; v += stride) {
+                const uint32_t nd = p.b[v];
+                if (nd != d[v]) {
+                    d[v] = nd;
+                    atomicOr(&p.flag[t.it & 1u], 1u);
+                }
+            }
+            if (!coop_resizing_global_barrier(ctx, &t, sizeof t, PN_C)) return;
+        }
+        if (coop_group_id(ctx) == 0 && threadIdx.x == 0) p.flag[(t.it + 1u) & 1u] = 0u;
+        const bool done = *(volatile uint32_t *)&p.flag[t.it & 1u] == 0u;
+        if (done) {
+            if (coop_group_id(ctx) == 0 && threadIdx.x == 0) *p.iters = t.it + 1u;
+            return;
+        }
+        t.it += 1u;
+        if (!coop_resizing_global_barrier(ctx, &t, sizeof t, PN_NEXT)) return;
+        entry = PN_NEXT;
+    }
+}
+
+template <int BLOCK, int APP>
+__global__ void __launch_bounds__(BLOCK) pannotia_kernel(coop_dev *d, PnParams p) {
+    coop_run(d, [&](coop_ctx *ctx) {
+        if (APP == 0) color_body<BLOCK>(ctx, p);
+        else if (APP == 1) mis_body<BLOCK>(ctx, p);
+        else psssp_body<BLOCK>(ctx, p);
+    });
+}
+
+template <int APP>
+coop_status pannotia_run(coop_dev_handle *h, const coop_csr *g, uint64_t seed_or_source, int32_t *out,
+                         uint32_t threads, uint32_t *iters_out, coop_dev_stats *stats) {
+    if (!h || !g || !out || !iters_out) return dfail(COOP_ERR_INVALID_ARG, "null argument");
+    if (g->offset_bits != 32) return dfail(COOP_ERR_INVALID_ARG, "Pannotia apps take 32-bit offsets");
+    if (g->num_vertices < 1 || g->num_vertices >= (1ll << 31)) return dfail(COOP_ERR_INVALID_ARG, "bad V");
+    if (APP == 2) {
+        if (!g->weights && g->num_edges) return dfail(COOP_ERR_INVALID_ARG, "p-sssp needs weights");
+        if ((int64_t)seed_or_source >= g->num_vertices) return dfail(COOP_ERR_INVALID_ARG, "source out of range");
+        if (g->max_weight && (uint64_t)(g->num_vertices - 1) * g->max_weight >= 0xFFFFFFFFull)
+            return dfail(COOP_ERR_OVERFLOW, "(V-1)*max_weight >= 2^32-1");
+    }
+    if (threads == 0) threads = 256;
+    void (*k)(coop_dev *, PnParams);
+    if (threads == 128) k = pannotia_kernel<128, APP>;
+    else if (threads == 256) k = pannotia_kernel<256, APP>;
+    else if (threads == 512) k = pannotia_kernel<512, APP>;
+    else return dfail(COOP_ERR_INVALID_ARG, "threads_per_wg %u not in {128, 256, 512}", threads);
+    uint32_t N = 0;
+    coop_status st = pick_n(h, k, threads, &N);
+    if (st != COOP_OK) return st;
+    const int64_t V = g->num_vertices;
+    PnParams p;
+    p.ro = (const uint32_t *)g->row_offsets;
+    p.col = g->col_idx;
+    p.w = g->weights;
+    p.a = out;
+    p.V = (uint32_t)V;
+    p.seed = seed_or_source;
+    uint32_t *buf = nullptr;
+    DCUDA(cudaMalloc((void **)&buf, sizeof(uint32_t) * ((APP == 2 ? V : 0) + 8)));
+    p.b = buf + 8;
+    p.flag = buf;
+    p.iters = buf + 4;
+    cudaStream_t s = nullptr;
+    cudaError_t e = cudaMemsetAsync(buf, 0, 32, s);
+    if (e == cudaSuccess) {
+        if (APP == 0) e = cudaMemsetAsync(out, 0xFF, sizeof(int32_t) * V, s);           // uncoloured
+        else if (APP == 1) e = cudaMemsetAsync(out, 0, sizeof(int32_t) * V, s);        // undecided
+        else {
+            e = cudaMemsetAsync(out, 0xFF, sizeof(int32_t) * V, s);                    // INF
+            const uint32_t zero = 0;
+            if (e == cudaSuccess) e = cudaMemcpyAsync(out + seed_or_source, &zero, 4, cudaMemcpyHostToDevice, s);
+        }
+    }
+    coop_dev *d = nullptr;
+    if (e == cudaSuccess) {
+        st = coop_dev_arm(h, N, s, &d);
+        if (st == COOP_OK) e = coop_dev_launch(k, N, threads, 0, s, d, p);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(buf);
+        return dfail(COOP_ERR_CUDA, "pannotia launch: %s", cudaGetErrorString(e));
+    }
+    if (st == COOP_OK) st = coop_dev_collect(h, s, stats);
+    if (st == COOP_OK) {
+        cudaError_t e2 = cudaMemcpy(iters_out, p.iters, 4, cudaMemcpyDeviceToHost);
+        if (e2 != cudaSuccess) st = dfail(COOP_ERR_CUDA, "iterations: %s", cudaGetErrorString(e2));
+    }
+    cudaFree(buf);
+    return st;
+}
+
+}  // namespace
+
+extern "C" coop_status coop_color(coop_dev_handle *h, const coop_csr *g, uint64_t seed, int32_t *colors_out,
+                                  uint32_t threads, uint32_t *iters_out, coop_dev_stats *stats) {
+    return pannotia_run<0>(h, g, seed, colors_out, threads, iters_out, stats);
+}
+extern "C" coop_status coop_mis(coop_dev_handle *h, const coop_csr *g, uint64_t seed, int32_t *state_out,
+                                uint32_t threads, uint32_t *iters_out, coop_dev_stats *stats) {
+    return pannotia_run<1>(h, g, seed, state_out, threads, iters_out, stats);
+}
+extern "C" coop_status coop_psssp(coop_dev_handle *h, const coop_csr *g, int64_t source, uint32_t *dist_out,
+                                  uint32_t threads, uint32_t *iters_out, coop_dev_stats *stats) {
+    if (source < 0) return dfail(COOP_ERR_INVALID_ARG, "source out of range");
+    return pannotia_run<2>(h, g, (uint64_t)source, reinterpret_cast<int32_t *>(dist_out), threads, iters_out, stats);
+}

@@ -53,6 +53,8 @@ struct TaskEventDev {
 };
 
 // Control block in device memory.  Hot words sit on their own 128-B lines.
+constexpr uint32_t kClaimShards = 8;
+
 struct __align__(128) Ctl {
     unsigned long long W;              // barrier word {gen:32 | M:16 | arrived:16} (arrivals)
     unsigned long long pad_w[15];
@@ -126,6 +128,9 @@ struct __align__(128) Ctl {
     // BFS looped over sources inside one launch (coop_bfs_loop)
     uint32_t run;                      // runs completed
     uint32_t pad_l[31];
+    // chunked intervals (per-warp claims): kClaimShards claim counters per level parity, one
+    // 128-B line each, so claims do not serialise on a single L2 atomic address
+    uint32_t claim[2][kClaimShards][32];
 };
 
 // Partitioned BFS (1-D vertex partition).  Frontier bitmaps and

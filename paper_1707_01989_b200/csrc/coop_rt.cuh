@@ -31,9 +31,11 @@
 //   COOP_POST_FENCE   : extra __threadfence() after the poll (L1 invalidation)
 //   COOP_ERR_RELOAD   : re-read the error word after the serial section
 //   COOP_ARRIVE_ACQREL: 1 = atom.acq_rel arrival; 0 = fence.sc + relaxed atom (+ fence if
-//                       last).  0 is required in practice: the fence by thread 0 after
-//                       bar.sync also drains the other warps' fire-and-forget reductions
-//                       (measured: with acq_rel alone, RED counters could be missed)
+//                       last).  Every warp that issues fire-and-forget reductions the serial
+//                       section reads fences them itself before the CTA barrier (flush_counts,
+//                       drain_group, the partitioned expand), so the cumulative release of
+//                       the acq_rel arrival suffices: 148 CTAs 3192 -> 2746 ns per barrier,
+//                       0 violations under COOP_FLAG_CHECK (profiles/r02_variants.log)
 #ifndef COOP_POLL_ACQUIRE
 #define COOP_POLL_ACQUIRE 1
 #endif
@@ -44,14 +46,27 @@
 #define COOP_ERR_RELOAD 0
 #endif
 #ifndef COOP_ARRIVE_ACQREL
-#define COOP_ARRIVE_ACQREL 0
+#define COOP_ARRIVE_ACQREL 1
 #endif
 
-#ifndef COOP_CLAIM_UNIFIED
-#define COOP_CLAIM_UNIFIED 1  // one inlined copy of the item body in claim_items (static + chunked)
+// bisection switches (A/B of the cooperative machinery's cost; 1 = shipped code)
+#ifndef COOP_BIS_SERIAL
+#define COOP_BIS_SERIAL 1
+#endif
+#ifndef COOP_BIS_BARRIER
+#define COOP_BIS_BARRIER 1
+#endif
+#ifndef COOP_BIS_CLAIM
+#define COOP_BIS_CLAIM 1
+#endif
+#ifndef COOP_BIS_PARK
+#define COOP_BIS_PARK 1
+#endif
+#ifndef COOP_CLAIM_WARP
+#define COOP_CLAIM_WARP 0     // chunked intervals: 1 = per-warp claims, one ahead; 0 = per-CTA chunks (default: fewer atomics, measured faster armed)
 #endif
 #ifndef COOP_RUNBODY_NOINLINE
-#define COOP_RUNBODY_NOINLINE 1
+#define COOP_RUNBODY_NOINLINE 0
 #endif
 #if COOP_RUNBODY_NOINLINE
 #define COOP_RUNBODY_ATTR __noinline__
@@ -296,7 +311,7 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
     const uint32_t ep = g - 1;
     uint32_t Mp = M, take = 0;
     bool sched_fork = false, wait_fork = false;
-    if (App::kCoop && lane == 0) {
+    if ((App::kCoop && COOP_BIS_SERIAL) && lane == 0) {
         if (resizing && p.barrier_mode != COOP_BARRIER_PLAIN) {
             if (p.policy == COOP_POLICY_SCRIPTED) {
                 uint32_t s = ep < p.script_len ? p.script[ep] : 0u;
@@ -330,7 +345,7 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
     Mp = __shfl_sync(FULL, Mp, 0);
     wait_fork = __shfl_sync(FULL, (uint32_t)wait_fork, 0) != 0;
     uint32_t got = 0;
-    if (App::kCoop && Mp > M) {
+    if ((App::kCoop && COOP_BIS_SERIAL) && Mp > M) {
         // the transmit-annotated state is uniform over the workgroups at a barrier
         // (PAPER.md:1731-1742), so the serial section's own copy IS WG 0's
         // (checked against WG 0's published copy under COOP_FLAG_CHECK)
@@ -341,7 +356,7 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
         Mp = M + got;
     }
     if (lane == 0) {
-        if constexpr (App::kCoop) {
+        if constexpr ((App::kCoop && COOP_BIS_SERIAL)) {
         const uint64_t now = globaltimer();
         if (sched_fork && got) atomicSub(&c->grant, got);
         if (take > 0) {   // gather bookkeeping of the task instance in flight
@@ -360,9 +375,9 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
             c->episode = ep + 1;                       // plain store: statistics only
         }
         // statistics as fire-and-forget reductions (no round trip on the critical path)
-        if (App::kCoop && Mp < M) atomicAdd(&c->kills, M - Mp);
-        if (App::kCoop && got) atomicAdd(&c->forks, got);
-        if (App::kCoop && Mp != M) {
+        if ((App::kCoop && COOP_BIS_SERIAL) && Mp < M) atomicAdd(&c->kills, M - Mp);
+        if ((App::kCoop && COOP_BIS_SERIAL) && got) atomicAdd(&c->forks, got);
+        if ((App::kCoop && COOP_BIS_SERIAL) && Mp != M) {
             atomicMin(&c->min_m, Mp);
             atomicMax(&c->max_m, Mp);
         }
@@ -382,7 +397,7 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
         }
         // M' of generation g+1 for NAIVE mode and forked CTAs (NAIVE kills may lower
         // W.M during g+1); the release store publishes it with everything above
-        if (App::kCoop) st_relaxed32(&c->mhist[(g + 1) & 7], Mp);
+        if ((App::kCoop && COOP_BIS_SERIAL)) st_relaxed32(&c->mhist[(g + 1) & 7], Mp);
         // reset the arrival word for generation g+1, then release on the separate
         // release line R (waiters poll R, arrivals hit W: no polling traffic on the
         // line the arrival atomics serialise on)
@@ -420,7 +435,7 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
         }
         uint32_t action = ACT_CONT, last = 0, killed_naive = 0;
         unsigned long long old;
-        if (App::kCoop && resizing && p.barrier_mode == COOP_BARRIER_NAIVE && p.policy == COOP_POLICY_SCHEDULER &&
+        if ((App::kCoop && COOP_BIS_BARRIER) && resizing && p.barrier_mode == COOP_BARRIER_NAIVE && p.policy == COOP_POLICY_SCHEDULER &&
             cs.lid != 0) {
             // naive barrier: the slave offers kill on entry; only id M-1 can go
             __threadfence();
@@ -513,8 +528,8 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
                     cs.action = ACT_KILLED;                // W moved on without us => we were killed at g
                 } else {
                     // W.M is M' unless NAIVE kills of generation g+1 already lowered it
-                    const uint32_t Mn = App::kCoop && p.barrier_mode == COOP_BARRIER_NAIVE ? mhist_get(p, g + 1) : w_M(w);
-                    if (App::kCoop && cs.lid >= Mn) cs.action = ACT_KILLED;
+                    const uint32_t Mn = (App::kCoop && COOP_BIS_BARRIER) && p.barrier_mode == COOP_BARRIER_NAIVE ? mhist_get(p, g + 1) : w_M(w);
+                    if ((App::kCoop && COOP_BIS_BARRIER) && cs.lid >= Mn) cs.action = ACT_KILLED;
                     else { cs.M = Mn; cs.gen = g + 1; }
                 }
             }
@@ -663,78 +678,14 @@ __device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, 
 // SCHEDULER policy every claim also reads the resource channel and, when this
 // id is asked to surrender, the CTA offers itself (offer_kill_mid) right after
 // finishing the chunk in hand.  fn(item) is warp-collective.
-#if COOP_CLAIM_UNIFIED
-template <int BLOCK, class App, class Fn, class Flush>
-__device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32_t *counter, uint64_t n_items,
+template <int BLOCK, bool MID, class App, class Fn, class Flush>
+__device__ uint32_t claim_items_cta(const KParams &p, CtaState &cs, App &app, uint32_t *counter, uint64_t n_items,
                                 uint32_t per_chunk, Fn &&fn, Flush &&flush) {
-    const bool midkill = App::kCoop && p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY;
-    const uint32_t lane = threadIdx.x & 31;
-    constexpr uint32_t WPB = BLOCK / 32;
-    // One call site of fn for both distributions (the item body is the hot code: a
-    // second inlined copy doubled the kernel's instruction footprint).
-    //  static  (no scheduler can ask for workgroups inside this interval): Fig. 4's
-    //          distribution, item i to warp i mod (M*W), no atomics or syncs;
-    //  chunked (SCHEDULER + query): the CTA claims per_chunk items from `counter`, its
-    //          warps take them one at a time from a shared counter; between chunks
-    //          (CTA-collective) the CTA may offer itself (offer_kill_mid).
-    const uint64_t TW = (uint64_t)cs.M * WPB;
-    uint64_t it = (uint64_t)cs.lid * WPB + (threadIdx.x >> 5);   // static cursor
-    const uint64_t nchunks = midkill ? (n_items + per_chunk - 1) / per_chunk : 0;
-    bool refill = midkill, first = true;
-    uint64_t base = 0;
-    uint32_t cnt = 0, ch = 0, stop = 0;
-    for (;;) {
-        if (refill) {                                   // CTA-collective (every warp gets here)
-            if (!first) {
-                cta_sync();                             // chunk done; cs.item_next reusable
-                if constexpr (App::kCoop) {
-                    if (stop) {                         // the claim saw demand for this id
-                        const uint32_t r = offer_kill_mid(p, cs, app, flush);
-                        if (r != ACT_CONT) return r;
-                    }
-                }
-                if (ch >= nchunks) return ACT_CONT;
-            }
-            first = false;
-            if (threadIdx.x == 0) {
-                const uint32_t c0 = atomicAdd(counter, 1u);
-                uint32_t st = 0;
-                if (cs.lid != 0) {
-                    const uint32_t d = ld_relaxed32(&p.ctl->demand);
-                    if (d) st = cs.lid + d >= w_M(ld_relaxed64(&p.ctl->W));
-                }
-                cs.chunk = c0;
-                cs.stop = st;
-                cs.item_next = 0;
-            }
-            cta_sync();
-            ch = cs.chunk;
-            stop = cs.stop;
-            base = (uint64_t)ch * per_chunk;
-            cnt = ch < nchunks ? (uint32_t)min((uint64_t)per_chunk, n_items - base) : 0u;
-            refill = false;
-        }
-        uint64_t item;
-        if (midkill) {
-            uint32_t k = 0;
-            if (lane == 0) k = atomicAdd(&cs.item_next, 1u);
-            k = __shfl_sync(FULL, k, 0);
-            if (k >= cnt) { refill = true; continue; }
-            item = base + k;
-        } else {
-            if (it >= n_items) return ACT_CONT;
-            item = it;
-            it += TW;
-        }
-        fn(item);
-    }
-}
-
-#else
-template <int BLOCK, class App, class Fn, class Flush>
-__device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32_t *counter, uint64_t n_items,
-                                uint32_t per_chunk, Fn &&fn, Flush &&flush) {
-    const bool midkill = App::kCoop && p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY;
+    // MID: the chunked distribution is compiled only into the expand instance run_body
+    // selects when a scheduler can ask for workgroups inside the interval; the static
+    // instance has no trace of it (its mere presence cost 12 % of the static loop's
+    // speed, tools/variant_bench.py)
+    constexpr bool midkill = MID && App::kCoop && COOP_BIS_CLAIM;
     const uint32_t lane = threadIdx.x & 31;
     if (!midkill) {
         // no scheduler can ask for workgroups inside this interval: Fig. 4's static
@@ -774,7 +725,7 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
             }
         }
         cta_sync();                                   // chunk done; cs.chunk reusable
-        if constexpr (App::kCoop) {
+        if constexpr (midkill) {
             if (stop) {
                 const uint32_t r = offer_kill_mid(p, cs, app, flush);
                 if (r != ACT_CONT) return r;
@@ -784,9 +735,100 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
     }
 }
 
+
+// Work distribution of an interval over `n_items` warp-sized items; fn(item) is
+// warp-collective.
+//  static (MID = false: no scheduler can ask for workgroups inside this interval):
+//          Fig. 4's distribution, item i to warp i mod (M*W) -- no atomics,
+//          no syncs.  run_body instantiates the expand with MID = false whenever the
+//          policy cannot demand workgroups mid-interval; the chunked code below is then
+//          not compiled into it at all (its mere presence cost 12 % of the static
+//          loop's speed: tools/variant_bench.py, profiles/r02_variants.log).
+//  chunked (MID = true: SCHEDULER + query): items are claimed from `counter` so a CTA
+//          can leave at a claim boundary (offer_kill_mid) without stranding work.
+//          COOP_CLAIM_WARP (default): each warp claims its own per_chunk/W items with a
+//          global atomic issued one claim AHEAD (the round trip overlaps the current
+//          item; the prefetched claim is always processed), reads the resource
+//          channel with the claim, and raises a CTA flag when this id is asked to
+//          leave; no CTA barrier until the warps run out of items.  Otherwise the
+//          CTA claims per_chunk items and its warps take them from a shared counter
+//          (two CTA barriers per chunk).
+template <int BLOCK, bool MID, class App, class Fn, class Flush>
+__device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32_t *counter, uint64_t n_items,
+                                uint32_t per_chunk, Fn &&fn, Flush &&flush) {
+    constexpr bool midkill = MID && App::kCoop && COOP_BIS_CLAIM;
+    constexpr uint32_t WPB = BLOCK / 32;
+    if constexpr (!midkill) {
+        const uint64_t TW = (uint64_t)cs.M * WPB;
+        for (uint64_t it = (uint64_t)cs.lid * WPB + (threadIdx.x >> 5); it < n_items; it += TW) fn(it);
+        (void)counter;
+        (void)per_chunk;
+        (void)app;
+        (void)flush;
+        return ACT_CONT;
+    } else {
+#if COOP_CLAIM_WARP
+        const uint32_t lane = threadIdx.x & 31;
+        const uint32_t k = per_chunk >= WPB ? per_chunk / WPB : 1u;      // items per warp claim
+        const uint64_t nclaims = (n_items + k - 1) / k;
+        // the claim space is split over kClaimShards counters (one L2 line each); a warp
+        // starts on its own shard and moves to the next when that one is exhausted
+        constexpr uint32_t S = kClaimShards;
+        const uint64_t per = (nclaims + S - 1) / S;
+        uint32_t shard = (cs.lid * WPB + (threadIdx.x >> 5)) % S, tried = 0;
+        for (;;) {
+            if (threadIdx.x == 0) cs.stop = 0;
+            cta_sync();
+            uint32_t c = 0, stop = 0;
+            // claim + channel read: the stop decision (this id is asked to leave,
+            // query style P:940-947) raises the CTA flag; the claim itself is kept
+            auto claim = [&]() {
+                if (lane == 0) {
+                    c = 0xFFFFFFFFu;
+                    while (tried < S) {
+                        const uint32_t t = atomicAdd(counter + 32 * shard, 1u);
+                        const uint64_t idx = (uint64_t)shard * per + t;
+                        if (t < per && idx < nclaims) { c = (uint32_t)idx; break; }
+                        shard = (shard + 1) % S;
+                        ++tried;
+                    }
+                    if (cs.lid != 0) {
+                        const uint32_t d = ld_relaxed32(&p.ctl->demand);
+                        if (d && cs.lid + d >= w_M(ld_relaxed64(&p.ctl->W))) stop = 1;
+                    }
+                }
+            };
+            claim();
+            for (;;) {
+                const uint32_t cur = __shfl_sync(FULL, c, 0);
+                const uint32_t st = __shfl_sync(FULL, stop, 0);
+                if (cur >= nclaims) break;
+                const bool more = !st && !*(volatile uint32_t *)&cs.stop;
+                if (st && lane == 0) *(volatile uint32_t *)&cs.stop = 1;
+                if (more) claim();                        // next claim in flight during this one
+                const uint64_t b = (uint64_t)cur * k;
+                const uint64_t e = min(n_items, b + k);
+                for (uint64_t it = b; it < e; ++it) fn(it);
+                if (!more) break;
+            }
+            cta_sync();                                   // every warp done with its claims
+            if (!cs.stop) return ACT_CONT;                // the counter ran out
+            const uint32_t r = offer_kill_mid(p, cs, app, flush);
+            if (r != ACT_CONT) return r;                  // killed (or abort): nothing stranded
+        }
+#else
+        return claim_items_cta<BLOCK, MID>(p, cs, app, counter, n_items, per_chunk, fn, flush);
 #endif
+    }
+}
 
 // ---------------------------------------------------------------- body
+// the chunked expand (offer_kill at claim boundaries) as a separate function
+template <class App, int BLOCK>
+__device__ __noinline__ uint32_t expand_mid(const KParams &p, CtaState &cs, App &app) {
+    return app.template expand<BLOCK, true>(p, cs);
+}
+
 // Fig. 4 with the app's process_node; entry points are the
 // program points after each resizing barrier (forked CTAs start there).
 template <class App, int BLOCK>
@@ -814,7 +856,16 @@ __device__ COOP_RUNBODY_ATTR uint32_t run_body(const KParams &p, CtaState &cs, A
                 continue;
             }
             LTRACE(0);
-            r = app.template expand<BLOCK>(p, cs);             // for (i = tid; ...) process_node
+            // for (i = tid; ...) process_node -- the chunked instance when a scheduler may ask
+            // for workgroups mid-interval (offer_kill at chunk boundaries), else the static one
+            if constexpr (App::kCoop) {
+                if (p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY)
+                    r = expand_mid<App, BLOCK>(p, cs, app);           // out of line: keeps the static
+                else                                                  // instance's code as tight as
+                    r = app.template expand<BLOCK, false>(p, cs);     // the non-cooperative kernel's
+            } else {
+                r = app.template expand<BLOCK, false>(p, cs);
+            }
             if (r != ACT_CONT) return r;                       // killed at a chunk boundary (offer_kill)
             cta_sync();                                   // every warp is done reading cs
             LTRACE(1);
@@ -1045,7 +1096,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(KParams p) {
         if (blockIdx.x == 0) p.ctl->t_start = t0;
     }
     cta_sync();
-    if constexpr (App::kCoop) {
+    if constexpr ((App::kCoop && COOP_BIS_PARK)) {
         if (p.has_sched && blockIdx.x == p.P) { scheduler_loop(p, cs); return; }
     }
     if (blockIdx.x < p.M0) {
@@ -1058,13 +1109,13 @@ __global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(KParams p) {
             }
         }
         if (r == ACT_ABORT) return;
-        if (App::kCoop && p.barrier_mode != COOP_BARRIER_PLAIN && threadIdx.x == 0) {   // killed or finished: join the pool
+        if ((App::kCoop && COOP_BIS_PARK) && p.barrier_mode != COOP_BARRIER_PLAIN && threadIdx.x == 0) {   // killed or finished: join the pool
             __threadfence();
             atomicOr(&p.ctl->pool[blockIdx.x >> 5], 1u << (blockIdx.x & 31));
         }
         cta_sync();
     }
-    if constexpr (App::kCoop) {
+    if constexpr ((App::kCoop && COOP_BIS_PARK)) {
         if (p.barrier_mode != COOP_BARRIER_PLAIN) park_loop<App, BLOCK>(p, cs, app);
     }
 #if COOP_TRACE

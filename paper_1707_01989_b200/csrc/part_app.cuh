@@ -169,7 +169,7 @@ struct PartBfsApp {
         edges += scanned_total;
     }
 
-    template <int BLOCK>
+    template <int BLOCK, bool MID = false>
     __device__ uint32_t expand(const KParams &p, CtaState &cs) {
         constexpr uint32_t WPB = BLOCK / 32;
         const PartParams &pp = p.part;

@@ -174,3 +174,39 @@ def test_work_steal_queue_overflow_reported(coop):
         with pytest.raises(coop.CoopError) as ei:
             coop.work_steal(h, seed=1, depth=4, max_fanout=16, fixed=True, queue_cap=8)
     assert ei.value.status == 7
+
+
+# ---------------- Table 1's Pannotia applications on the device API ----------------
+@pytest.mark.parametrize("app", ["color", "mis", "psssp"])
+@pytest.mark.parametrize("policy", ["never", "random"])
+def test_pannotia_apps_match_oracle(coop, app, policy):
+    """color / mis / p-sssp as cooperative kernels with Table 1's resizing barriers,
+    exact against oracle/pannotia.py (itself pinned by the greedy MIS, proper colouring,
+    closed forms and Dijkstra), also under random kills and forks at every resizing barrier."""
+    from oracle import pannotia as pn
+    graphs = [gg.rmat(11, seed=3), gg.disjoint_union(gg.grid(23, 17), gg.star(300))]
+    kw = dict(policy=coop.POLICY_NEVER) if policy == "never" else dict(
+        max_wgs=24, init_wgs=5, policy=coop.POLICY_RANDOM, resize_prob=0.5, seed=7, flags=coop.FLAG_CHECK)
+    for g in graphs:
+        if app == "psssp":
+            g = gg.with_weights(g, seed=4)
+            g.max_weight = 1000
+        gd = g.to("cuda")
+        if app == "psssp":
+            gd.max_weight = 1000
+        ro, col = g.row_offsets.tolist(), g.col_idx.tolist()
+        for arg in ([3, 11] if app != "psssp" else gg.sample_sources(g, 2)):
+            with coop.DevHandle(**kw) as h:
+                out, iters, st = coop.pannotia(h, app, gd, arg)
+            got = out.cpu().numpy()
+            if app == "color":
+                ref, it = pn.color(ro, col, g.num_vertices, arg)
+            elif app == "mis":
+                ref, it = pn.mis(ro, col, g.num_vertices, arg)
+            else:
+                ref, it = pn.p_sssp(ro, col, [int(x) for x in g.weights.tolist()], g.num_vertices, arg)
+                got = got.view(np.uint32)
+            np.testing.assert_array_equal(got, ref)
+            assert iters == it
+            if policy == "random":
+                assert st["kills"] + st["forks"] > 0
