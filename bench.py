@@ -412,6 +412,28 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags, 
         "slowdown_armed_vs_noncoop": geo([c / b for c, b in zip(per["coop_scheduler_armed"], per["noncoop"])]),
         "aggregation": "geomean over sources of per-source medians of 3 interleaved runs"}
     t_coop = per["coop_never"]
+    # the north_star path alone: pure top-down BFS (expand / claim / compact every level, no
+    # bottom-up levels) with its own roofline (same algorithmic-bytes formula)
+    td_t, td_b, td_e = [], [], 0
+    for i in range(k):
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.fill_(2)
+        k0.record(stream)
+        k1.record(stream)
+        _, st = coop.bfs(g, srcs[i], out, threads_per_wg=args.threads, ev_kernel_start=k0, ev_kernel_end=k1)
+        torch.cuda.synchronize(dev)
+        td_t.append(k0.elapsed_time(k1))
+        td_b.append(alg_bytes_bfs(st, g.num_vertices))
+        td_e += int(g.degrees()[out >= 0].sum().item()) // 2
+        if not args.no_verify:
+            checked.append((srcs[i], out.clone()))
+    peak, _ = _peaks()
+    ach = sum(td_b) / (sum(td_t) * 1e-3) / 1e9
+    ex["bfs_topdown"] = {"kernel_ms_mean": statistics.mean(td_t), "gteps": td_e / (sum(td_t) * 1e-3) / 1e9,
+                         "sources": k, "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                                                    "frac": ach / peak,
+                                                    "alg_bytes_per_launch": sum(td_b) / len(td_b)},
+                         "note": "top-down only (FLAG_DIROPT off): the north_star expand/claim/compact path"}
     # multitasked: scheduler CTA posts a task every P with Q = N/4 WGs (scaled light preset)
     mt = {}
     for name, (P_us, E_us) in {"stress": (200, 20)}.items():
@@ -571,8 +593,11 @@ def run_partitioned(args, ws, rank, local):
     V = part.num_vertices
     vb, ve = part.v_begin, part.v_end
     indeg = torch.bincount(part.col_local.to(torch.int64), minlength=ve - vb)   # = degree (symmetric graph)
-    pb = pt.PartitionedBFS(part, dev)
-    pb.connect_ipc()
+    pb = pt.PartitionedBFS(part, dev, exchange=args.exchange)
+    if args.exchange == "nccl":
+        pb.connect_nccl()                 # north_star's NCCL all-gather data plane
+    else:
+        pb.connect_ipc()                  # fused: in-kernel NVLink peer stores
     eg = torch.tensor([float(part.num_edges)], device=dev, dtype=torch.float64)
     dist.all_reduce(eg)
     pb.E_global = int(eg.item())
@@ -613,7 +638,10 @@ def run_partitioned(args, ws, rank, local):
                 "scaling": "weak", "vs_baseline": None, "dtype": "int32",
                 "data": "synthetic (RMAT, Graph500 parameters, seed 1, relabelled), generated per rank",
                 "config": {"workload": f"BFS RMAT-{scale} 1-D vertex-partitioned over {ws} GPUs (configs[4]), "
-                                       "frontier all-gather inside the cooperative kernel over NVLink peer memory",
+                                       + ("frontier all-gather by ncclAllGather per level (host relay)"
+                                          if args.exchange == "nccl" else
+                                          "frontier all-gather inside the cooperative kernel over NVLink peer memory"),
+                           "exchange": args.exchange,
                            "scale": scale, "vertices": V, "parallelism": f"1-D partition x{ws}",
                            "l2": "flushed (256 MB write) before every step", "graph_gen_s": round(gen_s, 2)},
                 "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": args.steps * ws,
@@ -637,6 +665,8 @@ def main():
     ap.add_argument("--no-verify", action="store_true", help="skip the oracle comparison of the outputs")
     ap.add_argument("--no-paper-multitask", action="store_true", help="skip the 10 s paper-preset loops")
     ap.add_argument("--loop-s", type=float, default=10.0, help="seconds per multitask loop (>= 10: P:1045)")
+    ap.add_argument("--exchange", default="nvlink", choices=["nvlink", "nccl"],
+                    help="N > 1: frontier exchange of the partitioned BFS")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -274,6 +274,7 @@ class PartCSR:
     nranks: int
     row_offsets: torch.Tensor
     col_local: torch.Tensor
+    weights: Optional[torch.Tensor] = None     # of the local edges (weighted graphs)
 
     @property
     def num_edges(self) -> int:
@@ -320,7 +321,8 @@ def partition(g: CSR, P: int, rank: int) -> PartCSR:
     cm = torch.zeros(col.numel() + 1, dtype=torch.int64, device=col.device)
     cm[1:] = torch.cumsum(keep.to(torch.int64), 0)
     ro = cm[g.row_offsets]
-    return PartCSR(g.num_vertices, vb, ve, rank, P, ro, (col[keep] - vb).to(torch.int32))
+    w = None if g.weights is None else g.weights[keep]
+    return PartCSR(g.num_vertices, vb, ve, rank, P, ro, (col[keep] - vb).to(torch.int32), w)
 
 
 def rmat_partition(scale: int, P: int, rank: int, edgefactor: int = 16, seed: int = 1, device="cpu",

@@ -304,6 +304,20 @@ typedef struct {
  * on COOP_OK entry i = hop distance of vertex v_begin + i, -1 if unreachable. */
 coop_status coop_bfs_part(const coop_part *part, int64_t source, int32_t *levels_owned_out,
                           const coop_opts *opts, coop_stats *stats);
+/* Partitioned SSSP ("(vertex, dist) exchange"): the same 1-D layout
+ * with weights_local (device uint32[num_edges], aligned with col_local); the
+ * frontier is exchanged as (vertex, distance) pairs: part->frontier[q][0..1] are
+ * rank q's two inboxes of uint64[num_vertices] (pairs of source rank r at offset
+ * v_begin(r)); slices must be graphgen.part_bounds' uniform ones.  Per round:
+ * relax the local edges of every rank's pairs (64-bit atomicMin on
+ * {dist | round mark}, reading R8), store the owned improved vertices with their
+ * final round distance into every rank's inbox, cross-GPU barrier in the second
+ * resizing barrier's serial section (counts; 0 = done).  dist_owned_out: device
+ * uint32[v_end - v_begin], 0xFFFFFFFF unreachable.  Blocking / asynchronous. */
+coop_status coop_sssp_part(const coop_part *part, const uint32_t *weights_local, int64_t source,
+                           uint32_t *dist_owned_out, const coop_opts *opts, coop_stats *stats);
+coop_status coop_sssp_part_launch(const coop_part *part, const uint32_t *weights_local, int64_t source,
+                                  uint32_t *dist_owned_out, const coop_opts *opts, coop_handle **handle);
 /* Asynchronous variant (finish with coop_wait); several ranks may share one GPU
  * when each uses its own opts->workspace and stream. */
 coop_status coop_bfs_part_launch(const coop_part *part, int64_t source, int32_t *levels_owned_out,

@@ -74,6 +74,7 @@
 #include <stdint.h>
 
 #include "coop.h"
+#include "coop_protocol.cuh"
 
 #define COOP_TX_MAX 64u                 /* bytes of transmitted state */
 #define COOP_DEV_MAX_CTAS 4096u
@@ -142,52 +143,9 @@ enum { COOP_ST_ACTIVE = 0, COOP_ST_KILLED = 1, COOP_ST_ABORT = 2 };
 
 namespace coop_detail {
 
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-__device__ __forceinline__ unsigned long long ld_acq64(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ unsigned long long ld_rlx64(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ uint32_t ld_acq32(const uint32_t *p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ uint32_t ld_rlx32(const uint32_t *p) {
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_rel64(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void st_rel32(uint32_t *p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_rlx64(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t W_gen(unsigned long long w) { return (uint32_t)(w >> 32); }
-__device__ __forceinline__ uint32_t W_M(unsigned long long w) { return (uint32_t)(w >> 16) & 0xFFFFu; }
-__device__ __forceinline__ uint32_t W_arr(unsigned long long w) { return (uint32_t)w & 0xFFFFu; }
-__device__ __forceinline__ unsigned long long W_pack(uint32_t g, uint32_t M, uint32_t a) {
-    return ((unsigned long long)g << 32) | ((unsigned long long)(M & 0xFFFFu) << 16) | (a & 0xFFFFu);
-}
-__device__ __forceinline__ unsigned long long mix(unsigned long long z) {   /* splitmix64 finaliser */
-    z += 0x9E3779B97F4A7C15ull;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
-}
+/* ordered accesses, the packed words and the generator come from the shared
+ * protocol header (the same steps the BFS/SSSP runtime uses) */
+using namespace coop_proto;
 
 /* CTA barrier after a region only some lanes of a warp execute (thread-0
  * blocks, spin loops).  Measured on sm_100a (tools/fork_repro.cu): when ptxas
@@ -207,10 +165,10 @@ __device__ __forceinline__ void cta_sync_after_t0() {
 __device__ __forceinline__ bool abort_check(coop_ctx *c, uint32_t &spins) {
     if ((++spins & 63u) != 0) return false;
     coop_dev *d = c->d;
-    if (ld_rlx32(&d->err) != COOP_DEV_ERR_NONE) return true;
-    if (gtimer() > c->deadline) {
+    if (ld_relaxed32(&d->err) != COOP_DEV_ERR_NONE) return true;
+    if (globaltimer() > c->deadline) {
         atomicCAS(&d->err, COOP_DEV_ERR_NONE, COOP_DEV_ERR_TIMEOUT);
-        st_rel32(&d->done, 1u);
+        st_release32(&d->done, 1u);
         return true;
     }
     return false;
@@ -230,7 +188,7 @@ __device__ __forceinline__ void assign(coop_dev *d, uint32_t phys, uint32_t lid,
     mb->entry = entry;
     copy_tx(mb->tx, tx, bytes);
     __threadfence();
-    st_rel32(&mb->flag, f + 1u);
+    st_release32(&mb->flag, f + 1u);
 }
 
 /* Warp-collective (warp 0): claim up to k parked CTAs from the pool bitmap.
@@ -241,52 +199,13 @@ __device__ __forceinline__ void assign(coop_dev *d, uint32_t phys, uint32_t lid,
 __device__ __noinline__ uint32_t claim_pool(coop_ctx *c, uint32_t k, bool wait, uint32_t *out_phys, uint32_t base,
                                             uint32_t gen, uint32_t entry, const uint8_t *tx, uint32_t bytes) {
     coop_dev *d = c->d;
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t nwords = (d->N + 31u) / 32u;
-    uint32_t got = 0, spins = 0;
-    while (got < k) {
-        for (uint32_t w0 = 0; w0 < nwords && got < k; w0 += 32u) {
-            const uint32_t wi = w0 + lane;
-            uint32_t word = wi < nwords ? ld_rlx32(&d->pool[wi]) : 0u;
-            const uint32_t cnt = __popc(word);
-            uint32_t incl = cnt;
-            for (int s = 1; s < 32; s <<= 1) {
-                const uint32_t n = __shfl_up_sync(0xffffffffu, incl, s);
-                if (lane >= (uint32_t)s) incl += n;
-            }
-            const uint32_t excl = incl - cnt, need = k - got;
-            const uint32_t want = need > excl ? min(cnt, need - excl) : 0u;
-            uint32_t mask = 0u;
-            for (uint32_t i = 0; i < want; ++i) {
-                const uint32_t b = word & (0u - word);
-                mask |= b;
-                word ^= b;
-            }
-            uint32_t claimed = mask ? (atomicAnd(&d->pool[wi], ~mask) & mask) : 0u;
-            const uint32_t nc = __popc(claimed);
-            uint32_t ci = nc;
-            for (int s = 1; s < 32; s <<= 1) {
-                const uint32_t n = __shfl_up_sync(0xffffffffu, ci, s);
-                if (lane >= (uint32_t)s) ci += n;
-            }
-            uint32_t r = got + ci - nc;
-            while (claimed) {
-                const uint32_t b = __ffs(claimed) - 1u;
-                claimed &= claimed - 1u;
-                if (out_phys) out_phys[r] = wi * 32u + b;
-                else assign(d, wi * 32u + b, base + r, gen, entry, tx, bytes);
-                ++r;
-            }
-            got += __shfl_sync(0xffffffffu, ci, 31);
-        }
-        if (!wait || got >= k) break;
-        uint32_t ab = 0;
-        if (lane == 0) ab = abort_check(c, spins) ? 1u : 0u;
-        if (__shfl_sync(0xffffffffu, ab, 0)) break;
-        __nanosleep(128);
-    }
-    __syncwarp();
-    return got;
+    uint32_t spins = 0;
+    return claim_idle(d->pool, (d->N + 31u) / 32u, k, wait,
+        [&](uint32_t phys, uint32_t i) {
+            if (out_phys) out_phys[i] = phys;
+            else assign(d, phys, base + i, gen, entry, tx, bytes);
+        },
+        [&]() { return abort_check(c, spins); });
 }
 
 /* Serial section of episode g (warp 0 of the CTA completing it; all M active
@@ -308,14 +227,14 @@ __device__ __noinline__ uint32_t serial_section(coop_ctx *c, uint32_t g, uint32_
             if (s) Mp = s;
             wait = true;
         } else if (d->policy == COOP_POLICY_RANDOM) {
-            unsigned long long h = mix(d->seed * 0x2545F4914F6CDD1Dull + ep);
+            unsigned long long h = mix64(d->seed * 0x2545F4914F6CDD1Dull + ep);
             if ((uint32_t)h < d->resize_thresh) Mp = 1u + (uint32_t)((h >> 32) % d->N);
             wait = true;
         } else if (d->policy == COOP_POLICY_SCHEDULER) {
             /* query(): W = outstanding demand, satisfied up to M-1 in one episode */
-            uint32_t t = ld_rlx32(&d->demand_taken);
+            uint32_t t = ld_relaxed32(&d->demand_taken);
             for (;;) {
-                const uint32_t posted = ld_rlx32(&d->demand_posted);
+                const uint32_t posted = ld_relaxed32(&d->demand_posted);
                 if (posted <= t || M <= 1) break;
                 const uint32_t want = min(posted - t, M - 1u);
                 const uint32_t old = atomicCAS(&d->demand_taken, t, t + want);
@@ -325,9 +244,9 @@ __device__ __noinline__ uint32_t serial_section(coop_ctx *c, uint32_t g, uint32_
             if (take) {
                 Mp = M - take;
             } else if (M < d->N) {
-                uint32_t gt = ld_rlx32(&d->grant_taken);
+                uint32_t gt = ld_relaxed32(&d->grant_taken);
                 for (;;) {
-                    const uint32_t posted = ld_rlx32(&d->grant_posted);
+                    const uint32_t posted = ld_relaxed32(&d->grant_posted);
                     if (posted <= gt) break;
                     const uint32_t want = min(posted - gt, d->N - M);
                     const uint32_t old = atomicCAS(&d->grant_taken, gt, gt + want);
@@ -377,8 +296,7 @@ __device__ __noinline__ uint32_t serial_section(coop_ctx *c, uint32_t g, uint32_
                 atomicCAS(&d->err, COOP_DEV_ERR_NONE, COOP_DEV_ERR_INVARIANT);
             }
         }
-        st_rlx64(&d->W, W_pack(g + 1u, Mp, 0u));
-        st_rel64(&d->R, W_pack(g + 1u, Mp, 0u));
+        publish(&d->W, &d->R, g + 1u, Mp);
     }
     return __shfl_sync(0xffffffffu, Mp, 0);
 }
@@ -399,27 +317,25 @@ __device__ __noinline__ bool barrier(coop_ctx *c, uint32_t kind, const void *tx,
             atomicAdd(&d->chk_arr[g & 1u], 1u);
             atomicOr(&d->idmap[g & 1u][c->lid >> 5], 1u << (c->lid & 31u));
         }
-        __threadfence();
-        const unsigned long long old = atomicAdd(&d->W, 1ull);
-        const uint32_t last = W_arr(old) + 1u == W_M(old);
-        if (last) __threadfence();
-        if (W_gen(old) != g) {
+        const unsigned long long old = arrive_fenced(&d->W);
+        const uint32_t last = is_last(old);
+        if (w_gen(old) != g) {
             atomicCAS(&d->err, COOP_DEV_ERR_NONE, COOP_DEV_ERR_INVARIANT);
-            st_rel32(&d->done, 1u);
+            st_release32(&d->done, 1u);
         }
         c->last = last;
-        c->bar_M = W_M(old);
+        c->bar_M = w_M(old);
         if (!last) {
             uint32_t spins = 0;
             unsigned long long r;
             for (;;) {
-                r = ld_acq64(&d->R);
-                if (W_gen(r) != g) break;
+                r = ld_acquire64(&d->R);
+                if (w_gen(r) != g) break;
                 if (abort_check(c, spins)) { c->state = COOP_ST_ABORT; break; }
             }
             if (c->state != COOP_ST_ABORT) {
-                if (W_gen(r) != g + 1u || c->lid >= W_M(r)) c->state = COOP_ST_KILLED;
-                else { c->M = W_M(r); c->gen = g + 1u; }
+                if (fate(r, g, c->lid) == FATE_KILLED) c->state = COOP_ST_KILLED;
+                else { c->M = w_M(r); c->gen = g + 1u; }
             }
         }
     }
@@ -447,14 +363,14 @@ __device__ __forceinline__ void coop_get_transmit(const coop_ctx *c, void *dst, 
 }
 /* outstanding demand (query), capped at M-1 */
 __device__ __forceinline__ uint32_t coop_query_dev(const coop_ctx *c) {
-    const uint32_t p = coop_detail::ld_rlx32(&c->d->demand_posted), t = coop_detail::ld_rlx32(&c->d->demand_taken);
+    const uint32_t p = coop_detail::ld_relaxed32(&c->d->demand_posted), t = coop_detail::ld_relaxed32(&c->d->demand_taken);
     const uint32_t w = p > t ? p - t : 0u;
     return c->M > 1u ? min(w, c->M - 1u) : 0u;
 }
 /* body-detected error: every CTA leaves, the host call returns COOP_ERR_INVARIANT/... */
 __device__ __forceinline__ void coop_abort(coop_ctx *c, uint32_t code) {
     atomicCAS(&c->d->err, COOP_DEV_ERR_NONE, code);
-    coop_detail::st_rel32(&c->d->done, 1u);
+    coop_detail::st_release32(&c->d->done, 1u);
 }
 
 __device__ __forceinline__ bool coop_global_barrier(coop_ctx *c) {
@@ -474,23 +390,23 @@ __device__ __noinline__ bool coop_offer_kill(coop_ctx *c) {
         c->last = 0;
         c->offers += 1u;
         bool accept = false, took = false;
-        if (c->lid != 0u && ld_rlx32(&d->err) == COOP_DEV_ERR_NONE) {
+        if (c->lid != 0u && ld_relaxed32(&d->err) == COOP_DEV_ERR_NONE) {
             if (d->policy == COOP_POLICY_RANDOM) {
-                const unsigned long long h = mix(d->seed ^ ((unsigned long long)c->phys << 40) ^ (c->calls++ * 2u));
+                const unsigned long long h = mix64(d->seed ^ ((unsigned long long)c->phys << 40) ^ (c->calls++ * 2u));
                 accept = (uint32_t)h < d->kill_thresh;
             } else if (d->policy == COOP_POLICY_SCHEDULER) {
-                accept = ld_rlx32(&d->demand_posted) > ld_rlx32(&d->demand_taken);
+                accept = ld_relaxed32(&d->demand_posted) > ld_relaxed32(&d->demand_taken);
             }
-        } else if (ld_rlx32(&d->err) != COOP_DEV_ERR_NONE) {
+        } else if (ld_relaxed32(&d->err) != COOP_DEV_ERR_NONE) {
             c->state = COOP_ST_ABORT;
         }
         if (accept) {
-            unsigned long long w = ld_rlx64(&d->W);
-            if (c->lid + 1u == W_M(w) && W_M(w) > 1u) {   /* only the top id can go */
+            unsigned long long w = ld_relaxed64(&d->W);
+            if (c->lid + 1u == w_M(w) && w_M(w) > 1u) {   /* only the top id can go */
                 if (d->policy == COOP_POLICY_SCHEDULER) {
-                    uint32_t t = ld_rlx32(&d->demand_taken);
+                    uint32_t t = ld_relaxed32(&d->demand_taken);
                     for (;;) {
-                        if (ld_rlx32(&d->demand_posted) <= t) break;
+                        if (ld_relaxed32(&d->demand_posted) <= t) break;
                         const uint32_t old = atomicCAS(&d->demand_taken, t, t + 1u);
                         if (old == t) { took = true; break; }
                         t = old;
@@ -499,16 +415,8 @@ __device__ __noinline__ bool coop_offer_kill(coop_ctx *c) {
                 }
                 if (accept) {
                     __threadfence();                       /* release this CTA's work */
-                    bool ok = false;
-                    uint32_t M = W_M(w), a = W_arr(w);
-                    for (;;) {                             /* arrivals may race the CAS */
-                        if (W_M(w) != c->lid + 1u || W_gen(w) != c->gen) break;   /* a fork/kill moved M */
-                        M = W_M(w);
-                        a = W_arr(w);
-                        const unsigned long long prev = atomicCAS(&d->W, w, W_pack(c->gen, M - 1u, a));
-                        if (prev == w) { ok = true; break; }
-                        w = prev;
-                    }
+                    uint32_t M = 0, a = 0;
+                    const bool ok = kill_top(&d->W, w, c->lid, c->gen, &a, &M);   /* fails if M/gen moved */
                     if (ok) {
                         c->state = COOP_ST_KILLED;
                         atomicAdd(&d->kills, 1u);
@@ -543,15 +451,15 @@ __device__ __noinline__ uint32_t coop_request_fork(coop_ctx *c, const void *tx, 
     coop_detail::cta_sync_after_t0();
     if (threadIdx.x == 0) {
         uint32_t k = 0;
-        const uint32_t M = W_M(ld_rlx64(&d->W));
-        if (M < d->N && ld_rlx32(&d->err) == COOP_DEV_ERR_NONE) {
+        const uint32_t M = w_M(ld_relaxed64(&d->W));
+        if (M < d->N && ld_relaxed32(&d->err) == COOP_DEV_ERR_NONE) {
             if (d->policy == COOP_POLICY_RANDOM) {
-                const unsigned long long h = mix(d->seed ^ ((unsigned long long)c->phys << 40) ^ (c->calls++ * 2u + 1u));
+                const unsigned long long h = mix64(d->seed ^ ((unsigned long long)c->phys << 40) ^ (c->calls++ * 2u + 1u));
                 if ((uint32_t)h < d->fork_thresh) k = 1u + (uint32_t)((h >> 32) % d->max_fork);
             } else if (d->policy == COOP_POLICY_SCHEDULER) {
-                uint32_t t = ld_rlx32(&d->grant_taken);
+                uint32_t t = ld_relaxed32(&d->grant_taken);
                 for (;;) {
-                    const uint32_t posted = ld_rlx32(&d->grant_posted);
+                    const uint32_t posted = ld_relaxed32(&d->grant_posted);
                     if (posted <= t) break;
                     const uint32_t want = min(min(posted - t, d->N - M), 32u);
                     const uint32_t old = atomicCAS(&d->grant_taken, t, t + want);
@@ -571,13 +479,7 @@ __device__ __noinline__ uint32_t coop_request_fork(coop_ctx *c, const void *tx, 
         uint32_t base = 0;
         if (lane == 0 && got) {
             /* publish the new active count: W {g, M, a} -> {g, M + got, a} */
-            unsigned long long w = ld_rlx64(&d->W);
-            for (;;) {
-                const unsigned long long prev = atomicCAS(&d->W, w, W_pack(W_gen(w), W_M(w) + got, W_arr(w)));
-                if (prev == w) break;
-                w = prev;
-            }
-            base = W_M(w);
+            base = add_forks(&d->W, got);
             atomicAdd(&d->forks, got);
             atomicMax(&d->max_m, base + got);
             c->M = base + got;
@@ -600,7 +502,7 @@ __device__ void coop_run(coop_dev *d, Body &&body) {
     const uint32_t phys = blockIdx.x;
     {
         /* every thread stores the same values: no divergent branch before the first barrier */
-        const unsigned long long t0 = gtimer();
+        const unsigned long long t0 = globaltimer();
         const uint32_t M0 = d->M0;
         const unsigned long long to = d->timeout_ns;
         if (threadIdx.x == 0) {
@@ -619,9 +521,9 @@ __device__ void coop_run(coop_dev *d, Body &&body) {
             const uint32_t st = c->state;
             if (threadIdx.x == 0) {
                 if (c->state == COOP_ST_ACTIVE) {          /* finished: release the pool */
-                    if (atomicExch(&d->finished, 1u) == 0u) d->t_end = gtimer();
+                    if (atomicExch(&d->finished, 1u) == 0u) d->t_end = globaltimer();
                     __threadfence();
-                    st_rel32(&d->done, 1u);
+                    st_release32(&d->done, 1u);
                 } else if (c->state == COOP_ST_KILLED) {   /* back to the worker pool */
                     __threadfence();
                     atomicOr(&d->pool[phys >> 5], 1u << (phys & 31u));
@@ -641,7 +543,7 @@ __device__ void coop_run(coop_dev *d, Body &&body) {
             for (;;) {
                 uint32_t r = 0;
                 if (lane == 0) {
-                    const uint32_t f = ld_acq32(&mb->flag);
+                    const uint32_t f = ld_acquire32(&mb->flag);
                     if (f != c->consumed) {
                         c->consumed = f;
                         c->lid = mb->lid;
@@ -649,9 +551,9 @@ __device__ void coop_run(coop_dev *d, Body &&body) {
                         c->entry = mb->entry;
                         copy_tx(c->tx, mb->tx, COOP_TX_MAX);
                         r = 1;
-                    } else if (ld_acq32(&d->done)) {
+                    } else if (ld_acquire32(&d->done)) {
                         const uint32_t bit = 1u << (phys & 31u);
-                        if (ld_rlx32(&d->err) != COOP_DEV_ERR_NONE) r = 2;
+                        if (ld_relaxed32(&d->err) != COOP_DEV_ERR_NONE) r = 2;
                         else if (atomicAnd(&d->pool[phys >> 5], ~bit) & bit) r = 2;   /* not claimed: leave */
                         /* else claimed by a forker: the assignment is on its way */
                     }
@@ -665,7 +567,7 @@ __device__ void coop_run(coop_dev *d, Body &&body) {
                 for (;;) {
                     uint32_t r = 0;
                     if (lane == 0) {
-                        if (W_gen(ld_acq64(&d->R)) == c->gen) r = 1;
+                        if (w_gen(ld_acquire64(&d->R)) == c->gen) r = 1;
                         else if (abort_check(c, spins)) r = 2;
                     }
                     r = __shfl_sync(0xffffffffu, r, 0);
@@ -673,7 +575,7 @@ __device__ void coop_run(coop_dev *d, Body &&body) {
                     if (r) break;
                 }
                 if (lane == 0 && act == 1) {
-                    c->M = W_M(ld_rlx64(&d->W));
+                    c->M = w_M(ld_relaxed64(&d->W));
                     c->state = COOP_ST_ACTIVE;
                 }
             }

@@ -170,6 +170,10 @@ SIGNATURES = {
     "coop_bfs_loop": (ctypes.c_int, [ctypes.POINTER(CooperativeCSR), _P, ctypes.c_uint32, ctypes.c_uint64, _P,
                                      ctypes.POINTER(ctypes.c_uint64), ctypes.c_uint32,
                                      ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(Opts), ctypes.POINTER(Stats)]),
+    "coop_sssp_part": (ctypes.c_int, [ctypes.POINTER(CoopPart), _P, ctypes.c_int64, _P, ctypes.POINTER(Opts),
+                                      ctypes.POINTER(Stats)]),
+    "coop_sssp_part_launch": (ctypes.c_int, [ctypes.POINTER(CoopPart), _P, ctypes.c_int64, _P, ctypes.POINTER(Opts),
+                                             ctypes.POINTER(_P)]),
     "coop_bfs_part_nccl": (ctypes.c_int, [ctypes.POINTER(CoopPart), ctypes.c_int64, _P, _P, ctypes.POINTER(Opts),
                                           ctypes.POINTER(Stats)]),
     "coop_nccl_get_unique_id": (ctypes.c_int, [_P]),
@@ -212,6 +216,8 @@ def load(path: str = LIB_PATH):
                                "(or __graft_entry__.build()); there is no CPU fallback")
         lib = ctypes.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
+            if path != LIB_PATH and not hasattr(lib, name):
+                continue        # an older build variant (tools/): only what it exports is usable
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

@@ -38,6 +38,10 @@
 #ifndef COOP_BU_CHUNK
 #define COOP_BU_CHUNK 16u     // bottom-up items per mid-interval claim (scheduler policy only)
 #endif
+#ifndef COOP_L2_HINTS
+#define COOP_L2_HINTS 1       // streaming reads (probe records, row offsets, columns of the bottom-up
+                              // scan) carry an L2 evict_first policy so the hot bitmaps stay resident
+#endif
 #ifndef COOP_SSSP_MIN_SZ
 #define COOP_SSSP_MIN_SZ 8    // SSSP: smallest worklist group per warp item (32 = fixed groups)
 #endif
@@ -69,6 +73,38 @@ __device__ __forceinline__ void reset_claims(Ctl *c, uint32_t parity) {
 #pragma unroll
     for (uint32_t r = 0; r < kClaimShards; ++r) c->claim[parity][r][0] = 0;
 }
+
+// read-only loads with an L2 eviction-priority hint (createpolicy + ld.L2::cache_hint)
+__device__ __forceinline__ unsigned long long l2_evict_first_policy() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ int32_t ld_hint(const int32_t *a, unsigned long long pol) {
+    int32_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_hint(const uint32_t *a, unsigned long long pol) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int64_t ld_hint(const int64_t *a, unsigned long long pol) {
+    int64_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_hint(const unsigned long long *a, unsigned long long pol) {
+    unsigned long long v;
+    asm volatile("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+    return v;
+}
+#if COOP_L2_HINTS
+#define LDS(ptr) ld_hint((ptr), pol_stream)
+#else
+#define LDS(ptr) __ldg(ptr)
+#endif
 
 template <typename OffT, bool KCOOP = true>
 struct BfsApp {
@@ -598,6 +634,9 @@ struct BfsApp {
                                                uint64_t &edges, uint32_t &reached, uint64_t &mfsum) {
         const uint32_t lane = threadIdx.x & 31;
         const uint32_t L1 = cs.level + 1;
+#if COOP_L2_HINTS
+        const unsigned long long pol_stream = l2_evict_first_policy();
+#endif
         const uint32_t *fcur = p.fbits[cs.level % 3];
         uint32_t *fnext = p.fbits[L1 % 3];
         const OffT *ro = static_cast<const OffT *>(p.ro);
@@ -640,8 +679,8 @@ struct BfsApp {
                 found[k] = false;
                 if (bit[k] < 32 && !p.probe) {
                     const uint64_t v = (w0 + o) * 32 + bit[k];
-                    b[k] = __ldg(ro + v);
-                    e[k] = __ldg(ro + v + 1);
+                    b[k] = LDS(ro + v);
+                    e[k] = LDS(ro + v + 1);
                 }
             }
             uint32_t deg[K];
@@ -654,8 +693,8 @@ struct BfsApp {
 #pragma unroll
                 for (int k = 0; k < K; ++k) {   // the offset is loaded alongside (coalesced, independent)
                     const uint64_t v = (w0 + own[k]) * 32 + bit[k];
-                    rec[k] = bit[k] < 32 ? __ldg(p.probe + v) : 0ull;
-                    b0[k] = bit[k] < 32 ? __ldg(ro + v) : (OffT)0;
+                    rec[k] = bit[k] < 32 ? LDS(p.probe + v) : 0ull;
+                    b0[k] = bit[k] < 32 ? LDS(ro + v) : (OffT)0;
                 }
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
@@ -691,7 +730,7 @@ struct BfsApp {
                 for (int k = 0; k < K; ++k) {
                     const bool act = b[k] < e[k] && !found[k];
 #pragma unroll
-                    for (int jj = 0; jj < EPS; ++jj) u[k][jj] = (act && b[k] + jj < e[k]) ? __ldg(col + b[k] + jj) : -1;
+                    for (int jj = 0; jj < EPS; ++jj) u[k][jj] = (act && b[k] + jj < e[k]) ? LDS(col + b[k] + jj) : -1;
                 }
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
@@ -718,7 +757,7 @@ struct BfsApp {
                     bool hit = false;
                     for (OffT x = lb; x < le; x += 32) {
                         const OffT xe = x + lane;
-                        const int32_t uu = xe < le ? __ldg(col + xe) : -1;
+                        const int32_t uu = xe < le ? LDS(col + xe) : -1;
                         const bool h = uu >= 0 && ((fcur[(uint32_t)uu >> 5] >> (uu & 31)) & 1u);
                         const uint32_t hm = __ballot_sync(FULL, h);
                         const OffT lim = min((OffT)32, (OffT)(le - x));

@@ -25,6 +25,7 @@
 #include "../../include/coop.h"
 #include "apps.cuh"
 #include "part_app.cuh"
+#include "part_sssp.cuh"
 
 using namespace coop;
 
@@ -93,6 +94,7 @@ static void *pick_block(uint32_t threads) {
 // kill/fork or chunk-claim code), the T2 baseline
 static void *select_kernel(uint32_t app, int off64, uint32_t threads, bool plain) {
     if (app == APP_PBFS) return off64 ? pick_block<PartBfsApp<int64_t>>(threads) : pick_block<PartBfsApp<uint32_t>>(threads);
+    if (app == APP_PSSSP) return off64 ? pick_block<PartSsspApp<int64_t>>(threads) : pick_block<PartSsspApp<uint32_t>>(threads);
     if (app == APP_BFS) {
         if (plain) return off64 ? pick_block<BfsApp<int64_t, false>>(threads) : pick_block<BfsApp<uint32_t, false>>(threads);
         return off64 ? pick_block<BfsApp<int64_t>>(threads) : pick_block<BfsApp<uint32_t>>(threads);
@@ -325,6 +327,7 @@ struct RunReq {
     HostChannel *host;          // handle API (device pointer of mapped host memory)
     bool async;                 // do not synchronise (handle API)
     const NcclExt *nx;          // APP_PBFS with the NCCL data plane (coop_bfs_part_nccl)
+    const uint32_t *part_w;     // APP_PSSSP: weights of the local edges
     const int64_t *sources;     // APP_BFS source loop (coop_bfs_loop): device array
     uint32_t n_src;
     uint64_t loop_ns;
@@ -417,7 +420,7 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
     kp.app = r.app;
     const uint32_t threads = o.threads_per_wg ? o.threads_per_wg : (r.app == APP_BARRIER ? 128u : 512u);
     int off64 = 0;
-    if (r.app == APP_PBFS) {
+    if (r.app == APP_PBFS || r.app == APP_PSSSP) {
         const coop_part *pt = r.part;
         if (!pt) return fail(COOP_ERR_INVALID_ARG, "part is NULL");
         if (pt->num_vertices < 1 || pt->num_vertices > (int64_t)INT32_MAX)
@@ -469,7 +472,20 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
             pp.host_ready = r.nx->host_ready;
             pp.slice_words = r.nx->slice_words;
         }
-        if (o.flags & COOP_FLAG_DIROPT) {
+        if (r.app == APP_PSSSP) {
+            if (!r.part_w && pt->num_edges > 0) return fail(COOP_ERR_INVALID_ARG, "partitioned SSSP needs weights");
+            // inbox offsets of every source rank: the uniform slices of graphgen.part_bounds
+            const uint64_t nw = ((uint64_t)pt->num_vertices + 31) / 32, sw = (nw + pt->nranks - 1) / pt->nranks;
+            for (int q = 0; q <= pt->nranks; ++q)
+                pp.qvb[q] = std::min<int64_t>(pt->num_vertices, (int64_t)(32 * sw * q));
+            pp.qvb[pt->nranks] = pt->num_vertices;
+            if (pp.qvb[pt->rank] != pt->v_begin || pp.qvb[pt->rank + 1] != pt->v_end)
+                return fail(COOP_ERR_INVALID_ARG, "partitioned SSSP needs the uniform slices of graphgen.part_bounds");
+            kp.w = r.part_w;
+            kp.dist_out = static_cast<uint32_t *>(r.out);
+            kp.level_out = nullptr;
+        }
+        if (o.flags & COOP_FLAG_DIROPT && r.app == APP_PBFS) {
             if (!pt->rows_offsets || (!pt->rows_col && pt->v_end > pt->v_begin) || pt->num_edges_global <= 0)
                 return fail(COOP_ERR_INVALID_ARG, "COOP_FLAG_DIROPT needs rows_offsets / rows_col / num_edges_global");
             pp.rro = pt->rows_offsets;
@@ -526,7 +542,7 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
     uint32_t M0 = o.init_wgs ? o.init_wgs : P;
     if (M0 < 1 || M0 > P) return fail(COOP_ERR_INVALID_ARG, "init_wgs %u not in [1, %u]", M0, P);
     if (plain) M0 = P;
-    const uint32_t bpl = r.app == APP_PBFS ? 2u : (o.barriers_per_level ? o.barriers_per_level : 1);
+    const uint32_t bpl = (r.app == APP_PBFS || r.app == APP_PSSSP) ? 2u : (o.barriers_per_level ? o.barriers_per_level : 1);
     if (bpl != 1 && bpl != 2) return fail(COOP_ERR_INVALID_ARG, "barriers_per_level must be 1 or 2");
     if (o.policy == COOP_POLICY_SCRIPTED && o.script_len && !o.script) return fail(COOP_ERR_INVALID_ARG, "script NULL");
     if (o.resize_prob < 0 || o.resize_prob > 1) return fail(COOP_ERR_INVALID_ARG, "resize_prob not in [0,1]");
@@ -551,7 +567,7 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
 
     // ---- scratch
     const uint64_t V = r.app == APP_BARRIER ? 0 : (uint64_t)kp.V;
-    const uint64_t E = (r.app == APP_BARRIER || r.app == APP_PBFS) ? 0 : (uint64_t)r.g->num_edges;
+    const uint64_t E = (r.app == APP_BARRIER || r.app == APP_PBFS || r.app == APP_PSSSP) ? 0 : (uint64_t)r.g->num_edges;
     CUDA_TRY(s->ctl.ensure(sizeof(Ctl) + sizeof(Mailbox) * kMaxCtas));   // mailboxes follow the control block
     CUDA_TRY(s->stamp.ensure(4ull * kMaxCtas));
     const uint32_t mcap = 1u << 16, lcap = 1u << 16, ecap = 4096;
@@ -588,6 +604,14 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
         const uint64_t nown = (uint64_t)(kp.part.ve - kp.part.vb);
         CUDA_TRY(s->visited.ensure(4 * ((nown + 31) / 32) + 4));
         kp.visited = static_cast<uint32_t *>(s->visited.p);
+    } else if (r.app == APP_PSSSP) {
+        const uint64_t nown = (uint64_t)(kp.part.ve - kp.part.vb);
+        CUDA_TRY(s->qlev.ensure(8 * nown + 8));
+        CUDA_TRY(s->ql0.ensure(4 * nown + 4));
+        CUDA_TRY(s->ql1.ensure(4 * nown + 4));
+        kp.dq = static_cast<unsigned long long *>(s->qlev.p);
+        kp.part.list[0] = static_cast<uint32_t *>(s->ql0.p);
+        kp.part.list[1] = static_cast<uint32_t *>(s->ql1.p);
     } else if (r.app == APP_SSSP) {
         CUDA_TRY(s->qlev.ensure(8 * V));
         CUDA_TRY(s->ql0.ensure(4 * V));
@@ -752,7 +776,7 @@ extern "C" coop_status coop_bfs_loop(const coop_csr *g, const int64_t *sources, 
     CUDA_TRY(cudaMemcpy(hs.data(), sources, 8ull * n_sources, cudaMemcpyDeviceToHost));
     for (int64_t v : hs)
         if (v < 0 || v >= g->num_vertices) return fail(COOP_ERR_INVALID_ARG, "source %lld out of range", (long long)v);
-    RunReq r = {APP_BFS, g, nullptr, hs[0], levels_out, opts, stats, 0, nullptr, false, nullptr,
+    RunReq r = {APP_BFS, g, nullptr, hs[0], levels_out, opts, stats, 0, nullptr, false, nullptr, nullptr,
                 sources, n_sources, loop_ns, run_cap};
     Prepared pr;
     Scratch *s = nullptr;
@@ -1001,6 +1025,20 @@ extern "C" coop_status coop_bfs_part_launch(const coop_part *part, int64_t sourc
                                             const coop_opts *opts, coop_handle **handle) {
     if (!handle) return fail(COOP_ERR_INVALID_ARG, "handle NULL");
     RunReq r = {APP_PBFS, nullptr, part, source, levels_owned_out, opts, nullptr, 0, nullptr, true};
+    const bool chan = opts && opts->policy == COOP_POLICY_SCHEDULER;
+    return launch_handle(r, opts, chan, handle);
+}
+
+extern "C" coop_status coop_sssp_part(const coop_part *part, const uint32_t *weights_local, int64_t source,
+                                      uint32_t *dist_owned_out, const coop_opts *opts, coop_stats *stats) {
+    RunReq r = {APP_PSSSP, nullptr, part, source, dist_owned_out, opts, stats, 0, nullptr, false, nullptr, weights_local};
+    return run_blocking(r);
+}
+
+extern "C" coop_status coop_sssp_part_launch(const coop_part *part, const uint32_t *weights_local, int64_t source,
+                                             uint32_t *dist_owned_out, const coop_opts *opts, coop_handle **handle) {
+    if (!handle) return fail(COOP_ERR_INVALID_ARG, "handle NULL");
+    RunReq r = {APP_PSSSP, nullptr, part, source, dist_owned_out, opts, nullptr, 0, nullptr, true, nullptr, weights_local};
     const bool chan = opts && opts->policy == COOP_POLICY_SCHEDULER;
     return launch_handle(r, opts, chan, handle);
 }

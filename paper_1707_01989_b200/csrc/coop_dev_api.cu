@@ -293,7 +293,7 @@ struct WsParams {
     uint32_t D, B, fixed, rounds, cap;
 };
 
-__device__ __forceinline__ unsigned long long splitmix(unsigned long long x) { return coop_detail::mix(x); }
+__device__ __forceinline__ unsigned long long splitmix(unsigned long long x) { return coop_proto::mix64(x); }
 
 __device__ __forceinline__ void q_lock(WsQueue *q) {
     while (atomicCAS(&q->lock, 0u, 1u) != 0u) __nanosleep(32);
@@ -603,7 +603,7 @@ constexpr uint32_t PN_INF = 0xFFFFFFFFu;
 
 // (splitmix64(seed ^ v), v) > (splitmix64(seed ^ u), u)
 __device__ __forceinline__ bool prio_gt(unsigned long long seed, uint32_t v, uint32_t u) {
-    const unsigned long long pv = coop_detail::mix(seed ^ v), pu = coop_detail::mix(seed ^ u);
+    const unsigned long long pv = coop_proto::mix64(seed ^ v), pu = coop_proto::mix64(seed ^ u);
     return pv > pu || (pv == pu && v > u);
 }
 

@@ -19,7 +19,7 @@ enum : uint32_t { ACT_CONT = 0, ACT_KILLED = 1, ACT_DONE = 2, ACT_ABORT = 3, ACT
 enum : uint32_t { ENTRY_START = 0, ENTRY_AFTER_RB1 = 1, ENTRY_AFTER_RB2 = 2, ENTRY_RESTART = 3 };
 // error codes written to Ctl::err (host maps to coop_status)
 enum : uint32_t { DERR_NONE = 0, DERR_TIMEOUT = 1, DERR_INVARIANT = 2, DERR_OVERFLOW = 3 };
-enum : uint32_t { APP_BFS = 0, APP_SSSP = 1, APP_BARRIER = 2, APP_PBFS = 3 };
+enum : uint32_t { APP_BFS = 0, APP_SSSP = 1, APP_BARRIER = 2, APP_PBFS = 3, APP_PSSSP = 4 };
 constexpr int kMaxRanks = 8;                         // partitioned BFS: GPUs of one NVSwitch node
 // BFS level modes (direction optimisation): top-down over the frontier queue,
 // top-down over the frontier bitmap (after a bottom-up level), bottom-up
@@ -128,6 +128,10 @@ struct __align__(128) Ctl {
     // BFS looped over sources inside one launch (coop_bfs_loop)
     uint32_t run;                      // runs completed
     uint32_t pad_l[31];
+    // partitioned SSSP: pairs per source rank in this round's inbox; own list lengths per parity
+    unsigned long long qcnt[kMaxRanks];
+    uint32_t list_n[2];
+    uint32_t pad_ps[14];
     // chunked intervals (per-warp claims): kClaimShards claim counters per level parity, one
     // 128-B line each, so claims do not serialise on a single L2 atomic address
     uint32_t claim[2][kClaimShards][32];
@@ -159,6 +163,10 @@ struct PartParams {
     const unsigned long long *cnt_recv;            // [2][nranks][4], all-gathered with the slice
     volatile uint32_t *host_ready;     // host-mapped mirror of `ready` (the host enqueues ahead)
     uint64_t slice_words;              // words per rank slice (uniform: v_begin == rank * 32 * slice_words)
+    // partitioned SSSP (part_sssp.cuh): F[q][b] are rank q's inboxes of (vertex, dist) pairs
+    // (u64[V]), source rank r's pairs at offset qvb[r]; list[b] = own improved vertices
+    int64_t qvb[kMaxRanks + 1];
+    uint32_t *list[2];
 };
 
 // Host -> GPU packet channel (host-mapped pinned memory; the paper's SVM atomics).

@@ -23,6 +23,7 @@
 #pragma once
 #include <stdint.h>
 #include "coop_internal.h"
+#include "../../include/coop_protocol.cuh"
 #include "../../include/coop.h"
 
 // Barrier implementation switches (A/B measured with tools/barrier_variants.sh;
@@ -126,48 +127,22 @@ __device__ __forceinline__ void cta_sync() {
 #endif
 
 // ---------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint64_t globaltimer() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ uint32_t ld_acquire32(const uint32_t *p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ uint32_t ld_relaxed32(const uint32_t *p) {
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release32(uint32_t *p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_release64(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void st_relaxed64(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void st_relaxed32(uint32_t *p, uint32_t v) {
-    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long atom_add_acq_rel64(unsigned long long *p, unsigned long long v) {
-    unsigned long long old;
-    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
-    return old;
-}
+// ordered accesses, the packed words and the generator: the shared protocol header
+// (include/coop_protocol.cuh, also used by the device API)
+using coop_proto::globaltimer;
+using coop_proto::ld_acquire64;
+using coop_proto::ld_acquire32;
+using coop_proto::ld_relaxed32;
+using coop_proto::ld_relaxed64;
+using coop_proto::st_release32;
+using coop_proto::st_release64;
+using coop_proto::st_relaxed64;
+using coop_proto::st_relaxed32;
+using coop_proto::atom_add_acq_rel64;
+using coop_proto::w_gen;
+using coop_proto::w_M;
+using coop_proto::w_arr;
+using coop_proto::mix64;
 __device__ __forceinline__ unsigned long long ld_acquire_sys64(const unsigned long long *p) {
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -182,9 +157,6 @@ __device__ __forceinline__ uint32_t ld_sys32(const volatile uint32_t *p) {
     return v;
 }
 
-__device__ __forceinline__ uint32_t w_gen(unsigned long long w) { return (uint32_t)(w >> 32); }
-__device__ __forceinline__ uint32_t w_M(unsigned long long w) { return (uint32_t)(w >> 16) & 0xFFFF; }
-__device__ __forceinline__ uint32_t w_arr(unsigned long long w) { return (uint32_t)w & 0xFFFF; }
 
 __device__ __forceinline__ void prefetch_l2(const void *a) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
@@ -202,12 +174,6 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
     return m;
-}
-__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finaliser (counter RNG)
-    z += 0x9E3779B97F4A7C15ull;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
 }
 // lowest `n` set bits of `w`
 __device__ __forceinline__ uint32_t lowest_bits(uint32_t w, uint32_t n) {
@@ -258,46 +224,19 @@ __device__ __forceinline__ uint32_t mhist_get(const KParams &p, uint32_t gen);
 // With `wait`, keeps trying until k are found (killed CTAs park promptly).
 __device__ __noinline__ uint32_t fork_from_pool(const KParams &p, const CtaState &cs, uint32_t gnext, uint32_t M,
                                    uint32_t k, uint32_t entry, const Transmit &tx0, bool wait) {
-    const uint32_t lane = threadIdx.x & 31;
-    Ctl *c = p.ctl;
-    const uint32_t nwords = (p.P + 31) / 32;
-    uint32_t got = 0, spins = 0;
-    while (got < k) {
-        for (uint32_t w0 = 0; w0 < nwords && got < k; w0 += 32) {
-            const uint32_t wi = w0 + lane;
-            uint32_t word = wi < nwords ? ld_relaxed32(&c->pool[wi]) : 0u;
-            uint32_t cnt = __popc(word);
-            uint32_t incl = warp_incl_scan(cnt), excl = incl - cnt;
-            uint32_t need = k - got;
-            uint32_t want = need > excl ? min(cnt, need - excl) : 0u;
-            uint32_t mask = lowest_bits(word, want);
-            uint32_t claimed = mask ? (atomicAnd(&c->pool[wi], ~mask) & mask) : 0u;
-            uint32_t nc = __popc(claimed);
-            uint32_t cincl = warp_incl_scan(nc), cexcl = cincl - nc;
-            uint32_t ctot = __shfl_sync(FULL, cincl, 31);
-            uint32_t r = 0;
-            while (claimed) {
-                uint32_t b = __ffs(claimed) - 1;
-                claimed &= claimed - 1;
-                uint32_t phys = wi * 32 + b;
-                Mailbox *mb = p.mb + phys;
-                Transmit t = tx0;
-                t.gen = gnext;
-                t.lid = M + got + cexcl + r++;
-                t.entry = entry;
-                mb->tx = t;
-                __threadfence();
-                st_release32(&mb->flag, gnext);
-            }
-            got += ctot;
-        }
-        if (!wait || got >= k) break;
-        uint32_t abort = 0;
-        if (lane == 0) abort = spin_check(p, cs, spins) ? 1u : 0u;
-        if (__shfl_sync(FULL, abort, 0)) break;
-        __nanosleep(256);
-    }
-    return got;
+    uint32_t spins = 0;
+    return coop_proto::claim_idle(p.ctl->pool, (p.P + 31) / 32, k, wait,
+        [&](uint32_t phys, uint32_t i) {                    // mailbox: id M+i, generation, WG 0's state
+            Mailbox *mb = p.mb + phys;
+            Transmit t = tx0;
+            t.gen = gnext;
+            t.lid = M + i;
+            t.entry = entry;
+            mb->tx = t;
+            __threadfence();
+            st_release32(&mb->flag, gnext);
+        },
+        [&]() { return spin_check(p, cs, spins); });
 }
 
 // ---------------------------------------------------------------- barrier
@@ -401,8 +340,7 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
         // reset the arrival word for generation g+1, then release on the separate
         // release line R (waiters poll R, arrivals hit W: no polling traffic on the
         // line the arrival atomics serialise on)
-        st_relaxed64(&c->W, pack_w(g + 1, Mp, 0));
-        st_release64(&c->R, pack_w(g + 1, Mp, 0));
+        coop_proto::publish(&c->W, &c->R, g + 1, Mp);
     }
     *out_mp = Mp;
 }
@@ -446,14 +384,14 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
                 uint32_t d = ld_relaxed32(&c->demand);
                 if (d == 0) break;
                 if (atomicCAS(&c->demand, d, d - 1) != d) continue;
-                // W: {g, M, a} -> {g, M-1, a}; retry on concurrent arrivals
-                for (;;) {
-                    unsigned long long nw = pack_w(g, Mw - 1, w_arr(old));
-                    unsigned long long prev = atomicCAS(&c->W, old, nw);
-                    if (prev == old) break;
-                    old = prev;
-                    Mw = w_M(old);
+                // W: {g, M, a} -> {g, M-1, a} (retried on concurrent arrivals)
+                uint32_t a_k = 0, M_k = 0;
+                if (!coop_proto::kill_top(&c->W, old, cs.lid, g, &a_k, &M_k)) {
+                    atomicAdd(&c->demand, 1u);                  // W moved: give the unit back, arrive
+                    break;
                 }
+                old = pack_w(g, M_k, a_k);
+                Mw = M_k;
                 killed_naive = 1;
                 atomicAdd(&c->kills, 1u);
                 uint32_t cur = c->cur_task;
@@ -472,20 +410,18 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
                 break;
             }
             if (!killed_naive) {
-                old = atom_add_acq_rel64(&c->W, 1ull);
-                last = (w_arr(old) + 1 == w_M(old)) ? 1u : 0u;
+                old = coop_proto::arrive(&c->W);
+                last = coop_proto::is_last(old) ? 1u : 0u;
             }
         } else {
             // arrive: release the CTA's writes of this interval (bar.sync + cumulative
             // release) and, for the last arriver, acquire everybody else's
 #if COOP_ARRIVE_ACQREL
-            old = atom_add_acq_rel64(&c->W, 1ull);
-            last = (w_arr(old) + 1 == w_M(old)) ? 1u : 0u;
+            old = coop_proto::arrive(&c->W);
+            last = coop_proto::is_last(old) ? 1u : 0u;
 #else
-            __threadfence();
-            old = atomicAdd(&c->W, 1ull);
-            last = (w_arr(old) + 1 == w_M(old)) ? 1u : 0u;
-            if (last) __threadfence();
+            old = coop_proto::arrive_fenced(&c->W);
+            last = coop_proto::is_last(old) ? 1u : 0u;
 #endif
         }
 #if COOP_TRACE
@@ -621,12 +557,11 @@ __device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, 
                 // and let the query barrier take the demand (waiting here would deadlock)
                 if (cs.lid != M - 1) { act = w_arr(w) ? ACT_CONT : ACT_IDLE; break; }
                 if (atomicCAS(&c->demand, d, d - 1) != d) { w = ld_relaxed64(&c->W); continue; }
-                uint32_t a;
-                for (;;) {                                               // arrivals may race the CAS
-                    a = w_arr(w);
-                    const unsigned long long prev = atomicCAS(&c->W, w, pack_w(cs.gen, M - 1, a));
-                    if (prev == w) break;
-                    w = prev;
+                uint32_t a = 0, M_k = 0;
+                if (!coop_proto::kill_top(&c->W, w, cs.lid, cs.gen, &a, &M_k)) {   // W moved: not the top now
+                    atomicAdd(&c->demand, 1u);
+                    act = ACT_CONT;
+                    break;
                 }
                 atomicAdd(&c->kills, 1u);
                 atomicAdd(&c->mid_kills, 1u);

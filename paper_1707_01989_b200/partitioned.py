@@ -258,3 +258,87 @@ def simulate_one_gpu(g, P: int, source: int, *, threads: int = 256, ctas_per_ran
     stats = [pb.wait(h, level_cap) for pb, h in zip(parts, hs)]
     levels = torch.cat([pb.levels[: pb.part.v_end - pb.part.v_begin] for pb in parts])
     return levels, stats, parts
+
+
+class PartitionedSSSP(PartitionedBFS):
+    """This rank's share of the partitioned SSSP (coop_sssp_part): the BFS layout
+    plus the local edge weights; the exchange buffers are (vertex, distance) inboxes
+    of num_vertices uint64 each (two parities), shared like the BFS bitmaps."""
+
+    def __init__(self, part, device):
+        if part.weights is None:
+            raise ValueError("partitioned SSSP needs a weighted partition")
+        self.part = part
+        self.device = torch.device(device)
+        self.exchange = "nvlink"
+        self.comm = None
+        self._own_comm = False
+        self.V = part.num_vertices
+        E = part.num_edges
+        self.bits = 32 if E < (1 << 32) else 64
+        self.ro = part.row_offsets.to(self.device, torch.int32 if self.bits == 32 else torch.int64).contiguous()
+        self.col = part.col_local.to(self.device, torch.int32).contiguous()
+        self.w = part.weights.to(self.device, torch.int32).contiguous()
+        self.rro = self.ro[:1]
+        self.rcol = self.col[:0]
+        self.E_global = None
+        self.hub_ids = torch.zeros(0, dtype=torch.int32, device=self.device)
+        self.hub_pref = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.hub_degree = 0
+        lib = _lib()
+        with torch.cuda.device(self.device):
+            self.nwb = (8 * self.V + 16 + 255) // 256 * 256
+            f = ctypes.c_void_p()
+            coop._check(lib.coop_exchange_alloc(2 * self.nwb, ctypes.byref(f)))
+            g = ctypes.c_void_p()
+            coop._check(lib.coop_exchange_alloc(32 * MAX_RANKS, ctypes.byref(g)))
+        self.F_ptr, self.flags_ptr = f.value, g.value
+        self.levels = torch.empty(max(1, part.v_end - part.v_begin), dtype=torch.int32, device=self.device)
+        self.peer_F = [[None, None] for _ in range(MAX_RANKS)]
+        self.peer_flags = [None] * MAX_RANKS
+        self._opened = []
+        self.seq = 0
+
+    def launch(self, source: int, *, seq: Optional[int] = None, **opts):
+        lib = _lib()
+        if seq is None:
+            self.seq += 1
+            seq = self.seq
+        self._s = self._struct(seq)
+        self._o, self._k = coop.make_opts(**opts)
+        h = ctypes.c_void_p()
+        coop._check(lib.coop_sssp_part_launch(ctypes.byref(self._s), self.w.data_ptr() if self.w.numel() else None,
+                                              int(source), self.levels.data_ptr(), ctypes.byref(self._o),
+                                              ctypes.byref(h)))
+        return h
+
+    def run(self, source: int, *, level_cap: int = 0, **opts):
+        lib = _lib()
+        self.seq += 1
+        s = self._struct(self.seq)
+        o, k = coop.make_opts(**opts)
+        st, bufs = coop._stats_struct(0, level_cap, 0)
+        coop._check(lib.coop_sssp_part(ctypes.byref(s), self.w.data_ptr() if self.w.numel() else None, int(source),
+                                       self.levels.data_ptr(), ctypes.byref(o), ctypes.byref(st)))
+        return self.levels, coop._to_runstats(st, bufs)
+
+
+def simulate_one_gpu_sssp(g, P: int, source: int, *, threads: int = 256, ctas_per_rank: int = 16,
+                          device="cuda", parts=None, level_cap: int = 0, **opts):
+    """P SSSP ranks on ONE GPU (test harness), as simulate_one_gpu for BFS."""
+    import graphgen as gg
+    if parts is None:
+        parts = [PartitionedSSSP(gg.partition(g, P, r), device) for r in range(P)]
+    for pb in parts:
+        pb.connect_local(parts)
+    streams = [torch.cuda.Stream(device=device) for _ in range(P)]
+    torch.cuda.synchronize(device)
+    seq = max(pb.seq for pb in parts) + 1
+    hs = []
+    for r, pb in enumerate(parts):
+        pb.seq = seq
+        hs.append(pb.launch(source, seq=seq, threads_per_wg=threads, max_wgs=ctas_per_rank, workspace=r,
+                            stream=streams[r].cuda_stream, **opts))
+    stats = [pb.wait(h, level_cap) for pb, h in zip(parts, hs)]
+    dist = torch.cat([pb.levels[: pb.part.v_end - pb.part.v_begin] for pb in parts])
+    return dist, stats, parts

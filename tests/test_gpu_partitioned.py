@@ -173,3 +173,32 @@ def test_partitioned_bfs_two_processes_ipc(part, tmp_path):
             pytest.fail("two-process partitioned BFS timed out")
     for r, o in enumerate(outs):
         assert f"RANK {r} OK" in o, o[-3000:]
+
+
+# ---------------- partitioned SSSP: (vertex, distance) exchange ----------------
+@pytest.mark.parametrize("P", [1, 2, 3, 4])
+@pytest.mark.parametrize("name", ["grid", "rmat", "disconnected"])
+def test_partitioned_sssp_matches_dijkstra(part, P, name):
+    g = {"grid": lambda: gg.grid(40, 37), "rmat": lambda: gg.rmat(12, seed=5),
+         "disconnected": lambda: gg.disjoint_union(gg.rmat(10, seed=3), gg.path(200))}[name]()
+    g = gg.with_weights(g, seed=6)
+    parts = None
+    for s in [0] + gg.sample_sources(g, 2):
+        d, stats, parts = part.simulate_one_gpu_sssp(g, P, s, parts=parts, level_cap=4096)
+        np.testing.assert_array_equal(d.cpu().numpy().view(np.uint32), tb.dijkstra(g, s))
+    for pb in parts:
+        pb.close()
+
+
+def test_partitioned_sssp_under_resizes(part):
+    from paper_1707_01989_b200 import coop
+    g = gg.with_weights(gg.grid(30, 45), seed=2)
+    parts = None
+    for seed in range(3):
+        d, stats, parts = part.simulate_one_gpu_sssp(g, 3, 7, parts=parts, ctas_per_rank=12,
+                                                     policy=coop.POLICY_RANDOM, resize_prob=0.5, seed=seed,
+                                                     flags=coop.FLAG_CHECK)
+        np.testing.assert_array_equal(d.cpu().numpy().view(np.uint32), tb.dijkstra(g, 7))
+        assert sum(st.kills + st.forks for st in stats) > 0
+    for pb in parts:
+        pb.close()
