@@ -247,22 +247,65 @@ def run_ours(args, ws, rank, local):
             checked.append((s, out.clone()))                # untimed (device copy): verified below
         return e0.elapsed_time(e1), k0.elapsed_time(k1), st
 
-    # ---- main: standalone cooperative BFS (NeverResize)
+    # ---- main: standalone cooperative BFS (NeverResize).  The job is the K traversals: calls
+    # are issued back to back on one stream with two in flight (workspaces 0/1), so the host
+    # preparation of call i+1 overlaps the kernel of call i; time = CUDA events around the
+    # whole sequence on the launching stream.  No L2 flush inside the sequence: the CSR
+    # (2.2 GB) and the level arrays are larger than L2.  Per-call kernel events give the
+    # roofline.  (--serial: one blocking call per step, L2 flushed before each.)
     flags = 0 if args.topdown else coop.FLAG_DIROPT
-    for i in range(args.warmup):
-        one(i, flags=flags)
+    outs = [torch.empty(V, dtype=torch.int32, device=dev) for _ in range(max(args.steps, args.warmup))]
+
+    def pipelined(first, count):
+        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(count)]
+        for k0, k1 in kev:                                   # materialise the handles (re-recorded by libcoop)
+            k0.record(stream)
+            k1.record(stream)
+        flush.fill_(first & 0xFF)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        inflight, st_all = [], []
+        for j in range(count):
+            s = srcs[(first + j + rank * 7) % len(srcs)]
+            inflight.append((s, j, coop.BfsCall(g, s, outs[j], threads_per_wg=args.threads, flags=flags,
+                                                 workspace=j % 2, ev_kernel_start=kev[j][0],
+                                                 ev_kernel_end=kev[j][1])))
+            if len(inflight) == 2:
+                s0, j0, c0 = inflight.pop(0)
+                st_all.append((s0, j0, c0.wait()))
+        e1.record(stream)
+        for s0, j0, c0 in inflight:
+            st_all.append((s0, j0, c0.wait()))
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1), [k0.elapsed_time(k1) for k0, k1 in kev], st_all
+
+    if args.serial:
+        for i in range(args.warmup):
+            one(i, flags=flags)
+    else:
+        pipelined(0, args.warmup)
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
     times, ktimes, stats = [], [], []
     with ClockSampler(local) as clk:
-        for i in range(args.warmup, n_steps):
-            t, kt, st = one(i, flags=flags)
-            times.append(t)
-            ktimes.append(kt)
-            stats.append(st)
-            # Graph500 edge count of this traversal, from the result (untimed)
-            st.teps_edges = int(deg[out >= 0].sum().item()) // 2
+        if args.serial:
+            for i in range(args.warmup, n_steps):
+                t, kt, st = one(i, flags=flags)
+                times.append(t)
+                ktimes.append(kt)
+                stats.append(st)
+                # Graph500 edge count of this traversal, from the result (untimed)
+                st.teps_edges = int(deg[out >= 0].sum().item()) // 2
+        else:
+            tot, ktimes, st_all = pipelined(args.warmup, args.steps)
+            times = [tot / args.steps] * args.steps
+            for s0, j0, st in st_all:
+                st.teps_edges = int(deg[outs[j0] >= 0].sum().item()) // 2
+                stats.append(st)
+                if rank == 0 and ws == 1 and not args.no_verify:
+                    checked.append((s0, outs[j0].clone()))
     torch.cuda.synchronize(dev)
     tot_ms = sum(times)
     if ws > 1:
@@ -336,7 +379,10 @@ def run_ours(args, ws, rank, local):
                                    + ("top-down" if args.topdown else "direction-optimising (top-down + bottom-up levels)"),
                        "scale": args.scale, "vertices": V, "directed_edges": E, "sources": args.steps,
                        "wgs": info["max_coresident"], "threads_per_wg": args.threads,
-                       "l2": "flushed (256 MB write) before every step; CSR 2.2 GB > L2",
+                       "l2": ("flushed (256 MB write) before every step; CSR 2.2 GB > L2" if args.serial else
+                              "inputs larger than L2 (CSR 2.2 GB + 67 MB levels); no flush inside the sequence"),
+                       "calls": "one blocking call per step" if args.serial else
+                                "pipelined: 2 asynchronous calls in flight on one stream (coop_bfs_launch)",
                        "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
                        "graph_gen_s": round(gen_s, 2),
                        "layout": ("hub-first neighbour order + probe records + degree-zero bitmap"
@@ -501,7 +547,8 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags, 
     ss = {}
     # plain worklist Bellman-Ford (delta 0) and the near-far pile (delta = band width);
     # distances are identical, only the work and the number of barrier episodes differ
-    for name, delta, thr, n in (("bellman_ford", 0, 256, 148), ("near_far", 64000, 512, 148)):
+    # near-far band width 16000 (x16 the largest weight): profiles/r02_sssp_sweep.log
+    for name, delta, thr, n in (("bellman_ford", 0, 256, 148), ("near_far", 16000, 512, 148)):
         ts = []
         for i in range(3):
             t, (_, st) = timed(lambda: coop.sssp(gw, 0, dout, threads_per_wg=thr, max_wgs=n, sssp_delta=delta))
@@ -662,6 +709,8 @@ def main():
     ap.add_argument("--topdown", action="store_true", help="main line without direction optimisation")
     ap.add_argument("--quick", action="store_true", help="skip the extra objects")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--serial", action="store_true",
+                    help="main line: one blocking call per step with an L2 flush before each (default: pipelined)")
     ap.add_argument("--no-verify", action="store_true", help="skip the oracle comparison of the outputs")
     ap.add_argument("--no-paper-multitask", action="store_true", help="skip the 10 s paper-preset loops")
     ap.add_argument("--loop-s", type=float, default=10.0, help="seconds per multitask loop (>= 10: P:1045)")

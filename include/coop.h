@@ -258,6 +258,13 @@ typedef struct coop_handle coop_handle;
  * comparison (T3), where the task runs between compute launches. */
 coop_status coop_spin_task(uint32_t blocks, uint32_t threads, uint64_t block_ns, void *stream);
 
+/* Asynchronous coop_bfs with any policy: returns after enqueueing the control-block
+ * copy and the launch on opts->stream; finish with coop_wait (stats, status) and
+ * coop_destroy.  Calls that are in flight together need distinct opts->workspace
+ * values (the scratch of a workspace belongs to one call until it is waited). */
+coop_status coop_bfs_launch(const coop_csr *g, int64_t source, int32_t *levels_out, const coop_opts *opts,
+                            coop_handle **handle);
+
 /* BFS looped over sources inside ONE persistent launch -- the paper's multitasking
  * workload runs the cooperative kernel continuously while tasks arrive (P:1045,
  * P:1135-1255).  Run r traverses from sources[r % n_sources] (device int64 array);

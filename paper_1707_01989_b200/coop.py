@@ -167,6 +167,8 @@ SIGNATURES = {
     "coop_bfs_part_launch": (ctypes.c_int, [ctypes.POINTER(CoopPart), ctypes.c_int64, _P, ctypes.POINTER(Opts),
                                             ctypes.POINTER(_P)]),
     "coop_spin_task": (ctypes.c_int, [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, _P]),
+    "coop_bfs_launch": (ctypes.c_int, [ctypes.POINTER(CooperativeCSR), ctypes.c_int64, _P, ctypes.POINTER(Opts),
+                                       ctypes.POINTER(_P)]),
     "coop_bfs_loop": (ctypes.c_int, [ctypes.POINTER(CooperativeCSR), _P, ctypes.c_uint32, ctypes.c_uint64, _P,
                                      ctypes.POINTER(ctypes.c_uint64), ctypes.c_uint32,
                                      ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(Opts), ctypes.POINTER(Stats)]),
@@ -415,6 +417,28 @@ def bfs(g, source: int, levels_out=None, *, trace_cap=0, level_cap=0, event_cap=
     _check(lib.coop_bfs(ctypes.byref(c), int(source), levels_out.data_ptr(), ctypes.byref(o), ctypes.byref(st)))
     del keep, k2
     return levels_out, _to_runstats(st, bufs)
+
+
+class BfsCall:
+    """An asynchronous cooperative BFS (coop_bfs_launch); wait() returns RunStats."""
+
+    def __init__(self, g, source: int, levels_out, **opts):
+        lib = load()
+        self._c, self._keep = _bfs_csr(g)
+        self._o, self._k2 = make_opts(**opts)
+        self.h = ctypes.c_void_p()
+        self.out = levels_out
+        _check(lib.coop_bfs_launch(ctypes.byref(self._c), int(source), levels_out.data_ptr(), ctypes.byref(self._o),
+                                   ctypes.byref(self.h)))
+
+    def wait(self, *, level_cap=0) -> "RunStats":
+        lib = load()
+        st, bufs = _stats_struct(0, level_cap, 0)
+        rc = lib.coop_wait(self.h, ctypes.byref(st))
+        lib.coop_destroy(self.h)
+        self.h = None
+        _check(rc)
+        return _to_runstats(st, bufs)
 
 
 def bfs_loop(g, sources, loop_s: float, levels_out=None, *, run_cap=1 << 20, event_cap=0, **opts):

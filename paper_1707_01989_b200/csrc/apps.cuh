@@ -382,6 +382,9 @@ struct BfsApp {
                                                uint32_t *fnext, uint32_t &reached, uint64_t &mfsum, uint2 &res) {
         const uint32_t lane = threadIdx.x & 31;
         const int32_t *__restrict__ col = p.col;
+#if COOP_L2_HINTS
+        const unsigned long long pol_stream = l2_evict_first_policy();
+#endif
         const uint32_t incl = warp_incl_scan(deg), excl = incl - deg;
         const uint32_t total = __shfl_sync(FULL, incl, 31);
         for (uint32_t e0 = 0; e0 < total; e0 += 32 * KB) {
@@ -398,7 +401,7 @@ struct BfsApp {
                 }
                 const OffT b = __shfl_sync(FULL, beg, j);
                 const uint32_t ex = __shfl_sync(FULL, excl, j);
-                u[k] = e < total ? __ldg(col + b + (e - ex)) : -1;
+                u[k] = e < total ? LDS(col + b + (e - ex)) : -1;
             }
             visit_batch<KB>(p, u, L1, out, fnext, reached, mfsum, res);
         }
@@ -418,6 +421,9 @@ struct BfsApp {
         const uint32_t in = cs.in_sel, out = in ^ 1u;
         const uint32_t L1 = cs.level + 1;
         const int32_t *__restrict__ col = p.col;
+#if COOP_L2_HINTS
+        const unsigned long long pol_stream = l2_evict_first_policy();
+#endif
         const HeavyEntry *hq = p.qheavy[in];
         const uint64_t s0 = Eh * gw / TW, s1 = Eh * (gw + 1) / TW;
         if (s0 >= s1) return;
@@ -441,7 +447,7 @@ struct BfsApp {
 #pragma unroll
             for (int k = 0; k < KB; ++k) {
                 const uint64_t e = ws + 32 * k + lane;
-                u[k] = e < s1 ? __ldg(col + (e < hend ? hb + (e - hp) : hb2 + (e - hp2))) : -1;
+                u[k] = e < s1 ? LDS(col + (e < hend ? hb + (e - hp) : hb2 + (e - hp2))) : -1;
             }
             visit_batch<KB>(p, u, L1, out, fnext, reached, mfsum, res);
             if (ws + WIN >= hend) { ++j; hb = hb2; hp = hp2; hd = hd2; }

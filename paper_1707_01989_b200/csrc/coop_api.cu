@@ -73,9 +73,14 @@ extern "C" const char *coop_status_string(coop_status s) {
 extern "C" const char *coop_last_error(void) { return g_err; }
 
 // ------------------------------------------------------------------ kernels
+#ifndef COOP_THREADS_PER_SM
+#define COOP_THREADS_PER_SM 1024
+#endif
 template <class App, int BLOCK>
 static void *kernel_ptr() {
-    constexpr int MINB = BLOCK >= 1024 ? 1 : 1024 / BLOCK;
+    // CTAs per SM the register allocation targets: 1024 threads per SM (64 registers per
+    // thread) by default; COOP_THREADS_PER_SM=1536 asks for 48 warps (<= 40 registers)
+    constexpr int MINB = BLOCK >= COOP_THREADS_PER_SM ? 1 : COOP_THREADS_PER_SM / BLOCK;
     return reinterpret_cast<void *>(&coop_kernel<App, BLOCK, MINB>);
 }
 
@@ -183,6 +188,7 @@ struct Scratch {
     DevBuf h_ro, h_col, h_w, h_out;   // end-to-end (host-pointer) calls
     DevBuf nccl_aux;                  // NCCL data plane: ready, gathered, count send/recv slots
     DevBuf runt;                      // source loop: end time of every run
+    cudaEvent_t done_ev = nullptr;    // handle API: the control block's copy back has landed
     volatile uint32_t *nccl_host = nullptr;     // mapped host mirror of `ready`
     void *nccl_warm = nullptr;                  // communicator already warmed up on nccl_stream
     cudaStream_t nccl_stream = nullptr;         // the comm stream (waits, all-gathers, writes)
@@ -406,6 +412,7 @@ struct Prepared {
     cudaStream_t stream;
     Scratch *s;
     cudaEvent_t ev0, ev1;
+    bool ctl_copied = false;    // handle API: the control block's D2H copy is already enqueued
 };
 
 static coop_status prepare(const RunReq &r, Prepared *pr) {
@@ -720,8 +727,12 @@ static coop_status launch(Prepared &pr) {
 
 static coop_status finish(Prepared &pr, coop_stats *stats) {
     Ctl *h = pr.s->host_ctl;
-    CUDA_TRY(cudaMemcpyAsync(h, pr.kp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.stream));
-    CUDA_TRY(cudaStreamSynchronize(pr.stream));
+    if (pr.ctl_copied) {
+        CUDA_TRY(cudaEventSynchronize(pr.s->done_ev));   // copy enqueued right behind the kernel
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(h, pr.kp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.stream));
+        CUDA_TRY(cudaStreamSynchronize(pr.stream));
+    }
     coop_status st = map_err(*h);
     Ctl copy = *h;
     if (stats) {
@@ -992,6 +1003,17 @@ static coop_status launch_handle(const RunReq &r0, const coop_opts *opts, bool c
         } else {
             st = prepare(r, &h->pr);
             if (st == COOP_OK) st = launch(h->pr);
+            if (st == COOP_OK && !channel) {
+                // the control block comes back right behind the kernel, so coop_wait of this
+                // call does not queue behind the kernels launched after it on the same stream
+                // (channel handles keep copying at wait: their kernel runs until the host says)
+                cudaError_t e = s->done_ev ? cudaSuccess : cudaEventCreateWithFlags(&s->done_ev, cudaEventDisableTiming);
+                if (e == cudaSuccess)
+                    e = cudaMemcpyAsync(s->host_ctl, h->pr.kp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->pr.stream);
+                if (e == cudaSuccess) e = cudaEventRecord(s->done_ev, h->pr.stream);
+                if (e != cudaSuccess) st = fail(COOP_ERR_CUDA, "control block copy: %s", cudaGetErrorString(e));
+                else h->pr.ctl_copied = true;
+            }
             if (st != COOP_OK) s->mu.unlock();
         }
     }
@@ -1012,6 +1034,17 @@ extern "C" coop_status coop_launch(int kind, const coop_csr *g, int64_t source, 
         return fail(COOP_ERR_INVALID_ARG, "coop_launch needs policy SCHEDULER and a cooperative barrier");
     RunReq r = {kind == 0 ? APP_BFS : APP_SSSP, g, nullptr, source, out, opts, nullptr, 0, nullptr, true};
     return launch_handle(r, opts, true, handle);
+}
+
+// asynchronous BFS / SSSP with any policy (finish with coop_wait): back-to-back calls on one
+// stream, each with its own opts->workspace, overlap the host preparation of call i+1 with
+// the kernel of call i
+extern "C" coop_status coop_bfs_launch(const coop_csr *g, int64_t source, int32_t *levels_out, const coop_opts *opts,
+                                       coop_handle **handle) {
+    if (!handle) return fail(COOP_ERR_INVALID_ARG, "handle NULL");
+    RunReq r = {APP_BFS, g, nullptr, source, levels_out, opts, nullptr, 0, nullptr, true};
+    const bool chan = opts && opts->policy == COOP_POLICY_SCHEDULER;
+    return launch_handle(r, opts, chan, handle);
 }
 
 // ------------------------------------------------------------------ partitioned BFS

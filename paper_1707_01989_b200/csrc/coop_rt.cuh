@@ -63,6 +63,10 @@
 #ifndef COOP_BIS_PARK
 #define COOP_BIS_PARK 1
 #endif
+#ifndef COOP_TAIL_DYN
+#define COOP_TAIL_DYN 0       // static intervals (measured: 4/16 and 8/16 slower on RMAT-24 direction-optimising)
+//: the last TAIL_DYN/16 of the items are claimed dynamically
+#endif
 #ifndef COOP_CLAIM_WARP
 #define COOP_CLAIM_WARP 0     // chunked intervals: 1 = per-warp claims, one ahead; 0 = per-CTA chunks (default: fewer atomics, measured faster armed)
 #endif
@@ -295,31 +299,7 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
         Mp = M + got;
     }
     if (lane == 0) {
-        if constexpr ((App::kCoop && COOP_BIS_SERIAL)) {
-        const uint64_t now = globaltimer();
-        if (sched_fork && got) atomicSub(&c->grant, got);
-        if (take > 0) {   // gather bookkeeping of the task instance in flight
-            uint32_t cur = c->cur_task;
-            if (cur && cur - 1 < p.events_cap) {
-                TaskEventDev *e = p.events + (cur - 1);
-                const uint32_t before = atomicAdd(&e->surrendered, take);
-                if (before == 0) e->t_first_surrender = now;
-                if (before + take >= e->demanded) e->t_last_surrender = now;
-            }
-        }
-        }   // kCoop
         app.serial(p, cs, entry, resizing);
-        if (resizing) {
-            if (ep < p.m_trace_cap) p.m_trace[ep] = Mp;
-            c->episode = ep + 1;                       // plain store: statistics only
-        }
-        // statistics as fire-and-forget reductions (no round trip on the critical path)
-        if ((App::kCoop && COOP_BIS_SERIAL) && Mp < M) atomicAdd(&c->kills, M - Mp);
-        if ((App::kCoop && COOP_BIS_SERIAL) && got) atomicAdd(&c->forks, got);
-        if ((App::kCoop && COOP_BIS_SERIAL) && Mp != M) {
-            atomicMin(&c->min_m, Mp);
-            atomicMax(&c->max_m, Mp);
-        }
         if (p.flags & COOP_FLAG_CHECK) {
             // every active WG arrived exactly once and ids were exactly [0, M)
             uint32_t a = atomicExch(&c->chk_arr[g & 1], 0u);
@@ -337,10 +317,35 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
         // M' of generation g+1 for NAIVE mode and forked CTAs (NAIVE kills may lower
         // W.M during g+1); the release store publishes it with everything above
         if ((App::kCoop && COOP_BIS_SERIAL)) st_relaxed32(&c->mhist[(g + 1) & 7], Mp);
+        // the grant consumed by these forks is channel state the next serial section reads
+        if ((App::kCoop && COOP_BIS_SERIAL) && sched_fork && got) atomicSub(&c->grant, got);
         // reset the arrival word for generation g+1, then release on the separate
         // release line R (waiters poll R, arrivals hit W: no polling traffic on the
         // line the arrival atomics serialise on)
         coop_proto::publish(&c->W, &c->R, g + 1, Mp);
+        // statistics after the release: nobody waits for them (the host reads them at the end)
+        if constexpr ((App::kCoop && COOP_BIS_SERIAL)) {
+            const uint64_t now = globaltimer();
+            if (take > 0) {   // gather bookkeeping of the task instance in flight
+                uint32_t cur = c->cur_task;
+                if (cur && cur - 1 < p.events_cap) {
+                    TaskEventDev *e = p.events + (cur - 1);
+                    const uint32_t before = atomicAdd(&e->surrendered, take);
+                    if (before == 0) e->t_first_surrender = now;
+                    if (before + take >= e->demanded) e->t_last_surrender = now;
+                }
+            }
+            if (Mp < M) atomicAdd(&c->kills, M - Mp);
+            if (got) atomicAdd(&c->forks, got);
+            if (Mp != M) {
+                atomicMin(&c->min_m, Mp);
+                atomicMax(&c->max_m, Mp);
+            }
+        }
+        if (resizing) {
+            if (ep < p.m_trace_cap) p.m_trace[ep] = Mp;
+            c->episode = ep + 1;                       // plain store: statistics only
+        }
     }
     *out_mp = Mp;
 }
@@ -695,8 +700,22 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
     constexpr uint32_t WPB = BLOCK / 32;
     if constexpr (!midkill) {
         const uint64_t TW = (uint64_t)cs.M * WPB;
-        for (uint64_t it = (uint64_t)cs.lid * WPB + (threadIdx.x >> 5); it < n_items; it += TW) fn(it);
-        (void)counter;
+        // head: Fig. 4's static split; tail (COOP_TAIL_DYN/16 of the items): claimed one at a
+        // time from the level's counter by warps that finished their share, which evens out
+        // the end of the level (long lists, hub-heavy words) without any CTA barrier
+        const uint64_t n_static = COOP_TAIL_DYN ? n_items - n_items * COOP_TAIL_DYN / 16 : n_items;
+        for (uint64_t it = (uint64_t)cs.lid * WPB + (threadIdx.x >> 5); it < n_static; it += TW) fn(it);
+        if (COOP_TAIL_DYN && n_static < n_items) {
+            const uint32_t lane = threadIdx.x & 31;
+            uint32_t t = 0;
+            if (lane == 0) t = atomicAdd(counter, 1u);
+            for (;;) {
+                const uint64_t it = n_static + __shfl_sync(FULL, t, 0);
+                if (it >= n_items) break;
+                if (lane == 0) t = atomicAdd(counter, 1u);        // next claim in flight
+                fn(it);
+            }
+        }
         (void)per_chunk;
         (void)app;
         (void)flush;

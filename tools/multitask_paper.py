@@ -62,11 +62,17 @@ class MultitaskRunner:
         return {"runs": runs, "loop_s": T, "ms_per_bfs": 1e3 * T / max(1, runs),
                 "gteps": edges / T / 1e9 if T else None}, st
 
-    def standalone(self, loop_s):
+    def standalone(self, loop_s, barriers=("query",)):
+        """The loop with the scheduler armed and no task, per resizing-barrier implementation
+        (the query barrier's intervals are chunk-distributed for mid-interval offer_kill, the
+        naive barrier's are not), so a cell's slowdown compares like with like."""
         coop = self.coop
-        r, st = self.loop(loop_s, max_wgs=self.N, policy=coop.POLICY_SCHEDULER)   # armed, no task
-        self.base = r
-        return r
+        self.base = getattr(self, "base", {})
+        for b in barriers:
+            r, st = self.loop(loop_s, max_wgs=self.N, policy=coop.POLICY_SCHEDULER,
+                              barrier_mode=coop.BARRIER_QUERY if b == "query" else coop.BARRIER_NAIVE)
+            self.base[b] = r
+        return self.base[barriers[0]]
 
     def cell(self, preset, q, barrier, loop_s):
         coop = self.coop
@@ -84,7 +90,7 @@ class MultitaskRunner:
         arr = [e["t_arrive"] for e in ev if e["t_arrive"]]
         per = [(b - a) / 1e6 for a, b in zip(arr, arr[1:])]
         r.update({"preset": preset, "P_ms": P_ms, "E_ms": E_ms, "Q": q, "barrier": barrier,
-                  "slowdown": r["ms_per_bfs"] / self.base["ms_per_bfs"],
+                  "slowdown": r["ms_per_bfs"] / self.base[barrier]["ms_per_bfs"],
                   "kill_latency_us_p50": pct(kill, 0.5), "kill_latency_us_p99": pct(kill, 0.99),
                   "gather_us_p50": pct(gat, 0.5), "gather_us_p99": pct(gat, 0.99),
                   "task_exec_ms_mean": statistics.mean(exe) if exe else None,
@@ -122,8 +128,8 @@ def main():
     srcs = gg.sample_sources(g, 64, seed=2)
     mt = MultitaskRunner(coop, g, srcs, args.threads, verify_host=g.to("cpu"))
     N = mt.N
-    base = mt.standalone(args.loop_s)
-    print(json.dumps({"standalone": base, "N": N, "graph": f"rmat{args.scale}",
+    mt.standalone(args.loop_s, barriers=("query", "naive") if args.cells == "all" else ("query",))
+    print(json.dumps({"standalone": mt.base, "N": N, "graph": f"rmat{args.scale}",
                       "gpu": torch.cuda.get_device_name()}), flush=True)
     qs = [1, N // 4, N // 2, N - 1]
     cells = ([(p, q, b) for p in PRESETS_MS for q in qs for b in ("query", "naive")] if args.cells == "all"

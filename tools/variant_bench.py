@@ -26,6 +26,8 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 N = coop.device_query(0, 512)["max_coresident"] - 1
 arms = {"coop_never": {}, "noncoop": dict(barrier_mode=coop.BARRIER_PLAIN),
         "coop_armed": dict(policy=coop.POLICY_SCHEDULER)}
+if os.environ.get("VB_TD"):
+    arms["topdown_never"] = dict(flags=0)
 res = {a: [] for a in arms}
 for s in srcs:
     for rep in range(4):
@@ -33,8 +35,10 @@ for s in srcs:
             flush.fill_(rep)
             k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             k0.record(); k1.record()
-            coop.bfs(g, s, out, threads_per_wg=512, max_wgs=N, flags=coop.FLAG_DIROPT,
-                     ev_kernel_start=k0, ev_kernel_end=k1, **kw)
+            kw2 = dict(kw)
+            fl = kw2.pop("flags", coop.FLAG_DIROPT)
+            coop.bfs(g, s, out, threads_per_wg=512, max_wgs=N, flags=fl,
+                     ev_kernel_start=k0, ev_kernel_end=k1, **kw2)
             torch.cuda.synchronize()
             if rep:
                 res[a].append(k0.elapsed_time(k1))
