@@ -531,14 +531,18 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags, 
                                  "note": "BFS looped over 64 sources inside one launch, loop_s each; task = "
                                          "E ms of work on all N workgroups every P ms, Q = N/4 demanded"}
     # barrier ns vs L2 atomic RTT (configs[3] points)
-    rtt = coop.l2_atomic_rtt(200000)
+    rtt = coop.l2_atomic_rtt(50000)             # median over 8 SMs of a relaxed 64-bit atomic chain
+    lat = coop.l2_latency_profile(20000)
     bar = {}
     for n in (148, 592, 1184):
         r = coop.barrier_bench(n, 200000, threads=128, plain=True)
         r2 = coop.barrier_bench(n, 200000, threads=128, resize_prob=1 / 64, seed=3)
         bar[str(n)] = {"plain_ns": r["ns_per_barrier"], "resizing_p1_64_ns": r2["ns_per_barrier"],
                        "kills": r2["kills"], "forks": r2["forks"]}
-    ex["barrier"] = {"l2_atomic_rtt_ns": rtt, "per_ctas": bar}
+    for n in bar:
+        bar[n]["plain_over_rtt"] = bar[n]["plain_ns"] / rtt
+    ex["barrier"] = {"l2_atomic_rtt_ns": rtt, "rtt_def": "dependent atom.relaxed.gpu.add.u64 chain, one thread, "
+                     "median over 8 SMs on both dies", "l2_latency_profile_ns": lat, "per_ctas": bar}
     # SSSP on the 2048x2048 grid (configs[1])
     gw = gg.with_weights(gg.grid(2048, 2048, device=dev), seed=1)
     gw.max_weight = 1000

@@ -243,6 +243,12 @@ coop_status coop_barrier_bench(uint32_t n_ctas, uint32_t threads, uint64_t iters
  * word; returns ns per atomic (the denominator for ns/barrier).
  */
 coop_status coop_l2_atomic_rtt(uint64_t iters, double *ns_per_atomic);
+/* The same measurement per kind and SM: one thread on each of 8 SMs spread over both
+ * dies runs a dependent chain of `iters` operations on its own line; ns_out[kind*8 + k]
+ * (kinds: 0 atom.relaxed.add.u64, 1 atom.relaxed.add.u32, 2 atom.acq_rel.add.u64,
+ * 3 ld.acquire.u64).  coop_l2_atomic_rtt reports the median of kind 0 over the SMs:
+ * the denominator of the barrier's ns / RTT ratio. */
+coop_status coop_l2_latency_profile(uint64_t iters, double *ns_out);
 
 /* Diagnostics: barrier phase breakdown of the last call on workspace 0 (only
  * filled by a library built with -DCOOP_TRACE=1; zeros otherwise): clock64

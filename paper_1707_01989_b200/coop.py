@@ -151,6 +151,7 @@ SIGNATURES = {
                                           ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
                                           ctypes.POINTER(BarrierStats)]),
     "coop_l2_atomic_rtt": (ctypes.c_int, [ctypes.c_uint64, ctypes.POINTER(ctypes.c_double)]),
+    "coop_l2_latency_profile": (ctypes.c_int, [ctypes.c_uint64, ctypes.POINTER(ctypes.c_double)]),
     "coop_debug_trace": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint64)]),
     "coop_launch": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(CooperativeCSR), ctypes.c_int64, _P,
                                    ctypes.POINTER(Opts), ctypes.POINTER(_P)]),
@@ -509,6 +510,19 @@ def barrier_bench(n_ctas: int, iters: int, *, threads=128, resize_prob=0.0, seed
                                   BARRIER_PLAIN if plain else BARRIER_QUERY, FLAG_CHECK if check else 0,
                                   ctypes.byref(out)))
     return {f: getattr(out, f) for f, _ in BarrierStats._fields_}
+
+
+def l2_latency_profile(iters: int = 20000) -> dict:
+    """ns per dependent operation, per kind, on 8 SMs (coop_l2_latency_profile)."""
+    lib = load()
+    buf = (ctypes.c_double * 32)()
+    _check(lib.coop_l2_latency_profile(iters, buf))
+    names = ["atom_relaxed_u64", "atom_relaxed_u32", "atom_acq_rel_u64", "ld_acquire_u64"]
+    out = {}
+    for k, n in enumerate(names):
+        v = sorted(x for x in buf[8 * k: 8 * k + 8] if x > 0)
+        out[n] = {"min": v[0], "median": v[len(v) // 2], "max": v[-1], "sms": len(v)} if v else None
+    return out
 
 
 def l2_atomic_rtt(iters: int = 100000) -> float:

@@ -151,13 +151,34 @@ __global__ void isolated_kernel(const OffT *ro, int64_t V, uint32_t *bits) {
     }
 }
 
-__global__ void l2_rtt_kernel(unsigned long long *word, uint64_t iters, unsigned long long *out_ns) {
-    unsigned long long v = 0;
-    const uint64_t t0 = globaltimer();
-    for (uint64_t i = 0; i < iters; ++i) v = atomicAdd(word + (v >> 63), 1ull);   // dependent chain (v < 2^63)
-    const uint64_t t1 = globaltimer();
-    out_ns[0] = t1 - t0;
-    out_ns[1] = v;
+// L2 round-trip microbenchmark (the barrier's latency denominator): one thread on each
+// of 8 SMs spread over both dies (picked by %smid, the first CTA landing on the SM) runs
+// a dependent chain of `iters` operations on its own 128-B line; kinds:
+//   0 atom.relaxed.gpu.add.u64   1 atom.relaxed.gpu.add.u32   2 atom.acq_rel.gpu.add.u64
+//   3 ld.acquire.gpu.u64
+// out_ns[kind * 8 + k] = ns per operation on the k-th chosen SM.
+__global__ void l2_rtt_kernel(unsigned long long *words, uint32_t *claimed, uint64_t iters, double *out_ns) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const uint32_t nsm = gridDim.x;
+    int k = -1;
+    for (int j = 0; j < 8; ++j)
+        if (smid == (uint32_t)j * (nsm / 8)) k = j;
+    if (k < 0 || threadIdx.x != 0 || atomicCAS(claimed + k, 0u, 1u) != 0u) return;
+    unsigned long long *w = words + 16 * k;                       // own 128-B line
+    for (int kind = 0; kind < 4; ++kind) {
+        unsigned long long v = 0;
+        const uint64_t t0 = globaltimer();
+        for (uint64_t i = 0; i < iters; ++i) {
+            unsigned long long *a = w + (v >> 63);                 // dependent address (v < 2^63)
+            if (kind == 0) v = atomicAdd(a, 1ull);
+            else if (kind == 1) v = atomicAdd(reinterpret_cast<unsigned int *>(a), 1u) & 0x7FFFFFFFu;
+            else if (kind == 2) v = coop_proto::atom_add_acq_rel64(a, 1ull);
+            else v = coop_proto::ld_acquire64(a) & 0x7FFFFFFFFFFFFFFFull;
+        }
+        const uint64_t t1 = globaltimer();
+        out_ns[kind * 8 + k] = (double)(t1 - t0) / (double)iters + (v == ~0ull ? 1.0 : 0.0);
+    }
 }
 
 // ------------------------------------------------------------------ scratch
@@ -933,18 +954,39 @@ extern "C" coop_status coop_debug_ltrace(uint64_t *out, size_t n) {
 }
 #endif
 
+static coop_status l2_profile(uint64_t iters, double *out32) {
+    unsigned long long *d = nullptr;
+    CUDA_TRY(cudaMalloc(&d, 16 * 8 * sizeof(unsigned long long) + 64 + 32 * sizeof(double)));
+    CUDA_TRY(cudaMemset(d, 0, 16 * 8 * sizeof(unsigned long long) + 64 + 32 * sizeof(double)));
+    uint32_t *claimed = reinterpret_cast<uint32_t *>(d + 16 * 8);
+    double *out = reinterpret_cast<double *>(d + 16 * 8 + 8);
+    int dev = 0, sms = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    l2_rtt_kernel<<<sms, 32>>>(d, claimed, iters, out);             // one CTA per SM
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpy(out32, out, 32 * sizeof(double), cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    return COOP_OK;
+}
+
 extern "C" coop_status coop_l2_atomic_rtt(uint64_t iters, double *ns_per_atomic) {
     if (!ns_per_atomic || iters == 0) return fail(COOP_ERR_INVALID_ARG, "bad arguments");
-    unsigned long long *d = nullptr;
-    CUDA_TRY(cudaMalloc(&d, 4 * sizeof(unsigned long long)));
-    CUDA_TRY(cudaMemset(d, 0, 4 * sizeof(unsigned long long)));
-    l2_rtt_kernel<<<1, 1>>>(d, iters, d + 2);
-    CUDA_TRY(cudaGetLastError());
-    unsigned long long h[2];
-    CUDA_TRY(cudaMemcpy(h, d + 2, sizeof h, cudaMemcpyDeviceToHost));
-    cudaFree(d);
-    *ns_per_atomic = (double)h[0] / (double)iters;
+    double t[32];
+    coop_status st = l2_profile(iters, t);
+    if (st != COOP_OK) return st;
+    std::vector<double> v;
+    for (int k = 0; k < 8; ++k)
+        if (t[k] > 0) v.push_back(t[k]);
+    if (v.empty()) return fail(COOP_ERR_CUDA, "no SM measured");
+    std::sort(v.begin(), v.end());
+    *ns_per_atomic = v[v.size() / 2];                               // median over the SMs
     return COOP_OK;
+}
+
+extern "C" coop_status coop_l2_latency_profile(uint64_t iters, double *ns_out) {
+    if (!ns_out || iters == 0) return fail(COOP_ERR_INVALID_ARG, "bad arguments");
+    return l2_profile(iters, ns_out);
 }
 
 // The competing task as a standalone (non-cooperative) kernel: `blocks` CTAs each

@@ -37,7 +37,7 @@ def test_header_declares_the_north_star_entry_points():
               "coop_nccl_comm_destroy"]:
         assert n in names
     assert "coop_bfs_loop" in names
-    assert len(names) == 49
+    assert len(names) == 50
 
 
 def test_library_exports_every_declared_symbol(lib_path):
