@@ -117,6 +117,23 @@ static void *select_kernel(uint32_t app, int off64, uint32_t threads, bool plain
     return nullptr;
 }
 
+// control block + mailboxes of one call: zero, then the generation-0 words and the pool
+__global__ void ctl_init_kernel(Ctl *c, uint32_t P, uint32_t M0) {
+    unsigned long long *w = reinterpret_cast<unsigned long long *>(c);
+    const uint32_t n = (uint32_t)((sizeof(Ctl) + sizeof(Mailbox) * P) / 8);   // mailboxes follow the block
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) w[i] = 0ull;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        c->W = pack_w(0, M0, 0);
+        c->R = pack_w(0, M0, 0);
+        c->mhist[0] = M0;
+        c->min_m = M0;
+        c->max_m = M0;
+        c->task_next = 0xFFFFFFFFu;
+    }
+    for (uint32_t b = M0 + threadIdx.x; b < P; b += blockDim.x) atomicOr(&c->pool[b >> 5], 1u << (b & 31));
+}
+
 __global__ void max_u32_kernel(const uint32_t *w, int64_t n, uint32_t *out) {
     uint32_t m = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -214,7 +231,8 @@ struct Scratch {
     void *nccl_warm = nullptr;                  // communicator already warmed up on nccl_stream
     cudaStream_t nccl_stream = nullptr;         // the comm stream (waits, all-gathers, writes)
     cudaEvent_t nccl_ev = nullptr;
-    Ctl *host_ctl = nullptr;          // pinned staging
+    Ctl *host_ctl = nullptr;          // pinned, host-mapped: the kernel's last CTA mirrors the control block here
+    Ctl *host_ctl_dev = nullptr;      // its device pointer
     std::mutex mu;
 };
 
@@ -235,8 +253,10 @@ static coop_status get_scratch(Scratch **out, uint32_t ws) {
             if (!g_scratch[dev][k].host_ctl) {
                 // control block + zeroed mailboxes: one pinned staging buffer, one H2D copy per call
                 const size_t bytes = sizeof(Ctl) + sizeof(Mailbox) * kMaxCtas;
-                CUDA_TRY(cudaHostAlloc((void **)&g_scratch[dev][k].host_ctl, bytes, cudaHostAllocDefault));
+                CUDA_TRY(cudaHostAlloc((void **)&g_scratch[dev][k].host_ctl, bytes, cudaHostAllocMapped));
                 memset((void *)g_scratch[dev][k].host_ctl, 0, bytes);
+                CUDA_TRY(cudaHostGetDevicePointer((void **)&g_scratch[dev][k].host_ctl_dev,
+                                                  (void *)g_scratch[dev][k].host_ctl, 0));
             }
     }
     s->device = dev;
@@ -378,13 +398,17 @@ static coop_status fill_stats(const Ctl &c, const KParams &kp, coop_stats *st, c
     st->tasks_completed = c.tasks_completed;
     st->bottom_up_levels = c.n_bu_levels;
     st->mid_kills = c.mid_kills;
+    bool pending = false;   // async copies to wait for (only then: a pipelined caller's next
+                            // kernel may already be queued on this stream)
     if (st->m_trace && st->m_trace_cap) {
         uint32_t n = std::min(st->m_trace_cap, std::min(c.episode, kp.m_trace_cap));
         if (n) CUDA_TRY(cudaMemcpyAsync(st->m_trace, kp.m_trace, n * 4, cudaMemcpyDeviceToHost, stream));
+        pending |= n != 0;
     }
     if (st->level_sizes && st->level_sizes_cap) {
         uint32_t n = std::min(st->level_sizes_cap, std::min(c.levels + 1, kp.level_cap));
         if (n) CUDA_TRY(cudaMemcpyAsync(st->level_sizes, kp.level_sizes, n * 4, cudaMemcpyDeviceToHost, stream));
+        pending |= n != 0;
     }
     if (st->level_end_ns && st->level_end_ns_cap) {
         uint32_t n = std::min(st->level_end_ns_cap, std::min(c.levels, kp.level_cap));
@@ -412,7 +436,7 @@ static coop_status fill_stats(const Ctl &c, const KParams &kp, coop_stats *st, c
             st->task_events[i].surrendered = tmp[i].surrendered;
         }
     }
-    CUDA_TRY(cudaStreamSynchronize(stream));
+    if (pending) CUDA_TRY(cudaStreamSynchronize(stream));
     return COOP_OK;
 }
 
@@ -704,18 +728,11 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
     }
 
     // ---- control block
-    Ctl *h = s->host_ctl;
-    memset(h, 0, sizeof(Ctl));
-    h->W = pack_w(0, M0, 0);
-    h->R = pack_w(0, M0, 0);
-    h->mhist[0] = M0;
-    h->min_m = M0;
-    h->max_m = M0;
-    h->task_next = 0xFFFFFFFFu;
-    for (uint32_t b = M0; b < P; ++b) h->pool[b >> 5] |= 1u << (b & 31);
-    // one copy: the control block and the P mailboxes behind it (the staging buffer's mailbox
-    // part is zero and never written on the host)
-    CUDA_TRY(cudaMemcpyAsync(kp.ctl, h, sizeof(Ctl) + sizeof(Mailbox) * P, cudaMemcpyHostToDevice, stream));
+    // the control block and the P mailboxes behind it, initialised on the device (no
+    // host-to-device copy per call); the kernel's last CTA mirrors the block back
+    kp.ctl_mirror = s->host_ctl_dev;
+    ctl_init_kernel<<<1, 512, 0, stream>>>(kp.ctl, P, M0);
+    CUDA_TRY(cudaGetLastError());
     if (sched) CUDA_TRY(cudaMemsetAsync(kp.events, 0, sizeof(TaskEventDev) * ecap, stream));
     pr->kp = kp;
     pr->kern = kern;
@@ -747,13 +764,9 @@ static coop_status launch(Prepared &pr) {
 }
 
 static coop_status finish(Prepared &pr, coop_stats *stats) {
-    Ctl *h = pr.s->host_ctl;
-    if (pr.ctl_copied) {
-        CUDA_TRY(cudaEventSynchronize(pr.s->done_ev));   // copy enqueued right behind the kernel
-    } else {
-        CUDA_TRY(cudaMemcpyAsync(h, pr.kp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.stream));
-        CUDA_TRY(cudaStreamSynchronize(pr.stream));
-    }
+    Ctl *h = pr.s->host_ctl;          // mirrored by the kernel's last CTA (mapped memory)
+    if (pr.ctl_copied) CUDA_TRY(cudaEventSynchronize(pr.s->done_ev));   // recorded right behind the kernel
+    else CUDA_TRY(cudaStreamSynchronize(pr.stream));
     coop_status st = map_err(*h);
     Ctl copy = *h;
     if (stats) {
@@ -1050,8 +1063,6 @@ static coop_status launch_handle(const RunReq &r0, const coop_opts *opts, bool c
                 // call does not queue behind the kernels launched after it on the same stream
                 // (channel handles keep copying at wait: their kernel runs until the host says)
                 cudaError_t e = s->done_ev ? cudaSuccess : cudaEventCreateWithFlags(&s->done_ev, cudaEventDisableTiming);
-                if (e == cudaSuccess)
-                    e = cudaMemcpyAsync(s->host_ctl, h->pr.kp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->pr.stream);
                 if (e == cudaSuccess) e = cudaEventRecord(s->done_ev, h->pr.stream);
                 if (e != cudaSuccess) st = fail(COOP_ERR_CUDA, "control block copy: %s", cudaGetErrorString(e));
                 else h->pr.ctl_copied = true;

@@ -131,7 +131,8 @@ struct __align__(128) Ctl {
     // partitioned SSSP: pairs per source rank in this round's inbox; own list lengths per parity
     unsigned long long qcnt[kMaxRanks];
     uint32_t list_n[2];
-    uint32_t pad_ps[14];
+    uint32_t exits;                    // CTAs that left the kernel (the last one mirrors this block to the host)
+    uint32_t pad_ps[13];
     // chunked intervals (per-warp claims): kClaimShards claim counters per level parity, one
     // 128-B line each, so claims do not serialise on a single L2 atomic address
     uint32_t claim[2][kClaimShards][32];
@@ -235,6 +236,9 @@ struct KParams {
     const int64_t *sources; uint32_t n_src;
     uint64_t loop_ns;
     unsigned long long *run_t; uint32_t run_cap;   // globaltimer at the end of each run
+    // host-mapped copy of the control block, written by the last CTA to leave the kernel
+    // (the call's status and statistics reach the host without a copy-back operation)
+    Ctl *ctl_mirror;
     // periodic task generator
     uint32_t task_wgs, task_blocks, task_max;
     uint64_t task_block_ns, task_period_ns, task_first_ns;

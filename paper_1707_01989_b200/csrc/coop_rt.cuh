@@ -830,6 +830,7 @@ __device__ COOP_RUNBODY_ATTR uint32_t run_body(const KParams &p, CtaState &cs, A
         }
         skip_to_rb1 = false;
         app.template between<BLOCK>(p, cs);                   // CTA work between Fig. 4's two barriers
+        cta_sync();                                           // every warp has read the barrier's result
         if (threadIdx.x == 0) cs.level += 1;                  // reset(out_nodes) done in serial; level++
         if (p.bpl == 2) {
             r = barrier(p, cs, app, true, ENTRY_AFTER_RB2);   // resizing_global_barrier() #2
@@ -1032,10 +1033,8 @@ __device__ __noinline__ void park_loop(const KParams &p, CtaState &cs, App &app)
 }
 
 // ---------------------------------------------------------------- kernel
-template <class App, int BLOCK, int MINB>
-__global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(KParams p) {
-    __shared__ CtaState cs;
-    App app;
+template <class App, int BLOCK>
+__device__ __forceinline__ void kernel_body(const KParams &p, CtaState &cs, App &app) {
     if (threadIdx.x == 0) {
         const uint64_t t0 = globaltimer();
 #if COOP_TRACE
@@ -1076,6 +1075,32 @@ __global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(KParams p) {
     if (threadIdx.x == 0 && blockIdx.x == 0)
         for (int i = 0; i < 12; ++i) p.ctl->trace[i + (i >= 6 ? 2 : 0)] = cs.tr[i];
 #endif
+}
+
+
+template <class App, int BLOCK, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(KParams p) {
+    __shared__ CtaState cs;
+    __shared__ uint32_t s_last;
+    App app;
+    kernel_body<App, BLOCK>(p, cs, app);
+    // epilogue: the last CTA out mirrors the control block into host-mapped memory, so the
+    // host reads status and statistics without a device-to-host copy operation per call
+    if (p.ctl_mirror) {
+        cta_sync();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last = atomicAdd(&p.ctl->exits, 1u) + 1u == gridDim.x ? 1u : 0u;
+            if (s_last) __threadfence();
+        }
+        cta_sync();
+        if (s_last) {
+            const unsigned long long *src = reinterpret_cast<const unsigned long long *>(p.ctl);
+            unsigned long long *dst = reinterpret_cast<unsigned long long *>(p.ctl_mirror);
+            for (uint32_t i = threadIdx.x; i < sizeof(Ctl) / 8; i += BLOCK) dst[i] = __ldcg(src + i);
+            __threadfence_system();
+        }
+    }
 }
 
 }  // namespace coop

@@ -27,20 +27,34 @@ srcs = gg.sample_sources(g, 16, seed=2)
 outs = [torch.empty(g.num_vertices, dtype=torch.int32, device="cuda") for _ in range(args.calls)]
 
 
+import time  # noqa: E402
+host = []
+
+
 def run():
     inflight = []
+    t00 = time.perf_counter()
     for j in range(args.calls):
+        a = time.perf_counter()
         inflight.append(coop.BfsCall(g, srcs[j], outs[j], threads_per_wg=512, flags=coop.FLAG_DIROPT, workspace=j % 2))
+        b = time.perf_counter()
+        host.append((f"launch {j}", (a - t00) * 1e6, (b - a) * 1e6))
         if len(inflight) == 2:
+            a = time.perf_counter()
             inflight.pop(0).wait()
+            b = time.perf_counter()
+            host.append((f"wait {j - 1}", (a - t00) * 1e6, (b - a) * 1e6))
     for c in inflight:
         c.wait()
     torch.cuda.synchronize()
 
 
 run()
+host.clear()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     run()
+for name, start, dur in host:
+    print(f"host {name:10s} at {start:9.1f} us  took {dur:8.1f} us")
 path = "/tmp/call_gap_trace.json"
 prof.export_chrome_trace(path)
 ev = json.load(open(path))["traceEvents"]
