@@ -6,11 +6,13 @@
 A step = one cooperative BFS (the whole hot path of SURVEY §8(a): persistent
 launch, init, per-level expand/claim/compact, resizing barriers, termination)
 from one source of RMAT-24 (Graph500 parameters, seed 1), inputs
-resident in HBM.  Sources are distinct degree>0 vertices (seed 2).  The CSR
-(2.2 GB) is larger than the 126 MB L2 and L2 is additionally flushed (256 MB
-write) before every timed step.  Time: CUDA events on the launching stream
-around each call; value = GTEPS (Graph500 convention: undirected edges of the
-reached component / time).  Extra objects report the multitasked run (periodic
+resident in HBM.  Sources are distinct degree>0 vertices (seed 2).  The job is
+the K traversals, issued as asynchronous calls (coop_bfs_launch) on one stream
+with two in flight; time = CUDA events around the whole sequence on the
+launching stream (--serial: one blocking call per step, each bracketed by
+events, L2 flushed before each).  The CSR (2.2 GB) is larger than the 126 MB
+L2.  value = GTEPS (Graph500 convention: undirected edges of the reached
+component / time); every timed output is compared with the oracle.  Extra objects report the multitasked run (periodic
 competing task), the non-cooperative persistent baseline, ns per barrier vs the
 L2 atomic round trip, and SSSP on the 2048x2048 grid (configs[1]).
 
@@ -18,7 +20,8 @@ L2 atomic round trip, and SSSP on the 2048x2048 grid (configs[1]).
 workload: the base contract's reference arm for this tier.
 Under torchrun (N>1): the 1-D vertex-partitioned BFS (configs[4]),
 weak scaling with 2^24 vertices per GPU, frontier exchanged inside the kernel
-over NVLink peer memory; time = max over ranks, rank 0 prints.
+over NVLink peer memory (--exchange nccl: per-level ncclAllGather); time = max
+over ranks, rank 0 prints.
 """
 from __future__ import annotations
 

@@ -42,6 +42,9 @@
 #define COOP_L2_HINTS 1       // streaming reads (probe records, row offsets, columns of the bottom-up
                               // scan) carry an L2 evict_first policy so the hot bitmaps stay resident
 #endif
+#ifndef COOP_TD_TAIL
+#define COOP_TD_TAIL 8        // top-down levels: the last TD_TAIL/16 of the items are claimed dynamically
+#endif
 #ifndef COOP_SSSP_MIN_SZ
 #define COOP_SSSP_MIN_SZ 8    // SSSP: smallest worklist group per warp item (32 = fixed groups)
 #endif
@@ -875,7 +878,7 @@ struct BfsApp {
         } else if (mode == BFS_TDB) {                         // item = 32 frontier words
             r = claim_items<BLOCK, MID>(p, cs, *this, &p.ctl->claim[in][0][0], (nw + 31) / 32, 4u * WPB, [&](uint64_t g) {
                 tdb_group(p, cs, g, fnext, edges, reached, mfsum, res);
-            }, flush);
+            }, flush, COOP_TD_TAIL);
         } else {                                              // item = 32 light frontier entries
             expand_heavy(p, cs, gw, TW, fnext, edges, reached, mfsum, res);
             LTRACE(5);
@@ -886,7 +889,8 @@ struct BfsApp {
             uint32_t sz = 32;
             while (sz > 1 && (nl + sz - 1) / sz < TW) sz >>= 1;
             r = claim_items<BLOCK, MID>(p, cs, *this, &p.ctl->claim[in][0][0], (nl + sz - 1) / sz, 4u * WPB,
-                            [&](uint64_t g) { tdq_group(p, cs, g, sz, fnext, edges, reached, mfsum, res); }, flush);
+                            [&](uint64_t g) { tdq_group(p, cs, g, sz, fnext, edges, reached, mfsum, res); }, flush,
+                            COOP_TD_TAIL);
         }
         LTRACE(6);
         if (r == ACT_CONT) flush();

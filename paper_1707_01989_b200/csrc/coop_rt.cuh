@@ -695,7 +695,7 @@ __device__ uint32_t claim_items_cta(const KParams &p, CtaState &cs, App &app, ui
 //          (two CTA barriers per chunk).
 template <int BLOCK, bool MID, class App, class Fn, class Flush>
 __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32_t *counter, uint64_t n_items,
-                                uint32_t per_chunk, Fn &&fn, Flush &&flush) {
+                                uint32_t per_chunk, Fn &&fn, Flush &&flush, uint32_t tail16 = COOP_TAIL_DYN) {
     constexpr bool midkill = MID && App::kCoop && COOP_BIS_CLAIM;
     constexpr uint32_t WPB = BLOCK / 32;
     if constexpr (!midkill) {
@@ -703,9 +703,9 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
         // head: Fig. 4's static split; tail (COOP_TAIL_DYN/16 of the items): claimed one at a
         // time from the level's counter by warps that finished their share, which evens out
         // the end of the level (long lists, hub-heavy words) without any CTA barrier
-        const uint64_t n_static = COOP_TAIL_DYN ? n_items - n_items * COOP_TAIL_DYN / 16 : n_items;
+        const uint64_t n_static = tail16 ? n_items - n_items * tail16 / 16 : n_items;
         for (uint64_t it = (uint64_t)cs.lid * WPB + (threadIdx.x >> 5); it < n_static; it += TW) fn(it);
-        if (COOP_TAIL_DYN && n_static < n_items) {
+        if (tail16 && n_static < n_items) {
             const uint32_t lane = threadIdx.x & 31;
             uint32_t t = 0;
             if (lane == 0) t = atomicAdd(counter, 1u);

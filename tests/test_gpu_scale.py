@@ -166,3 +166,25 @@ def test_bfs_source_loop_inside_one_launch(coop, mode):
     assert np.all(np.diff(t_end) > 0) and t_end[-1] >= 0.3
     if mode != "standalone":
         assert st.kills > 0 and st.forks > 0 and st.tasks_completed > 0
+
+
+def test_pipelined_async_bfs_calls(coop, rmat20):
+    """bench.py's main-line form: asynchronous coop_bfs_launch calls, two in flight on one
+    stream (workspaces 0/1), the control block initialised on the device and mirrored back by
+    the kernel's last CTA; every output exact and the statistics belong to their own call."""
+    g, gh = rmat20
+    srcs = gg.sample_sources(gh, 6, seed=9)
+    outs = [torch.empty(g.num_vertices, dtype=torch.int32, device="cuda") for _ in srcs]
+    inflight, done = [], []
+    for j, s in enumerate(srcs):
+        inflight.append((j, coop.BfsCall(g, s, outs[j], threads_per_wg=512, flags=coop.FLAG_DIROPT, workspace=j % 2)))
+        if len(inflight) == 2:
+            j0, c0 = inflight.pop(0)
+            done.append((j0, c0.wait()))
+    for j0, c0 in inflight:
+        done.append((j0, c0.wait()))
+    deg = np.diff(gh.row_offsets.numpy())
+    for j, st in done:
+        ref = tb.bfs(gh, srcs[j])
+        np.testing.assert_array_equal(outs[j].cpu().numpy(), ref)
+        assert st.reached == int((ref >= 0).sum()) and st.kernel_ns > 0
