@@ -145,7 +145,10 @@ typedef struct {
     uint32_t threads_per_wg;
     uint32_t tasks_posted, tasks_completed;
     uint32_t bottom_up_levels;  /* COOP_FLAG_DIROPT: levels run bottom-up */
-    uint32_t mid_kills;         /* workgroups that left at a chunk boundary inside an interval (offer_kill) */
+    uint32_t mid_kills;         /* workgroups that left inside an interval (offer_kill between items) */
+    uint32_t handbacks;         /* of those, workgroups that handed static items back to the survivors */
+    uint32_t replays;           /* replay intervals run (the survivors ran handed-back items) */
+    uint32_t reserved0;
     uint32_t *m_trace;          /* optional caller-owned HOST buffer: M after each resizing episode */
     uint32_t m_trace_cap;
     uint32_t *level_sizes;      /* optional caller-owned HOST buffer: frontier size per level */

@@ -8,7 +8,9 @@
  * Words:
  *   W = {gen:32 | M:16 | arrived:16}  arrival word; arrivals are atomic adds, the
  *                                     CTA completing arrived == M is the last arriver
- *   R = {gen:32 | M':16 | 0}          release word on its own 128-B line; waiters poll it
+ *   R = {gen:32 | M':16 | flags:16}   release word on its own 128-B line; waiters poll it
+ *                                     (flags, bit 0: a replay interval of handed-back work
+ *                                     follows before the level ends -- BFS/SSSP runtime)
  * Steps (each a single atomic or ordered access, as modelled):
  *   arrive        atom.add.acq_rel W += 1          (release this CTA's interval, and for
  *                                                    the last arriver acquire everyone's)
@@ -104,10 +106,11 @@ __device__ __forceinline__ unsigned long long arrive_fenced(unsigned long long *
 }
 
 // publish (last arriver, or the leaver completing the episode): reset arrivals for
-// generation g+1, then release every waiter
-__device__ __forceinline__ void publish(unsigned long long *W, unsigned long long *R, uint32_t g1, uint32_t Mp) {
+// generation g+1, then release every waiter (flags ride in R's low half-word)
+__device__ __forceinline__ void publish(unsigned long long *W, unsigned long long *R, uint32_t g1, uint32_t Mp,
+                                        uint32_t flags = 0u) {
     st_relaxed64(W, pack_w(g1, Mp, 0u));
-    st_release64(R, pack_w(g1, Mp, 0u));
+    st_release64(R, pack_w(g1, Mp, flags));
 }
 
 // a waiter's fate once R moved on from generation g

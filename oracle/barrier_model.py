@@ -6,8 +6,9 @@ barrier/fork/barrier/kill/barrier form of the Resizing-Barrier rule
 (PAPER.md:1573-1585); they collapse it into one episode on a packed word, in
 the spirit of the paper's efficient "query" barrier, and
 add kills outside the serial section (the naive barrier's arrival kill,
-PAPER.md:918-934; offer_kill at chunk boundaries inside an interval and the
-device API's bare offer_kill / request_fork).  The protocol is
+PAPER.md:918-934; offer_kill between the items of an interval with the rest of the
+leaver's static share handed back to the survivors, and the device API's bare
+offer_kill / request_fork).  The protocol is
 specified in DESIGN.md §4 and modelled here, independently of the CUDA source,
 at the granularity of single atomic operations by thread 0 of each CTA:
 
@@ -20,11 +21,18 @@ at the granularity of single atomic operations by thread 0 of each CTA:
                demand > 0: CAS demand d -> d-1, then CAS W {g,M,a} -> {g,M-1,a}
                (retrying on concurrent arrivals); the leaver completes the
                episode on the waiters' behalf iff a == M-1
-  mid kill     (chunk-counter intervals) a CTA whose claim saw
-               id + demand >= W.M finishes its chunk, then loops: read W, read
-               demand; give up if demand == 0 or id + demand < M or the
-               generation moved; if id != M-1: resume claiming once any CTA
-               arrived, else spin; if id == M-1: CAS demand, CAS W as above
+  mid kill     (static items + hand-back) every member runs its static items
+               (id, 0..K-1) of the level; after each item it reads demand d
+               and W.M and stops when id + d >= W.M (id != 0); then loops:
+               read W, read demand; resume if demand == 0 or id + demand < M
+               or the generation moved; if id != M-1: resume for the rest of
+               the interval (no more offers) once any CTA arrived, else spin;
+               if id == M-1: CAS demand, hand back the items not yet run,
+               kill-CAS W as above (on failure: withdraw them, return the
+               demand unit, resume)
+  replay       a serial section that finds handed-back items releases into a
+               replay interval of the same level (no policy, M' = M, R flag):
+               item i of the handed-back list runs on member i mod M
   bare kill    (device API) id == W.M-1 > 0: take one demand unit (SCHEDULER)
                or accept (RANDOM), CAS W {g,M,a} -> {g,M-1,a} unless M or gen
                moved; completes the episode iff a == M-1
@@ -58,9 +66,9 @@ properties checked on every transition:
                         P:622-624)
   P5 liveness        -- from every reachable state some continuation ends with
                         every CTA exited (no deadlock, no livelock)
-  P6 work coverage   -- with chunked intervals, every chunk of interval g is
-                        processed before barrier g releases (a CTA leaves only
-                        between chunks)
+  P6 work coverage   -- with static items and hand-back, every item of a level
+                        runs exactly once before the barrier that ends the level
+                        releases (a leaver's unrun items run in replay intervals)
 
 ``bugs`` injects known-wrong protocol variants so the tests can show each
 property is not vacuous; see :data:`BUGS`.
@@ -74,9 +82,9 @@ from dataclasses import dataclass, field, replace
 IDLE, CLAIMED, ASSIGNED, ACTIVE, TASK = "I", "C", "A", "X", "T"
 
 # CTA program counters
-(PARKED, IN_TASK, WAIT_GEN, WORK, CLAIM, PROC, OFFER, OFFER_D, OFFER_CASD, OFFER_CASW,
- ARRIVE, NV_D, NV_CASD, NV_CASW, SPIN, SER_POLICY, SER_CASD, SER_FORK, SER_RESET, SER_RELEASE,
- BK_R, BK_CASD, BK_CASW, BF_R, BF_CLAIM, BF_CASW, BF_ASSIGN, KILLED, EXITED) = range(29)
+(PARKED, IN_TASK, WAIT_GEN, WORK, HB_ITEM, HB_POLL, HB_POLLW, OFFER, OFFER_D, OFFER_CASD, DONATE,
+ OFFER_CASW, WITHDRAW, REPLAY_RUN, ARRIVE, NV_D, NV_CASD, NV_CASW, SPIN, SER_POLICY, SER_CASD, SER_FORK,
+ SER_RESET, SER_RELEASE, BK_R, BK_CASD, BK_CASW, BF_R, BF_CLAIM, BF_CASW, BF_ASSIGN, KILLED, EXITED) = range(33)
 
 BUGS = {
     "kill_by_M_only": "a waiter decides its fate from R.M alone, ignoring that R may be a later generation",
@@ -85,7 +93,10 @@ BUGS = {
                             "CTAs arrived (the rule before commit 2f99910)",
     "no_cap_on_behalf": "a leaver completing the episode forks up to N under a waiting policy although it is "
                         "not parked yet (ADVICE round 1, include/coop_device.cuh)",
-    "kill_with_chunk": "mid-interval: a CTA offers itself before finishing the chunk in hand",
+    "handback_skips_item": "mid-interval: the leaver hands back from the item after the one in hand, "
+                           "which it never finished",
+    "kill_without_handback": "mid-interval: the leaver leaves without handing its unrun items back",
+    "no_replay": "the serial section ignores handed-back items and ends the level",
     "kill_any_top": "kill-CAS writes M-1 from a stale M after a concurrent fork moved W.M",
 }
 
@@ -102,7 +113,8 @@ class Cfg:
     policy: str = "scripted"        # scripted | random | scheduler
     targets: tuple = ()             # scripted: M' per episode (0/absent = unchanged)
     barrier: str = "query"          # query | naive (scheduler policy)
-    chunks: int = 0                 # 0: static split; C: chunk counter + mid-interval offer_kill
+    items: int = 0                  # 0: an interval's work is one step; K: K static items per member
+                                    # with mid-interval offer_kill and hand-back (scheduler + query)
     bare: int = 0                   # device API: budget of bare offer_kill/request_fork calls per run
     demand: int = 0                 # host demand units (posted at nondeterministic times)
     withdraw: int = 0               # host withdrawals of outstanding demand
@@ -124,10 +136,13 @@ class Gen:
     cur: frozenset                  # current members: start ids + bare forks - kill-CAS leavers
     todo: frozenset                 # members that have not started their work of the interval
     arrived: frozenset = frozenset()
-    claimed: int = 0                # chunk counter
-    done: int = 0                   # chunks processed
     released: bool = False
     mprime: int = -1                # M' published at the release
+    level: int = 0                  # the level this interval belongs to (replay intervals repeat it)
+    items: frozenset = frozenset()  # hand-back mode: the level's items (owner id, k)
+    done: frozenset = frozenset()   #   items of the level run so far
+    donated: frozenset = frozenset()  # items handed back in this interval (withdrawn ones removed)
+    replay: tuple = ()              # a replay interval: the handed-back items it runs, in order
 
 
 @dataclass(frozen=True)
@@ -149,8 +164,13 @@ def _initial(cfg: Cfg) -> S:
     P, M0 = cfg.P, cfg.M0
     ctas = tuple(Cta(WORK, p, 0) if p < M0 else Cta(PARKED) for p in range(P))
     slots = tuple(ACTIVE if p < M0 else IDLE for p in range(P))
-    return S((0, M0, 0), (0, M0), 0, 0, (cfg.demand, cfg.withdraw, cfg.grant, cfg.bare), False, -1,
-             slots, (None,) * P, ctas, (Gen(frozenset(range(M0)), frozenset(range(M0)), released=True, mprime=M0),))
+    return S((0, M0, 0), (0, M0, 0), 0, 0, (cfg.demand, cfg.withdraw, cfg.grant, cfg.bare), False, -1,
+             slots, (None,) * P, ctas, (Gen(frozenset(range(M0)), frozenset(range(M0)), released=True, mprime=M0,
+                                            items=_level_items(cfg, M0)),))
+
+
+def _level_items(cfg: Cfg, M: int) -> frozenset:
+    return frozenset((i, k) for i in range(M) for k in range(cfg.items))
 
 
 def _set(t, i, v):
@@ -203,7 +223,7 @@ def _successors(s: S, cfg: Cfg):
             put(Cta(PARKED), slots=_set(s.slots, p, IDLE))
         elif c.pc == WAIT_GEN:
             if s.R[0] == g:
-                if g >= E:                  # forked at the final barrier
+                if s.hist[g].level >= E:    # forked at the final barrier
                     put(Cta(EXITED), slots=_set(s.slots, p, IDLE))
                 else:
                     put(Cta(WORK, c.lid, g))
@@ -220,63 +240,89 @@ def _successors(s: S, cfg: Cfg):
                                         f"not started {sorted(h.todo)})")
             hist = _gh(s, g, todo=h.todo - {c.lid})
             tpub = g if c.lid == 0 else s.tpub          # WG 0 publishes its transmit state
-            nxt = CLAIM if cfg.chunks else ARRIVE
-            put(Cta(nxt, c.lid, g), hist=hist, tpub=tpub)
-            if cfg.bare and bl and not cfg.chunks:
+            if h.replay:
+                nxt = Cta(REPLAY_RUN, c.lid, g)
+            else:
+                nxt = Cta(HB_ITEM, c.lid, g, (0, False)) if cfg.items else Cta(ARRIVE, c.lid, g)
+            put(nxt, hist=hist, tpub=tpub)
+            if cfg.bare and bl and not cfg.items:
                 nb = (dl, wl, gl, bl - 1)
                 if c.lid != 0:
                     put(Cta(BK_R, c.lid, g), hist=hist, tpub=tpub, budget=nb)
                 put(Cta(BF_R, c.lid, g), hist=hist, tpub=tpub, budget=nb)
-        # ---------------- chunked interval ----------------
-        elif c.pc == CLAIM:
+        # ---------------- static items, mid-interval offer_kill with hand-back ----------------
+        elif c.pc == HB_ITEM:
+            k, nostop = c.a
             h = s.hist[g]
-            ch = h.claimed
-            midkill = sched and cfg.barrier == "query"
-            stop = midkill and c.lid != 0 and s.demand > 0 and c.lid + s.demand >= s.W[1]
-            hist = _gh(s, g, claimed=h.claimed + 1)
-            if ch < cfg.chunks:
-                if stop and "kill_with_chunk" in bugs:
-                    put(Cta(OFFER, c.lid, g, (False,)), hist=hist)
-                else:
-                    put(Cta(PROC, c.lid, g, (stop,)), hist=hist)
-            elif stop:
-                put(Cta(OFFER, c.lid, g, (True,)), hist=hist)
+            if k == cfg.items:
+                put(Cta(ARRIVE, c.lid, g))
             else:
-                put(Cta(ARRIVE, c.lid, g), hist=hist)
-        elif c.pc == PROC:
-            h = s.hist[g]
-            hist = _gh(s, g, done=h.done + 1)
-            put(Cta(OFFER, c.lid, g, (False,)) if c.a[0] else Cta(CLAIM, c.lid, g), hist=hist)
+                it = (c.lid, k)
+                if it in h.done:
+                    raise ProtocolViolation(f"P6: item {it} of level {h.level} runs twice")
+                put(Cta(HB_POLL, c.lid, g, (k + 1, nostop)), hist=_gh(s, g, done=h.done | {it}))
+        elif c.pc == HB_POLL:                     # demand read with the item
+            k, nostop = c.a
+            midkill = sched and cfg.barrier == "query"
+            if midkill and c.lid != 0 and not nostop and s.demand > 0:
+                put(Cta(HB_POLLW, c.lid, g, (k, s.demand)))
+            else:
+                put(Cta(HB_ITEM, c.lid, g, (k, nostop)))
+        elif c.pc == HB_POLLW:                    # ... and W.M: asked to surrender?
+            k, d = c.a
+            if c.lid + d >= s.W[1]:
+                put(Cta(OFFER, c.lid, g, (k,)))
+            else:
+                put(Cta(HB_ITEM, c.lid, g, (k, False)))
         elif c.pc == OFFER:                       # loop head: read W
             put(Cta(OFFER_D, c.lid, g, (c.a[0], s.W)))
         elif c.pc == OFFER_D:                     # read demand, decide
-            last_chunk, w = c.a
+            k, w = c.a
             d = s.demand
             wg, M, arr = w
-            cont = Cta(ARRIVE, c.lid, g) if last_chunk else Cta(CLAIM, c.lid, g)
             if d == 0 or c.lid == 0 or c.lid + d < M or wg != g:
-                put(cont)
+                put(Cta(HB_ITEM, c.lid, g, (k, False)))
             elif c.lid != M - 1:
                 if arr and "midkill_wait_arrived" not in bugs:
-                    put(cont)
+                    put(Cta(HB_ITEM, c.lid, g, (k, True)))      # no more offers this interval
                 else:
-                    put(Cta(OFFER, c.lid, g, (last_chunk,)))        # spin
+                    put(Cta(OFFER, c.lid, g, (k,)))             # spin
             else:
-                put(Cta(OFFER_CASD, c.lid, g, (last_chunk, w, d)))
+                put(Cta(OFFER_CASD, c.lid, g, (k, w, d)))
         elif c.pc == OFFER_CASD:
-            last_chunk, w, d = c.a
+            k, w, d = c.a
             if s.demand == d:
-                put(Cta(OFFER_CASW, c.lid, g, (last_chunk, w, w[1])), demand=d - 1)
+                put(Cta(DONATE, c.lid, g, (k, w)), demand=d - 1)
             else:
-                put(Cta(OFFER, c.lid, g, (last_chunk,)))
-        elif c.pc == OFFER_CASW:
-            last_chunk, w, M = c.a
+                put(Cta(OFFER, c.lid, g, (k,)))
+        elif c.pc == DONATE:                      # hand back the items not yet run
+            k, w = c.a
+            k0 = k + 1 if "handback_skips_item" in bugs else k
+            rem = frozenset((c.lid, j) for j in range(k0, cfg.items))
+            if "kill_without_handback" in bugs:
+                rem = frozenset()
+            h = s.hist[g]
+            put(Cta(OFFER_CASW, c.lid, g, (k, w, rem)), hist=_gh(s, g, donated=h.donated | rem))
+        elif c.pc == OFFER_CASW:                  # kill_top: CAS W {g,M,a} -> {g,M-1,a}
+            k, w, rem = c.a
             if s.W == w:
-                if w[1] != M and "kill_any_top" not in bugs:
-                    raise ProtocolViolation(f"P2: kill-CAS writes M-1 from a stale M={M} (W.M={w[1]})")
-                out.extend(_kill_cas(s, p, c, M, w[2], cfg))
+                out.extend(_kill_cas(s, p, c, w[1], w[2], cfg))
+            elif s.W[0] != g or s.W[1] != c.lid + 1:
+                put(Cta(WITHDRAW, c.lid, g, (k, rem)))           # M or gen moved: not the top now
             else:
-                put(Cta(OFFER_CASW, c.lid, g, (last_chunk, s.W, M)))   # prev: keep M, new a
+                put(Cta(OFFER_CASW, c.lid, g, (k, s.W, rem)))    # arrivals raced the CAS
+        elif c.pc == WITHDRAW:
+            k, rem = c.a
+            h = s.hist[g]
+            put(Cta(HB_ITEM, c.lid, g, (k, False)), hist=_gh(s, g, donated=h.donated - rem), demand=s.demand + 1)
+        elif c.pc == REPLAY_RUN:                  # this member's share of the handed-back items
+            h = s.hist[g]
+            M = h.mprime
+            mine = [it for i, it in enumerate(h.replay) if i % M == c.lid]
+            for it in mine:
+                if it in h.done:
+                    raise ProtocolViolation(f"P6: item {it} of level {h.level} runs twice")
+            put(Cta(ARRIVE, c.lid, g), hist=_gh(s, g, done=h.done | frozenset(mine)))
         # ---------------- arrival ----------------
         elif c.pc == ARRIVE:
             if sched and cfg.barrier == "naive" and c.lid != 0 and not c.a:
@@ -312,7 +358,7 @@ def _successors(s: S, cfg: Cfg):
             else:
                 put(Cta(NV_CASW, c.lid, g, (s.W,)))        # prev: M and a re-read
         elif c.pc == SPIN:
-            rg, rM = s.R
+            rg, rM, _ = s.R
             if rg == g:
                 continue
             if "kill_by_M_only" in bugs:
@@ -324,7 +370,7 @@ def _successors(s: S, cfg: Cfg):
                 raise ProtocolViolation(f"P3: id {c.lid} killed={killed} with M'={mp}")
             if killed:
                 put(Cta(KILLED, c.lid, g))
-            elif rg >= E:
+            elif s.hist[rg].level >= E:
                 put(Cta(EXITED), done=s.done or c.lid == 0, slots=_set(s.slots, p, IDLE))
             else:
                 put(Cta(WORK, c.lid, rg))
@@ -332,6 +378,9 @@ def _successors(s: S, cfg: Cfg):
         elif c.pc == SER_POLICY:
             M, behalf = c.a
             wait = cfg.policy in ("scripted", "random")
+            if cfg.items and s.hist[g].donated and "no_replay" not in bugs:
+                put(Cta(SER_RESET, c.lid, g, (M, behalf, M, True)))     # a replay interval follows
+                continue
             if cfg.policy == "scripted":
                 t = cfg.targets[g] if g < len(cfg.targets) else 0
                 choices = [max(1, min(P, t)) if t else M]
@@ -369,28 +418,32 @@ def _successors(s: S, cfg: Cfg):
                     put(Cta(SER_FORK, c.lid, g, (M, behalf, mp, got + 1, wait, sf)),
                         slots=_set(s.slots, q, ASSIGNED), mail=_set(s.mail, q, (M + got, g + 1, ("wg0", g))))
                 elif not wait:
-                    put(Cta(SER_RESET, c.lid, g, (M, behalf, M + got)),
+                    put(Cta(SER_RESET, c.lid, g, (M, behalf, M + got, False)),
                         grant=s.grant - got if sf else s.grant)
                 # else: wait for a CTA to park (self loop)
             else:
-                put(Cta(SER_RESET, c.lid, g, (M, behalf, mp)), grant=s.grant - got if sf else s.grant)
+                put(Cta(SER_RESET, c.lid, g, (M, behalf, mp, False)), grant=s.grant - got if sf else s.grant)
         elif c.pc == SER_RESET:
-            M, behalf, mp = c.a
+            M, behalf, mp, rpl = c.a
             h = s.hist[g]
             if h.cur != h.arrived or h.todo:
                 raise ProtocolViolation(f"P1: barrier {g} completes with arrivals {sorted(h.arrived)} "
                                         f"of members {sorted(h.cur)}")
-            if cfg.chunks and h.done != cfg.chunks:
-                raise ProtocolViolation(f"P6: barrier {g} completes with {h.done}/{cfg.chunks} chunks processed")
-            hist = s.hist + (Gen(frozenset(range(mp)), frozenset(range(mp))),)
-            put(Cta(SER_RELEASE, c.lid, g, (M, behalf, mp)), W=(g + 1, mp, 0), hist=hist)
+            if rpl:
+                ng = Gen(frozenset(range(mp)), frozenset(range(mp)), level=h.level, items=h.items, done=h.done,
+                         replay=tuple(sorted(h.donated)))
+            else:
+                if cfg.items and h.done != h.items:
+                    raise ProtocolViolation(f"P6: level {h.level} ends with items {sorted(h.items - h.done)} not run")
+                ng = Gen(frozenset(range(mp)), frozenset(range(mp)), level=h.level + 1, items=_level_items(cfg, mp))
+            put(Cta(SER_RELEASE, c.lid, g, (M, behalf, mp, rpl)), W=(g + 1, mp, 0), hist=s.hist + (ng,))
         elif c.pc == SER_RELEASE:
-            M, behalf, mp = c.a
+            M, behalf, mp, rpl = c.a
             hist = _set(s.hist, g + 1, replace(s.hist[g + 1], released=True, mprime=mp))
-            st = replace(s, R=(g + 1, mp), hist=hist)
+            st = replace(s, R=(g + 1, mp, int(rpl)), hist=hist)
             if behalf or c.lid >= mp:
                 put(Cta(KILLED, c.lid, g), st)
-            elif g + 1 >= E:
+            elif hist[g + 1].level >= E:
                 put(Cta(EXITED), st, done=s.done or c.lid == 0, slots=_set(s.slots, p, IDLE))
             else:
                 put(Cta(WORK, c.lid, g + 1), st)
@@ -491,6 +544,8 @@ class Result:
     terminal: int
     max_gen: int = 0
     kills_seen: set = field(default_factory=set)
+    max_level: int = 0
+    replays: int = 0
 
 
 def explore_cfg(cfg: Cfg, max_states: int = 3_000_000) -> Result:
@@ -506,7 +561,7 @@ def explore_cfg(cfg: Cfg, max_states: int = 3_000_000) -> Result:
     succ: list[list[int]] = []
     q = deque([0])
     good = []
-    max_gen = 0
+    max_gen = max_level = replays = 0
     while q:
         i = q.popleft()
         s = states[i]
@@ -528,12 +583,16 @@ def explore_cfg(cfg: Cfg, max_states: int = 3_000_000) -> Result:
             succ.append([])
         succ[i] = lst
         max_gen = max(max_gen, s.W[0])
+        if s.W[0] < len(s.hist):
+            max_level = max(max_level, s.hist[s.W[0]].level)
+            if s.hist[s.W[0]].replay:
+                replays += 1
         if not lst:
             if not all(c.pc == EXITED for c in s.ctas):
                 raise ProtocolViolation(f"P5 deadlock: {_fmt(s)}")
-            for g in range(cfg.E):
-                if s.hist[g].todo:
-                    raise ProtocolViolation(f"P2: interval {g} ids {sorted(s.hist[g].todo)} never worked")
+            for g, h in enumerate(s.hist):
+                if h.level < cfg.E and h.todo:
+                    raise ProtocolViolation(f"P2: interval {g} ids {sorted(h.todo)} never worked")
             good.append(i)
     # P5 (liveness): backward reachability from the good terminal states
     pred: list[list[int]] = [[] for _ in states]
@@ -553,7 +612,7 @@ def explore_cfg(cfg: Cfg, max_states: int = 3_000_000) -> Result:
     for i, flag in enumerate(ok):
         if not flag:
             raise ProtocolViolation(f"P5 livelock/deadlock: no continuation terminates from {_fmt(states[i])}")
-    return Result(len(states), len(good), max_gen)
+    return Result(len(states), len(good), max_gen, max_level=max_level, replays=replays)
 
 
 def _fmt(s: S) -> str:

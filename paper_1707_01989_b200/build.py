@@ -7,6 +7,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
@@ -35,13 +36,25 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
     if not force and out == LIB and not needs_build():
         return LIB
-    cmd = [NVCC, *FLAGS, *( ["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines],
-           "-o", out + ".tmp", *SOURCES]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
-    if verbose:
-        sys.stderr.write(res.stderr)
+    # one nvcc per translation unit, in parallel (separate TUs either way: no -rdc), then link
+    common = [NVCC, *FLAGS[:-1], *(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines]]
+    objs = [f"{out}.{os.path.basename(s)}.o" for s in SOURCES]
+
+    def compile_one(i):
+        return subprocess.run([*common, "-c", "-o", objs[i], SOURCES[i]], capture_output=True, text=True)
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, range(len(SOURCES))))
+    results.append(subprocess.run([NVCC, *FLAGS, "-o", out + ".tmp", *objs], capture_output=True, text=True)
+                   if all(r.returncode == 0 for r in results) else results[0])
+    for o in objs:
+        if os.path.exists(o):
+            os.remove(o)
+    for res in results:
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
+        if verbose:
+            sys.stderr.write(res.stderr)
     os.replace(out + ".tmp", out)
     return out
 

@@ -69,6 +69,7 @@ class Stats(ctypes.Structure):
                 ("n_wgs", ctypes.c_uint32), ("threads_per_wg", ctypes.c_uint32),
                 ("tasks_posted", ctypes.c_uint32), ("tasks_completed", ctypes.c_uint32),
                 ("bottom_up_levels", ctypes.c_uint32), ("mid_kills", ctypes.c_uint32),
+                ("handbacks", ctypes.c_uint32), ("replays", ctypes.c_uint32), ("reserved0", ctypes.c_uint32),
                 ("m_trace", ctypes.POINTER(ctypes.c_uint32)), ("m_trace_cap", ctypes.c_uint32),
                 ("level_sizes", ctypes.POINTER(ctypes.c_uint32)), ("level_sizes_cap", ctypes.c_uint32),
                 ("level_end_ns", ctypes.POINTER(ctypes.c_uint64)), ("level_end_ns_cap", ctypes.c_uint32),
@@ -252,6 +253,8 @@ class RunStats:
     tasks_completed: int = 0
     bottom_up_levels: int = 0
     mid_kills: int = 0
+    handbacks: int = 0
+    replays: int = 0
     m_trace: list = field(default_factory=list)
     level_sizes: list = field(default_factory=list)
     level_end_ns: list = field(default_factory=list)
@@ -393,7 +396,7 @@ def _to_runstats(st: Stats, bufs) -> RunStats:
     r = RunStats(**{k: getattr(st, k) for k in ("kernel_ns", "edges_scanned", "frontier_total", "reached",
                                                 "levels", "episodes", "kills", "forks", "min_m", "max_m",
                                                 "n_wgs", "threads_per_wg", "tasks_posted", "tasks_completed",
-                                                "bottom_up_levels", "mid_kills")})
+                                                "bottom_up_levels", "mid_kills", "handbacks", "replays")})
     if "m" in bufs:
         r.m_trace = list(bufs["m"][: min(st.episodes, st.m_trace_cap)])
     if "l" in bufs:

@@ -35,9 +35,6 @@
 #ifndef COOP_BU_SOLO
 #define COOP_BU_SOLO 8        // bottom-up (compacted): per-lane steps before the warp takes a list over (same sweep)
 #endif
-#ifndef COOP_BU_CHUNK
-#define COOP_BU_CHUNK 16u     // bottom-up items per mid-interval claim (scheduler policy only)
-#endif
 #ifndef COOP_L2_HINTS
 #define COOP_L2_HINTS 1       // streaming reads (probe records, row offsets, columns of the bottom-up
                               // scan) carry an L2 evict_first policy so the hot bitmaps stay resident
@@ -833,7 +830,7 @@ struct BfsApp {
         mfsum = 0;
     }
 
-    template <int BLOCK, bool MID = false>
+    template <int BLOCK, int DIST = DIST_STATIC>
     __device__ uint32_t expand(const KParams &p, CtaState &cs) {
         constexpr uint32_t WPB = BLOCK / 32;
         const uint32_t warp = threadIdx.x >> 5;
@@ -846,7 +843,7 @@ struct BfsApp {
         uint32_t reached = 0;
         const uint32_t mode = cs.app_u32[5];
         uint32_t *fnext = p.dopt ? p.fbits[(cs.level + 1) % 3] : nullptr;
-        if (p.dopt) {   // recycle the bitmap of level L-1 as the next-next frontier (static split)
+        if (p.dopt && DIST != DIST_REPLAY) {   // recycle the bitmap of level L-1 as the next-next frontier (static split)
             uint32_t *fold = p.fbits[(cs.level + 2) % 3];
             const uint64_t nw = ((uint64_t)p.V + 31) / 32;
             for (uint64_t i = (uint64_t)cs.lid * BLOCK + threadIdx.x; i < nw; i += (uint64_t)cs.M * BLOCK) fold[i] = 0u;
@@ -868,19 +865,19 @@ struct BfsApp {
             const uint32_t W = cs.app_u32[6] <= 1 ? COOP_BU_DENSE_W : 32u;
             // chunk = items claimed per CTA claim; only used when a scheduler can ask for workgroups
             // mid-interval (static split otherwise): it bounds the offer_kill latency
-            r = claim_items<BLOCK, MID>(p, cs, *this, &p.ctl->claim[in][0][0], (nw + W - 1) / W, COOP_BU_CHUNK, [&](uint64_t it) {
+            r = claim_items<BLOCK, DIST>(p, cs, *this, &p.ctl->claim[in][0][0], (nw + W - 1) / W, [&](uint64_t it) {
                 bu_compact<COOP_BU_K>(p, cs, it * W, nw, W, &s_bits[0][wb], &s_bits[1][wb], edges, reached, mfsum);
             }, flush);
         } else if (mode == BFS_BU) {                          // item = BU_KW 32-vertex words
-            r = claim_items<BLOCK, MID>(p, cs, *this, &p.ctl->claim[in][0][0], (nw + BU_KW - 1) / BU_KW, 128u, [&](uint64_t it) {
+            r = claim_items<BLOCK, DIST>(p, cs, *this, &p.ctl->claim[in][0][0], (nw + BU_KW - 1) / BU_KW, [&](uint64_t it) {
                 bu_words<BU_KW>(p, cs, it * BU_KW, nw, edges, reached, mfsum);
             }, flush);
         } else if (mode == BFS_TDB) {                         // item = 32 frontier words
-            r = claim_items<BLOCK, MID>(p, cs, *this, &p.ctl->claim[in][0][0], (nw + 31) / 32, 4u * WPB, [&](uint64_t g) {
+            r = claim_items<BLOCK, DIST>(p, cs, *this, &p.ctl->claim[in][0][0], (nw + 31) / 32, [&](uint64_t g) {
                 tdb_group(p, cs, g, fnext, edges, reached, mfsum, res);
             }, flush, COOP_TD_TAIL);
         } else {                                              // item = 32 light frontier entries
-            expand_heavy(p, cs, gw, TW, fnext, edges, reached, mfsum, res);
+            if (DIST != DIST_REPLAY) expand_heavy(p, cs, gw, TW, fnext, edges, reached, mfsum, res);
             LTRACE(5);
             // entries per warp item: 32 (a full gather) when there are enough items for
             // every warp, else fewer, down to one list per warp -- a small frontier of
@@ -888,7 +885,7 @@ struct BfsApp {
             const uint64_t nl = cs.app_u32[0];
             uint32_t sz = 32;
             while (sz > 1 && (nl + sz - 1) / sz < TW) sz >>= 1;
-            r = claim_items<BLOCK, MID>(p, cs, *this, &p.ctl->claim[in][0][0], (nl + sz - 1) / sz, 4u * WPB,
+            r = claim_items<BLOCK, DIST>(p, cs, *this, &p.ctl->claim[in][0][0], (nl + sz - 1) / sz,
                             [&](uint64_t g) { tdq_group(p, cs, g, sz, fnext, edges, reached, mfsum, res); }, flush,
                             COOP_TD_TAIL);
         }
@@ -1154,7 +1151,7 @@ struct SsspApp {
         __threadfence();   // far_min (RED) is read by the serial section
     }
 
-    template <int BLOCK, bool MID = false>
+    template <int BLOCK, int DIST = DIST_STATIC>
     __device__ uint32_t expand(const KParams &p, CtaState &cs) {
         constexpr uint32_t WPB = BLOCK / 32;
         const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1171,8 +1168,8 @@ struct SsspApp {
             const uint64_t TW = (uint64_t)cs.M * WPB;
             while (sz > COOP_SSSP_MIN_SZ && (items + sz - 1) / sz < TW) sz >>= 1;
         }
-        const uint32_t r = claim_items<BLOCK, MID>(p, cs, *this, &p.ctl->claim[cs.in_sel][0][0], (items + sz - 1) / sz,
-                                                   2u * WPB, [&](uint64_t g) {
+        const uint32_t r = claim_items<BLOCK, DIST>(p, cs, *this, &p.ctl->claim[cs.in_sel][0][0], (items + sz - 1) / sz,
+                                                    [&](uint64_t g) {
             if (drain) drain_group(p, cs, g);
             else relax_group(p, cs, g, sz, edges);
         }, flush);
@@ -1242,7 +1239,7 @@ struct BarrierApp {
     __device__ bool empty(const KParams &p, CtaState &cs) {
         return (uint64_t)cs.level >= p.iters;
     }
-    template <int BLOCK, bool MID = false>
+    template <int BLOCK, int DIST = DIST_STATIC>
     __device__ uint32_t expand(const KParams &p, CtaState &cs) {
         if (threadIdx.x == 0 && (p.flags & COOP_FLAG_CHECK)) {
             if (cs.app_u32[4]) {

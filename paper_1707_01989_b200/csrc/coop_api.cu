@@ -226,6 +226,7 @@ struct Scratch {
     DevBuf h_ro, h_col, h_w, h_out;   // end-to-end (host-pointer) calls
     DevBuf nccl_aux;                  // NCCL data plane: ready, gathered, count send/recv slots
     DevBuf runt;                      // source loop: end time of every run
+    DevBuf rep;                       // hand-back entries of mid-interval offer_kill [P][W]
     cudaEvent_t done_ev = nullptr;    // handle API: the control block's copy back has landed
     volatile uint32_t *nccl_host = nullptr;     // mapped host mirror of `ready`
     void *nccl_warm = nullptr;                  // communicator already warmed up on nccl_stream
@@ -398,6 +399,8 @@ static coop_status fill_stats(const Ctl &c, const KParams &kp, coop_stats *st, c
     st->tasks_completed = c.tasks_completed;
     st->bottom_up_levels = c.n_bu_levels;
     st->mid_kills = c.mid_kills;
+    st->handbacks = c.handbacks;
+    st->replays = c.replays;
     bool pending = false;   // async copies to wait for (only then: a pipelined caller's next
                             // kernel may already be queued on this stream)
     if (st->m_trace && st->m_trace_cap) {
@@ -683,6 +686,10 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
     kp.ctl = static_cast<Ctl *>(s->ctl.p);
     kp.mb = reinterpret_cast<Mailbox *>(static_cast<char *>(s->ctl.p) + sizeof(Ctl));
     kp.stamp = static_cast<uint32_t *>(s->stamp.p);
+    if (sched && o.barrier_mode == COOP_BARRIER_QUERY) {   // mid-interval offer_kill hands items back
+        CUDA_TRY(s->rep.ensure(sizeof(RepEntry) * (size_t)P * (threads / 32)));
+        kp.rep = static_cast<RepEntry *>(s->rep.p);
+    }
     kp.m_trace = static_cast<uint32_t *>(s->mtrace.p);
     kp.m_trace_cap = mcap;
     kp.level_sizes = static_cast<uint32_t *>(s->lsizes.p);

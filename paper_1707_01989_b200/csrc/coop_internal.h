@@ -133,10 +133,23 @@ struct __align__(128) Ctl {
     uint32_t list_n[2];
     uint32_t exits;                    // CTAs that left the kernel (the last one mirrors this block to the host)
     uint32_t pad_ps[13];
-    // chunked intervals (per-warp claims): kClaimShards claim counters per level parity, one
-    // 128-B line each, so claims do not serialise on a single L2 atomic address
+    // claim counters per level parity (dynamic tails of the top-down levels), one 128-B line each
     uint32_t claim[2][kClaimShards][32];
+    // hand-back of a mid-interval offer_kill (SCHEDULER + query): a CTA that leaves inside an
+    // interval hands the rest of its static share back; the serial section turns the handed-back
+    // items into a replay interval run by the survivors before the level ends
+    unsigned long long don;            // {donors:20 | items:44} handed back in the current interval
+    unsigned long long rep;            // `don` of the replay interval being run
+    unsigned long long rep_tw;         // warp stride M*W of the interval the items come from
+    uint32_t handbacks, replays;       // statistics
+    uint32_t pad_hb[26];
 };
+
+// one warp's handed-back static items: start, start + tw, ... (count of them), at flat
+// offset `prefix` of the replay interval; kRepVoid in start = withdrawn (the kill-CAS failed)
+struct RepEntry { uint64_t start; uint64_t prefix; uint32_t count; uint32_t pad; };
+constexpr uint64_t kRepVoid = 1ull << 63;
+constexpr uint64_t kMask44 = (1ull << 44) - 1;
 
 // Partitioned BFS (1-D vertex partition).  Frontier bitmaps and
 // flag blocks of every rank are device-visible here (own memory, or peer
@@ -239,6 +252,7 @@ struct KParams {
     // host-mapped copy of the control block, written by the last CTA to leave the kernel
     // (the call's status and statistics reach the host without a copy-back operation)
     Ctl *ctl_mirror;
+    RepEntry *rep;              // hand-back entries [P][W] (W = warps per CTA)
     // periodic task generator
     uint32_t task_wgs, task_blocks, task_max;
     uint64_t task_block_ns, task_period_ns, task_first_ns;

@@ -67,9 +67,6 @@
 #define COOP_TAIL_DYN 0       // static intervals (measured: 4/16 and 8/16 slower on RMAT-24 direction-optimising)
 //: the last TAIL_DYN/16 of the items are claimed dynamically
 #endif
-#ifndef COOP_CLAIM_WARP
-#define COOP_CLAIM_WARP 0     // chunked intervals: 1 = per-warp claims, one ahead; 0 = per-CTA chunks (default: fewer atomics, measured faster armed)
-#endif
 #ifndef COOP_RUNBODY_NOINLINE
 #define COOP_RUNBODY_NOINLINE 0
 #endif
@@ -93,8 +90,11 @@
 namespace coop {
 
 #if COOP_LTRACE
-// [level][blockIdx][expand start, expand end, after RB1, after RB2, app stamps 4..7]
-__device__ unsigned long long g_ltrace[64][1184][8];
+// [level][blockIdx][expand start, expand end, after RB1, after RB2, app stamps 4..7,
+//                   barrier: 8 arrival done, 9 serial section before publish (last arriver),
+//                   10 after publish (last arriver), 11 release seen (waiter)]
+constexpr int kLtraceSlots = 12;
+__device__ unsigned long long g_ltrace[64][1184][kLtraceSlots];
 #define LTRACE(k)                                                                         \
     do {                                                                                  \
         if (threadIdx.x == 0 && cs.level < 64 && blockIdx.x < 1184)                       \
@@ -198,7 +198,9 @@ struct CtaState {
     unsigned long long edges, frontier, reached;   // per-CTA stats, flushed at body exit
     uint32_t bar_M, bar_naive;                     // barrier: M of the episode, killed on entry (NAIVE)
     uint32_t wait_rel;                             // barrier: this CTA waits for the release word
-    uint32_t chunk, stop, item_next;               // chunk loop broadcast / per-warp item counter
+    uint32_t stop, nostop;                         // DIST_MID: asked to surrender / stop offering this interval
+    uint32_t replay, rep_M;                        // a replay interval follows this barrier; survivors' M in it
+    uint32_t rk[32];                               // DIST_MID: next static item index per warp
 #if COOP_TRACE
     unsigned long long tr[12];
     long long tr_last;
@@ -246,7 +248,7 @@ __device__ __noinline__ uint32_t fork_from_pool(const KParams &p, const CtaState
 // ---------------------------------------------------------------- barrier
 template <class App>
 __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_t g, uint32_t M,
-                               bool resizing, uint32_t entry, uint32_t *out_mp) {
+                               bool resizing, uint32_t entry, uint32_t *out_mp, uint32_t *out_flags) {
     const uint32_t lane = threadIdx.x & 31;
     Ctl *c = p.ctl;
     // every app passes exactly one non-resizing barrier (the init global_barrier at
@@ -254,7 +256,30 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
     const uint32_t ep = g - 1;
     uint32_t Mp = M, take = 0;
     bool sched_fork = false, wait_fork = false;
-    if ((App::kCoop && COOP_BIS_SERIAL) && lane == 0) {
+    // hand-back (SCHEDULER + query, barrier #1): items handed back by CTAs that left inside
+    // the interval make this episode the start of a replay interval -- the level is not
+    // over: no policy decision, no forks, no app serial work, M' = M
+    uint32_t replay = 0;
+    // the scheduler channel and the hand-back word: one batch of independent plain loads
+    // (after the arrival's acquire; the asm-volatile relaxed loads would serialise one
+    // round trip each on this critical path)
+    uint32_t d0 = 0, gr0 = 0;
+    if constexpr (App::kCoop) {
+        if (lane == 0 && resizing && p.policy == COOP_POLICY_SCHEDULER) {
+            const volatile Ctl *vc = c;
+            d0 = c->demand;
+            gr0 = c->grant;
+            if (entry == ENTRY_AFTER_RB1 && p.barrier_mode == COOP_BARRIER_QUERY) {
+                const unsigned long long dw = vc->don;
+                if (dw) {
+                    c->don = 0ull;
+                    if (dw & kMask44) { c->rep = dw; replay = 1; }
+                }
+            }
+        }
+        replay = __shfl_sync(FULL, replay, 0);
+    }
+    if ((App::kCoop && COOP_BIS_SERIAL) && lane == 0 && !replay) {
         if (resizing && p.barrier_mode != COOP_BARRIER_PLAIN) {
             if (p.policy == COOP_POLICY_SCRIPTED) {
                 uint32_t s = ep < p.script_len ? p.script[ep] : 0u;
@@ -267,7 +292,7 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
             } else if (p.policy == COOP_POLICY_SCHEDULER) {
                 if (p.barrier_mode == COOP_BARRIER_QUERY) {
                     // query(): W = demand, satisfied up to M-1 in this episode (reading R5)
-                    uint32_t d = ld_relaxed32(&c->demand);
+                    uint32_t d = d0;
                     while (d > 0 && M > 1) {
                         uint32_t t = min(d, M - 1);
                         uint32_t old = atomicCAS(&c->demand, d, d - t);
@@ -278,7 +303,7 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
                 if (take > 0) {
                     Mp = M - take;
                 } else {
-                    uint32_t gr = ld_relaxed32(&c->grant);
+                    const uint32_t gr = gr0;
                     if (gr > 0 && M < p.P) { Mp = M + min(gr, p.P - M); sched_fork = true; }
                 }
             }
@@ -299,7 +324,8 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
         Mp = M + got;
     }
     if (lane == 0) {
-        app.serial(p, cs, entry, resizing);
+        if (!replay) app.serial(p, cs, entry, resizing);
+        else atomicAdd(&c->replays, 1u);
         if (p.flags & COOP_FLAG_CHECK) {
             // every active WG arrived exactly once and ids were exactly [0, M)
             uint32_t a = atomicExch(&c->chk_arr[g & 1], 0u);
@@ -322,7 +348,9 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
         // reset the arrival word for generation g+1, then release on the separate
         // release line R (waiters poll R, arrivals hit W: no polling traffic on the
         // line the arrival atomics serialise on)
-        coop_proto::publish(&c->W, &c->R, g + 1, Mp);
+        LTRACE(9);
+        coop_proto::publish(&c->W, &c->R, g + 1, Mp, replay);
+        LTRACE(10);
         // statistics after the release: nobody waits for them (the host reads them at the end)
         if constexpr ((App::kCoop && COOP_BIS_SERIAL)) {
             const uint64_t now = globaltimer();
@@ -348,6 +376,7 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
         }
     }
     *out_mp = Mp;
+    *out_flags = replay;
 }
 
 __device__ __forceinline__ uint32_t mhist_get(const KParams &p, uint32_t gen) {
@@ -432,6 +461,7 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
 #if COOP_TRACE
         tr2 = clock64();
 #endif
+        if (resizing) LTRACE(8);
         if (w_gen(old) != g) { atomicCAS(&c->err, DERR_NONE, DERR_INVARIANT); set_abort(p, DERR_INVARIANT); }
         cs.last = last;
         cs.bar_M = killed_naive ? w_M(old) - 1 : w_M(old);   // M of the episode for the serial section
@@ -463,6 +493,7 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
             }
             if (threadIdx.x == 0) {
                 cs.wait_rel = 0u;
+                if (resizing) LTRACE(11);
                 if (stop == 2u) {
                     cs.action = ACT_ABORT;
                 } else if (w_gen(w) != g + 1) {
@@ -471,7 +502,7 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
                     // W.M is M' unless NAIVE kills of generation g+1 already lowered it
                     const uint32_t Mn = (App::kCoop && COOP_BIS_BARRIER) && p.barrier_mode == COOP_BARRIER_NAIVE ? mhist_get(p, g + 1) : w_M(w);
                     if ((App::kCoop && COOP_BIS_BARRIER) && cs.lid >= Mn) cs.action = ACT_KILLED;
-                    else { cs.M = Mn; cs.gen = g + 1; }
+                    else { cs.M = Mn; cs.gen = g + 1; cs.replay = w_arr(w) & 1u; }
                 }
             }
             __syncwarp();
@@ -494,7 +525,7 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
             } else {
                 const uint32_t Mn = p.barrier_mode == COOP_BARRIER_NAIVE ? mhist_get(p, g + 1) : w_M(w);
                 if (cs.lid >= Mn) cs.action = ACT_KILLED;
-                else { cs.M = Mn; cs.gen = g + 1; }
+                else { cs.M = Mn; cs.gen = g + 1; cs.replay = w_arr(w) & 1u; }
             }
         }
     }
@@ -505,11 +536,11 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
     cta_sync();
     if (cs.last) {  // uniform
         if (threadIdx.x < 32) {
-            uint32_t Mp;
-            serial_section(p, cs, app, cs.gen, cs.bar_M, resizing, entry, &Mp);
+            uint32_t Mp, fl;
+            serial_section(p, cs, app, cs.gen, cs.bar_M, resizing, entry, &Mp, &fl);
             if (threadIdx.x == 0) {
                 if (cs.bar_naive || cs.lid >= Mp) cs.action = ACT_KILLED;
-                else { cs.M = Mp; cs.gen = cs.gen + 1; cs.action = ACT_CONT; }
+                else { cs.M = Mp; cs.gen = cs.gen + 1; cs.action = ACT_CONT; cs.replay = fl; }
 #if COOP_ERR_RELOAD
                 if (ld_relaxed32(&c->err) != DERR_NONE) cs.action = ACT_ABORT;
 #endif
@@ -535,16 +566,54 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
 }
 
 // ---------------------------------------------------------------- mid-interval offer_kill
-// offer_kill at a chunk boundary inside an interval whose work is handed out
-// by a chunk counter (so a leaving CTA strands no work).  CTA-collective.
-// Query style: every id >= M - W stops claiming and offers until
-// claimed; only the current top id M-1 can go, by CAS on the
-// arrival word {g, M, a} -> {g, M-1, a}.  If everybody else is already waiting
-// at the barrier, the leaver completes the episode on their behalf.
-// Returns ACT_KILLED, ACT_CONT (resume claiming) or ACT_ABORT.  `flush` is
-// called (CTA-collective) before the CTA can be counted out.
-template <class App, class Flush>
-__device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, App &app, Flush &&flush) {
+// SCHEDULER + query: a CTA may leave inside an interval (the paper's remedy
+// for wide graphs whose barriers are rare) without any dynamic claiming.
+// Work stays split statically by (id, M) exactly as in Fig. 4; every warp
+// reads the demand word with each item, and a CTA asked to surrender (id >= M - demand,
+// query style P:940-947) stops after the items in hand, HANDS BACK the rest of its
+// static share (hand_back below) and offers itself.  Only the current top id M-1 can go
+// (P:541-548), by CAS on the arrival word {g, M, a} -> {g, M-1, a}; if everybody else
+// already waits at the barrier, the leaver completes the episode on their behalf.  The
+// serial section of the barrier sees the handed-back items and releases the survivors
+// into a replay interval that runs them (the level ends only after it).  Returns
+// ACT_KILLED, ACT_CONT (resume the static share) or ACT_ABORT; `flush` is called
+// (CTA-collective) before the CTA can be counted out.
+
+// thread 0: hand back what is left of this CTA's static share (cs.rk[w] = the next
+// item index of warp w; warp w's items are gw, gw + TW, ... below n); returns the donor
+// index, or ~0u when nothing is left
+template <int BLOCK>
+__device__ __forceinline__ uint32_t hand_back(const KParams &p, CtaState &cs, uint64_t n, uint64_t TW) {
+    constexpr uint32_t WPB = BLOCK / 32;
+    uint64_t start[WPB], cnt[WPB], tot = 0;
+#pragma unroll
+    for (uint32_t w = 0; w < WPB; ++w) {
+        start[w] = (uint64_t)cs.lid * WPB + w + (uint64_t)cs.rk[w] * TW;
+        cnt[w] = start[w] < n ? (n - start[w] + TW - 1) / TW : 0;
+        tot += cnt[w];
+    }
+    if (tot == 0) return ~0u;
+    Ctl *c = p.ctl;
+    const unsigned long long old = atomicAdd(&c->don, (1ull << 44) | tot);
+    const uint32_t idx = (uint32_t)(old >> 44);
+    uint64_t pre = old & kMask44;
+    RepEntry *e = p.rep + (uint64_t)idx * WPB;
+#pragma unroll
+    for (uint32_t w = 0; w < WPB; ++w) {
+        e[w].start = start[w];
+        e[w].prefix = pre;
+        e[w].count = (uint32_t)cnt[w];
+        pre += cnt[w];
+    }
+    st_relaxed64(&c->rep_tw, TW);          // the same value from every donor of the interval
+    atomicAdd(&c->handbacks, 1u);
+    return idx;
+}
+
+template <int BLOCK, class App, class Flush>
+__device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, App &app, Flush &&flush, uint64_t n,
+                                                uint64_t TW) {
+    constexpr uint32_t WPB = BLOCK / 32;
     Ctl *c = p.ctl;
     flush();
     cta_sync();
@@ -559,11 +628,20 @@ __device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, 
                 if (d == 0 || cs.lid == 0 || cs.lid + d < M || w_gen(w) != cs.gen) { act = ACT_CONT; break; }
                 // the ids above go first; but once some CTA has arrived at the barrier the top
                 // id may be among them and can no longer leave mid-interval: then stop offering
-                // and let the query barrier take the demand (waiting here would deadlock)
-                if (cs.lid != M - 1) { act = w_arr(w) ? ACT_CONT : ACT_IDLE; break; }
+                // for the rest of the interval and let the query barrier take the demand
+                // (waiting here would deadlock; re-offering at every item would thrash)
+                if (cs.lid != M - 1) {
+                    if (w_arr(w)) { act = ACT_CONT; cs.nostop = 1; } else act = ACT_IDLE;
+                    break;
+                }
                 if (atomicCAS(&c->demand, d, d - 1) != d) { w = ld_relaxed64(&c->W); continue; }
+                const uint32_t idx = hand_back<BLOCK>(p, cs, n, TW);
+                __threadfence();                           // the entries before the kill-CAS
                 uint32_t a = 0, M_k = 0;
                 if (!coop_proto::kill_top(&c->W, w, cs.lid, cs.gen, &a, &M_k)) {   // W moved: not the top now
+                    if (idx != ~0u)                        // withdraw: this CTA keeps its items
+                        for (uint32_t k = 0; k < WPB; ++k) p.rep[(uint64_t)idx * WPB + k].start |= kRepVoid;
+                    __threadfence();
                     atomicAdd(&c->demand, 1u);
                     act = ACT_CONT;
                     break;
@@ -582,6 +660,7 @@ __device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, 
                 if (a == M - 1) { serial = 1; Mnew = M - 1; }          // all others wait: complete for them
                 break;
             }
+            if (act == ACT_CONT) cs.stop = 0;
             cs.action = act;
             cs.last = serial;
             cs.bar_M = Mnew;
@@ -594,8 +673,8 @@ __device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, 
                 if (threadIdx.x == 0) cs.in_sel ^= 1u;
                 cta_sync();
                 if (threadIdx.x < 32) {
-                    uint32_t Mp;
-                    serial_section(p, cs, app, cs.gen, cs.bar_M, true, ENTRY_AFTER_RB1, &Mp);
+                    uint32_t Mp, fl;
+                    serial_section(p, cs, app, cs.gen, cs.bar_M, true, ENTRY_AFTER_RB1, &Mp, &fl);
                 }
                 cta_sync();
             }
@@ -611,176 +690,117 @@ __device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, 
     }
 }
 
-// Dynamic work distribution of an interval over `n_items` warp-sized items:
-// a CTA claims a chunk of `per_chunk` items from `counter`, its warps take the
-// chunk's items one at a time from a shared-memory counter (so a warp waits at
-// most one item for its siblings), then the CTA claims again.  With the
-// SCHEDULER policy every claim also reads the resource channel and, when this
-// id is asked to surrender, the CTA offers itself (offer_kill_mid) right after
-// finishing the chunk in hand.  fn(item) is warp-collective.
-template <int BLOCK, bool MID, class App, class Fn, class Flush>
-__device__ uint32_t claim_items_cta(const KParams &p, CtaState &cs, App &app, uint32_t *counter, uint64_t n_items,
-                                uint32_t per_chunk, Fn &&fn, Flush &&flush) {
-    // MID: the chunked distribution is compiled only into the expand instance run_body
-    // selects when a scheduler can ask for workgroups inside the interval; the static
-    // instance has no trace of it (its mere presence cost 12 % of the static loop's
-    // speed, tools/variant_bench.py)
-    constexpr bool midkill = MID && App::kCoop && COOP_BIS_CLAIM;
-    const uint32_t lane = threadIdx.x & 31;
-    if (!midkill) {
-        // no scheduler can ask for workgroups inside this interval: Fig. 4's static
-        // distribution, item i to warp i mod (M*W) -- no atomics, no syncs
-        constexpr uint32_t WPB = BLOCK / 32;
-        const uint64_t TW = (uint64_t)cs.M * WPB;
-        for (uint64_t it = (uint64_t)cs.lid * WPB + (threadIdx.x >> 5); it < n_items; it += TW) fn(it);
-        (void)counter;
-        (void)per_chunk;
-        (void)lane;
-        return ACT_CONT;
-    }
-    const uint64_t nchunks = (n_items + per_chunk - 1) / per_chunk;
-    for (;;) {
-        if (threadIdx.x == 0) {
-            const uint32_t ch = atomicAdd(counter, 1u);
-            uint32_t stop = 0;
-            if (midkill && cs.lid != 0) {
-                const uint32_t d = ld_relaxed32(&p.ctl->demand);
-                if (d) stop = cs.lid + d >= w_M(ld_relaxed64(&p.ctl->W));
-            }
-            cs.chunk = ch;
-            cs.stop = stop;
-            cs.item_next = 0;
-        }
-        cta_sync();
-        const uint32_t ch = cs.chunk, stop = cs.stop;
-        if (ch < nchunks) {
-            const uint64_t base = (uint64_t)ch * per_chunk;
-            const uint32_t cnt = (uint32_t)min((uint64_t)per_chunk, n_items - base);
-            for (;;) {
-                uint32_t it = 0;
-                if (lane == 0) it = atomicAdd(&cs.item_next, 1u);
-                it = __shfl_sync(FULL, it, 0);
-                if (it >= cnt) break;
-                fn(base + it);
-            }
-        }
-        cta_sync();                                   // chunk done; cs.chunk reusable
-        if constexpr (midkill) {
-            if (stop) {
-                const uint32_t r = offer_kill_mid(p, cs, app, flush);
-                if (r != ACT_CONT) return r;
-            }
-        }
-        if (ch >= nchunks) return ACT_CONT;
-    }
-}
-
-
 // Work distribution of an interval over `n_items` warp-sized items; fn(item) is
-// warp-collective.
-//  static (MID = false: no scheduler can ask for workgroups inside this interval):
-//          Fig. 4's distribution, item i to warp i mod (M*W) -- no atomics,
-//          no syncs.  run_body instantiates the expand with MID = false whenever the
-//          policy cannot demand workgroups mid-interval; the chunked code below is then
-//          not compiled into it at all (its mere presence cost 12 % of the static
-//          loop's speed: tools/variant_bench.py, profiles/r02_variants.log).
-//  chunked (MID = true: SCHEDULER + query): items are claimed from `counter` so a CTA
-//          can leave at a claim boundary (offer_kill_mid) without stranding work.
-//          COOP_CLAIM_WARP (default): each warp claims its own per_chunk/W items with a
-//          global atomic issued one claim AHEAD (the round trip overlaps the current
-//          item; the prefetched claim is always processed), reads the resource
-//          channel with the claim, and raises a CTA flag when this id is asked to
-//          leave; no CTA barrier until the warps run out of items.  Otherwise the
-//          CTA claims per_chunk items and its warps take them from a shared counter
-//          (two CTA barriers per chunk).
-template <int BLOCK, bool MID, class App, class Fn, class Flush>
+// warp-collective.  DIST:
+//  DIST_STATIC (no scheduler can ask for workgroups inside this interval): Fig. 4's
+//          distribution, item i to warp i mod (M*W) -- no atomics, no syncs;
+//          the last tail16/16 of the items are claimed one at a time from the level's
+//          counter by warps that finished their share (top-down levels: evens out the end
+//          of the level without any CTA barrier)
+//  DIST_MID (SCHEDULER + query): the same split; each item also reads the demand word
+//          (lane 0, the load overlaps the item), a CTA asked to surrender stops after the
+//          items in hand and offers itself with its remaining static items handed back
+//          (offer_kill_mid).  Tail items are claimed, so none is ever stranded.
+//  DIST_REPLAY: the survivors run the items handed back in the interval just ended,
+//          flattened (RepEntry prefixes) and split statically over the survivors' warps.
+enum : int { DIST_STATIC = 0, DIST_MID = 1, DIST_REPLAY = 2 };
+
+template <int BLOCK, int DIST, class App, class Fn, class Flush>
 __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32_t *counter, uint64_t n_items,
-                                uint32_t per_chunk, Fn &&fn, Flush &&flush, uint32_t tail16 = COOP_TAIL_DYN) {
-    constexpr bool midkill = MID && App::kCoop && COOP_BIS_CLAIM;
+                                Fn &&fn, Flush &&flush, uint32_t tail16 = COOP_TAIL_DYN) {
     constexpr uint32_t WPB = BLOCK / 32;
-    if constexpr (!midkill) {
-        const uint64_t TW = (uint64_t)cs.M * WPB;
-        // head: Fig. 4's static split; tail (COOP_TAIL_DYN/16 of the items): claimed one at a
-        // time from the level's counter by warps that finished their share, which evens out
-        // the end of the level (long lists, hub-heavy words) without any CTA barrier
-        const uint64_t n_static = tail16 ? n_items - n_items * tail16 / 16 : n_items;
-        for (uint64_t it = (uint64_t)cs.lid * WPB + (threadIdx.x >> 5); it < n_static; it += TW) fn(it);
-        if (tail16 && n_static < n_items) {
-            const uint32_t lane = threadIdx.x & 31;
-            uint32_t t = 0;
-            if (lane == 0) t = atomicAdd(counter, 1u);
-            for (;;) {
-                const uint64_t it = n_static + __shfl_sync(FULL, t, 0);
-                if (it >= n_items) break;
-                if (lane == 0) t = atomicAdd(counter, 1u);        // next claim in flight
-                fn(it);
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t n_static = tail16 ? n_items - n_items * tail16 / 16 : n_items;
+    if constexpr (DIST == DIST_REPLAY) {
+        // cs.rep_M = survivors; the items were numbered by the donors' interval
+        const Ctl *c = p.ctl;
+        const unsigned long long rw = __ldcg(&c->rep);
+        const uint64_t total = rw & kMask44, npairs = (rw >> 44) * WPB;
+        const uint64_t TWi = __ldcg(&c->rep_tw);
+        const uint64_t TWs = (uint64_t)cs.rep_M * WPB;
+        for (uint64_t f = (uint64_t)cs.lid * WPB + warp; f < total; f += TWs) {
+            uint64_t lo = 0, hi = npairs - 1;                 // last entry with prefix <= f
+            while (lo < hi) {
+                const uint64_t mid = (lo + hi + 1) >> 1;
+                if (__ldcg(&p.rep[mid].prefix) <= f) lo = mid; else hi = mid - 1;
             }
+            const uint64_t st = __ldcg(&p.rep[lo].start), pre = __ldcg(&p.rep[lo].prefix);
+            if (st & kRepVoid) continue;                      // withdrawn: its donor ran it
+            fn(st + (f - pre) * TWi);
         }
-        (void)per_chunk;
-        (void)app;
-        (void)flush;
+        (void)counter; (void)app; (void)flush; (void)n_static;
         return ACT_CONT;
     } else {
-#if COOP_CLAIM_WARP
-        const uint32_t lane = threadIdx.x & 31;
-        const uint32_t k = per_chunk >= WPB ? per_chunk / WPB : 1u;      // items per warp claim
-        const uint64_t nclaims = (n_items + k - 1) / k;
-        // the claim space is split over kClaimShards counters (one L2 line each); a warp
-        // starts on its own shard and moves to the next when that one is exhausted
-        constexpr uint32_t S = kClaimShards;
-        const uint64_t per = (nclaims + S - 1) / S;
-        uint32_t shard = (cs.lid * WPB + (threadIdx.x >> 5)) % S, tried = 0;
-        for (;;) {
-            if (threadIdx.x == 0) cs.stop = 0;
+        constexpr bool mid = DIST == DIST_MID && App::kCoop && COOP_BIS_CLAIM;
+        const uint64_t TW = (uint64_t)cs.M * WPB;
+        const uint64_t gw = (uint64_t)cs.lid * WPB + warp;
+        if constexpr (!mid) {
+            for (uint64_t it = gw; it < n_static; it += TW) fn(it);
+            if (tail16 && n_static < n_items) {
+                uint32_t t = 0;
+                if (lane == 0) t = atomicAdd(counter, 1u);
+                for (;;) {
+                    const uint64_t it = n_static + __shfl_sync(FULL, t, 0);
+                    if (it >= n_items) break;
+                    if (lane == 0) t = atomicAdd(counter, 1u);        // next claim in flight
+                    fn(it);
+                }
+            }
+            (void)app; (void)flush;
+            return ACT_CONT;
+        } else {
+            volatile uint32_t *stopf = &cs.stop;
+            if (threadIdx.x == 0) { cs.stop = 0; cs.nostop = 0; }
             cta_sync();
-            uint32_t c = 0, stop = 0;
-            // claim + channel read: the stop decision (this id is asked to leave,
-            // query style P:940-947) raises the CTA flag; the claim itself is kept
-            auto claim = [&]() {
-                if (lane == 0) {
-                    c = 0xFFFFFFFFu;
-                    while (tried < S) {
-                        const uint32_t t = atomicAdd(counter + 32 * shard, 1u);
-                        const uint64_t idx = (uint64_t)shard * per + t;
-                        if (t < per && idx < nclaims) { c = (uint32_t)idx; break; }
-                        shard = (shard + 1) % S;
-                        ++tried;
-                    }
-                    if (cs.lid != 0) {
-                        const uint32_t d = ld_relaxed32(&p.ctl->demand);
-                        if (d && cs.lid + d >= w_M(ld_relaxed64(&p.ctl->W))) stop = 1;
+            // has this CTA been asked to surrender?  (lane 0; d was loaded before the item)
+            auto asked = [&](uint32_t d) {
+                return d && cs.lid != 0 && !cs.nostop && cs.lid + d >= w_M(ld_relaxed64(&p.ctl->W));
+            };
+            uint64_t k = 0;
+            for (;;) {
+                // lane 0 decides, the warp follows (fn is warp-collective)
+                auto stopped = [&]() { return __shfl_sync(FULL, lane == 0 ? *stopf : 0u, 0) != 0; };
+                for (;; ++k) {
+                    const uint64_t it = gw + k * TW;
+                    if (it >= n_static || stopped()) break;
+                    uint32_t d = 0;
+                    if (lane == 0) d = ld_relaxed32(&p.ctl->demand);
+                    fn(it);
+                    if (lane == 0 && asked(d)) *stopf = 1u;
+                }
+                if (lane == 0) cs.rk[warp] = (uint32_t)k;
+                if (tail16 && n_static < n_items && !stopped()) {
+                    uint32_t t = 0;
+                    if (lane == 0) t = atomicAdd(counter, 1u);
+                    for (;;) {
+                        const uint64_t it = n_static + __shfl_sync(FULL, t, 0);
+                        if (it >= n_items) break;
+                        uint32_t d = 0, more = 0;
+                        if (lane == 0) {
+                            more = *stopf ? 0u : 1u;
+                            if (more) t = atomicAdd(counter, 1u);     // next claim in flight
+                            d = ld_relaxed32(&p.ctl->demand);
+                        }
+                        fn(it);                                       // a claimed item is always run
+                        if (lane == 0 && asked(d)) *stopf = 1u;
+                        if (!__shfl_sync(FULL, more, 0)) break;
                     }
                 }
-            };
-            claim();
-            for (;;) {
-                const uint32_t cur = __shfl_sync(FULL, c, 0);
-                const uint32_t st = __shfl_sync(FULL, stop, 0);
-                if (cur >= nclaims) break;
-                const bool more = !st && !*(volatile uint32_t *)&cs.stop;
-                if (st && lane == 0) *(volatile uint32_t *)&cs.stop = 1;
-                if (more) claim();                        // next claim in flight during this one
-                const uint64_t b = (uint64_t)cur * k;
-                const uint64_t e = min(n_items, b + k);
-                for (uint64_t it = b; it < e; ++it) fn(it);
-                if (!more) break;
+                cta_sync();
+                if (!cs.stop) return ACT_CONT;
+                const uint32_t r = offer_kill_mid<BLOCK>(p, cs, app, flush, n_static, TW);
+                if (r != ACT_CONT) return r;                          // killed (or abort): nothing stranded
+                k = cs.rk[warp];
             }
-            cta_sync();                                   // every warp done with its claims
-            if (!cs.stop) return ACT_CONT;                // the counter ran out
-            const uint32_t r = offer_kill_mid(p, cs, app, flush);
-            if (r != ACT_CONT) return r;                  // killed (or abort): nothing stranded
         }
-#else
-        return claim_items_cta<BLOCK, MID>(p, cs, app, counter, n_items, per_chunk, fn, flush);
-#endif
     }
 }
 
 // ---------------------------------------------------------------- body
-// the chunked expand (offer_kill at claim boundaries) as a separate function
-template <class App, int BLOCK>
-__device__ __noinline__ uint32_t expand_mid(const KParams &p, CtaState &cs, App &app) {
-    return app.template expand<BLOCK, true>(p, cs);
+// the expand instances of the scheduler-armed path (DIST_MID, DIST_REPLAY) out of line
+template <class App, int BLOCK, int DIST>
+__device__ __noinline__ uint32_t expand_dist(const KParams &p, CtaState &cs, App &app) {
+    return app.template expand<BLOCK, DIST>(p, cs);
 }
 
 // Fig. 4 with the app's process_node; entry points are the
@@ -812,19 +832,38 @@ __device__ COOP_RUNBODY_ATTR uint32_t run_body(const KParams &p, CtaState &cs, A
             LTRACE(0);
             // for (i = tid; ...) process_node -- the chunked instance when a scheduler may ask
             // for workgroups mid-interval (offer_kill at chunk boundaries), else the static one
+            const bool midk = App::kCoop && p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY;
             if constexpr (App::kCoop) {
-                if (p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY)
-                    r = expand_mid<App, BLOCK>(p, cs, app);           // out of line: keeps the static
-                else                                                  // instance's code as tight as
-                    r = app.template expand<BLOCK, false>(p, cs);     // the non-cooperative kernel's
+                if (midk)
+                    r = expand_dist<App, BLOCK, DIST_MID>(p, cs, app);     // out of line: keeps the static
+                else                                                      // instance's code as tight as
+                    r = app.template expand<BLOCK, DIST_STATIC>(p, cs);   // the non-cooperative kernel's
             } else {
-                r = app.template expand<BLOCK, false>(p, cs);
+                r = app.template expand<BLOCK, DIST_STATIC>(p, cs);
             }
-            if (r != ACT_CONT) return r;                       // killed at a chunk boundary (offer_kill)
+            if (r != ACT_CONT) return r;                       // killed inside the interval (offer_kill)
             cta_sync();                                   // every warp is done reading cs
             LTRACE(1);
             if (threadIdx.x == 0) cs.in_sel ^= 1u;            // swap(&in_nodes, &out_nodes)
             r = barrier(p, cs, app, true, ENTRY_AFTER_RB1);   // resizing_global_barrier() #1
+            if constexpr (App::kCoop) {
+                // hand-back: workgroups left inside the interval with static items undone; the
+                // survivors run them (items numbered by the donors' interval: cs.M = its M for
+                // the app's item parameters, cs.rep_M = the survivors) before the level ends
+                while (midk && r == ACT_CONT && cs.replay) {
+                    if (threadIdx.x == 0) {
+                        cs.in_sel ^= 1u;
+                        cs.rep_M = cs.M;
+                        cs.M = (uint32_t)(__ldcg(&p.ctl->rep_tw) / (BLOCK / 32));
+                    }
+                    cta_sync();
+                    r = expand_dist<App, BLOCK, DIST_REPLAY>(p, cs, app);
+                    if (r != ACT_CONT) return r;
+                    cta_sync();
+                    if (threadIdx.x == 0) { cs.M = cs.rep_M; cs.in_sel ^= 1u; }
+                    r = barrier(p, cs, app, true, ENTRY_AFTER_RB1);
+                }
+            }
             if (r != ACT_CONT) return r;
             LTRACE(2);
         }

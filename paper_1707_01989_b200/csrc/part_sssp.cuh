@@ -73,7 +73,7 @@ struct PartSsspApp {
         return done;
     }
 
-    template <int BLOCK, bool MID = false>
+    template <int BLOCK, int DIST = DIST_STATIC>
     __device__ uint32_t expand(const KParams &p, CtaState &cs) {
         constexpr uint32_t WPB = BLOCK / 32;
         const PartParams &pp = p.part;

@@ -349,16 +349,17 @@ def test_sssp_near_far_under_resizes(coop):
 
 # ---------------------------------------------------------------- mid-interval offer_kill
 def test_mid_interval_offer_kill_keeps_results_exact(coop):
-    """Chunk-distributed intervals let demanded workgroups leave at a chunk
-    boundary (offer_kill inside the level) instead of waiting for the
-    next resizing barrier; levels / distances stay bit-exact."""
+    """Demanded workgroups leave between the items of their static share (offer_kill
+    inside the level) instead of waiting for the next resizing barrier,
+    handing the rest of their share back; the survivors run it in a replay interval
+    before the level ends.  Levels / distances stay bit-exact."""
     info = coop.device_query(0, 256)
     N = info["max_coresident"] - 1
     g = gg.rmat(18, seed=3)
     gd = _dev(g)
     s = gg.sample_sources(g, 1)[0]
     ref = tb.bfs(g, s)
-    mids = 0
+    mids = hbs = reps = 0
     for flags in (0, coop.FLAG_DIROPT):
         for q in (1, N // 2, N - 1):
             lv, st = coop.bfs(gd, s, flags=flags | coop.FLAG_CHECK, threads_per_wg=256, policy=coop.POLICY_SCHEDULER,
@@ -366,7 +367,10 @@ def test_mid_interval_offer_kill_keeps_results_exact(coop):
                               event_cap=1024)
             np.testing.assert_array_equal(lv.cpu().numpy(), ref)
             mids += st.mid_kills
-    assert mids > 0
+            hbs += st.handbacks
+            reps += st.replays
+            assert st.handbacks <= st.mid_kills and (st.replays > 0) == (st.handbacks > 0)
+    assert mids > 0 and hbs > 0 and reps > 0
     gw = SSSP_GRAPHS["grid_w"]()
     d, st = coop.sssp(_dev(gw), 0, sssp_delta=500, threads_per_wg=256, policy=coop.POLICY_SCHEDULER, task_wgs=N // 2,
                       task_blocks=N, task_block_ns=2_000, task_period_ns=10_000, flags=coop.FLAG_CHECK)

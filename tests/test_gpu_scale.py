@@ -5,9 +5,6 @@ configs[1] against Dijkstra, the 64-bit row-offset path that single-GPU RMAT-27
 needs, multitasked runs at RMAT-20, and compute-sanitizer runs of the
 cooperative kernels.  Element-by-element comparison with the oracle."""
 import os
-import shutil
-import subprocess
-import sys
 
 import numpy as np
 import pytest
@@ -102,47 +99,6 @@ def test_sssp_forced_64bit_offsets(coop):
     for s in gg.sample_sources(g, 2):
         d, _ = coop.sssp(g64, s, policy=coop.POLICY_RANDOM, resize_prob=0.3, seed=s)
         np.testing.assert_array_equal(d.cpu().numpy().view(np.uint32), tb.dijkstra(g, s))
-
-
-SANITIZE_SCRIPT = r"""
-import sys, numpy as np, torch
-sys.path.insert(0, {root!r})
-import graphgen as gg
-from oracle import textbook as tb
-from paper_1707_01989_b200 import coop
-g = gg.rmat(10, seed=1); gd = g.to("cuda")
-for s in gg.sample_sources(g, 2):
-    for kw in (dict(), dict(flags=coop.FLAG_DIROPT), dict(policy=coop.POLICY_RANDOM, resize_prob=0.5, seed=s)):
-        lv, _ = coop.bfs(gd, s, threads_per_wg=256, max_wgs=16, timeout_ns=600_000_000_000, **kw)
-        assert np.array_equal(lv.cpu().numpy(), tb.bfs(g, s)), kw
-gw = gg.with_weights(gg.grid(12, 9), seed=1); gw.max_weight = 1000
-gwd = gw.to("cuda"); gwd.max_weight = 1000
-d, _ = coop.sssp(gwd, 0, threads_per_wg=256, max_wgs=16, policy=coop.POLICY_RANDOM, resize_prob=0.5, seed=2,
-                 timeout_ns=600_000_000_000)
-assert np.array_equal(d.cpu().numpy().view(np.uint32), tb.dijkstra(gw, 0))
-print("SANITIZE_OK")
-"""
-
-
-@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
-def test_compute_sanitizer(coop, tool, tmp_path):
-    """the cooperative BFS (top-down, direction-optimising, random resizes) and
-    SSSP under compute-sanitizer, on small graphs (the tool serialises and slows the kernels)."""
-    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
-    if not os.path.exists(cs):
-        pytest.skip("compute-sanitizer not found")
-    script = tmp_path / "san.py"
-    script.write_text(SANITIZE_SCRIPT.format(root=ROOT))
-    cmd = [cs, "--tool", tool, "--error-exitcode", "9", "--target-processes", "all"]
-    if tool == "memcheck":
-        cmd += ["--leak-check", "no"]
-    r = subprocess.run(cmd + [sys.executable, str(script)], capture_output=True, text=True, timeout=900)
-    log = r.stdout + r.stderr
-    with open(os.path.join(ROOT, "gpurun_out", f"sanitizer_{tool}.log") if os.path.isdir(
-            os.path.join(ROOT, "gpurun_out")) else os.devnull, "w") as f:
-        f.write(log)
-    assert r.returncode == 0 and "SANITIZE_OK" in log, log[-4000:]
-    assert "ERROR SUMMARY: 0 errors" in log or "0 errors" in log, log[-4000:]
 
 
 @pytest.mark.parametrize("mode", ["standalone", "query", "naive"])

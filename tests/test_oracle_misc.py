@@ -49,13 +49,14 @@ def test_barrier_model_catches_known_protocol_bugs(bug, msg):
 # O4 with the kill-CAS paths the GPU runs outside the serial section (VERDICT r1 "do this" 1):
 # the query barrier's serial-section kills under host demand/withdraw/grant at any time and
 # parked CTAs leaving for task blocks; the naive barrier's arrival kill; offer_kill
-# at chunk boundaries inside an interval; the device API's bare
+# between the static items of an interval with the leaver's unrun items handed back and run by
+# the survivors in a replay interval; the device API's bare
 # offer_kill / request_fork under RANDOM and SCHEDULER decisions.
 O4_CFGS = {
     "query_scheduler_tasks": bm.Cfg(3, 3, 3, "scheduler", demand=2, withdraw=1, grant=2, tasks=True),
     "query_scheduler_M0_2": bm.Cfg(3, 2, 3, "scheduler", demand=2, withdraw=1, grant=2),
     "naive_arrival_kill": bm.Cfg(3, 3, 3, "scheduler", barrier="naive", demand=2, withdraw=1, grant=2),
-    "mid_interval_kill": bm.Cfg(3, 3, 3, "scheduler", chunks=2, demand=2, withdraw=1, grant=1),
+    "mid_interval_kill_handback": bm.Cfg(3, 3, 3, "scheduler", items=2, demand=2, withdraw=1, grant=1),
     "device_api_random": bm.Cfg(3, 2, 3, "random", bare=2),
     "device_api_scheduler": bm.Cfg(3, 2, 3, "scheduler", bare=2, demand=2, grant=2),
 }
@@ -63,19 +64,25 @@ O4_CFGS = {
 
 @pytest.mark.parametrize("name", sorted(O4_CFGS))
 def test_barrier_protocol_kill_cas_paths_exhaustive(name):
-    r = bm.explore_cfg(O4_CFGS[name])
+    cfg = O4_CFGS[name]
+    r = bm.explore_cfg(cfg)
     assert r.terminal >= 1 and r.states > 1000
-    assert r.max_gen == O4_CFGS[name].E
+    assert r.max_level == cfg.E
+    if cfg.items:
+        assert r.replays > 0 and r.max_gen > cfg.E      # hand-backs were explored, with replay intervals
 
 
 # each injected bug is a plausible protocol mistake; the property that must catch it
 @pytest.mark.parametrize("bug,cfg,prop", [
     # the mid-interval deadlock that reached hardware (fixed in 2f99910): a demanded non-top id
     # kept waiting for the top to leave although the top had already arrived
-    ("midkill_wait_arrived", bm.Cfg(3, 3, 2, "scheduler", chunks=2, demand=2), "P5"),
+    ("midkill_wait_arrived", bm.Cfg(3, 3, 2, "scheduler", items=2, demand=2), "P5"),
     # a leaver completing the episode forks N-M under a waiting policy
     ("no_cap_on_behalf", bm.Cfg(3, 2, 2, "random", bare=2), "P5"),
-    ("kill_with_chunk", bm.Cfg(3, 3, 2, "scheduler", chunks=2, demand=2), "P6"),
+    # hand-back: the leaver's unrun static items must reach the survivors, exactly once
+    ("handback_skips_item", bm.Cfg(3, 3, 2, "scheduler", items=2, demand=2), "P6"),
+    ("kill_without_handback", bm.Cfg(3, 3, 2, "scheduler", items=2, demand=2), "P6"),
+    ("no_replay", bm.Cfg(3, 3, 2, "scheduler", items=2, demand=2), "P6"),
     ("kill_any_top", bm.Cfg(3, 2, 2, "random", bare=2), "P2"),
     ("no_wait_gen", bm.Cfg(3, 2, 3, "scheduler", demand=1, grant=2), "P1"),
 ])

@@ -24,7 +24,8 @@ from paper_1707_01989_b200 import build, coop  # noqa: E402
 
 lib_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build_variants", "libcoop_ltrace.so")
 os.makedirs(os.path.dirname(lib_path), exist_ok=True)
-build.build(out=lib_path, defines=["COOP_LTRACE=1"])
+if not (os.environ.get("LT_NOBUILD") and os.path.exists(lib_path)):   # prebuilt on the CPU side
+    build.build(out=lib_path, defines=["COOP_LTRACE=1"])
 coop.load(lib_path)
 lib = ctypes.CDLL(lib_path)
 lib.coop_debug_ltrace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
@@ -33,7 +34,7 @@ flags = int(sys.argv[1]) if len(sys.argv) > 1 else coop.FLAG_DIROPT
 nsrc = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 g = gg.rmat(24, seed=1, device="cuda", chunk=1 << 26)
 out = torch.empty(g.num_vertices, dtype=torch.int32, device="cuda")
-buf = np.zeros((64, 1184, 8), dtype=np.uint64)
+buf = np.zeros((64, 1184, 12), dtype=np.uint64)
 for s in gg.sample_sources(g, nsrc, seed=2):
     for rep in range(2):
         lib.coop_debug_ltrace(None, 0)
@@ -52,11 +53,18 @@ for s in gg.sample_sources(g, nsrc, seed=2):
         rows.append({"L": L, "size": st.level_sizes[L] if L < len(st.level_sizes) else None,
                      "start": round(float(rel[:, 0].max()), 1), "end50": round(float(np.median(rel[:, 1])), 1),
                      "end_max": round(float(rel[:, 1].max()), 1), "rb1": round(float(rel[:, 2].max()), 1),
-                     "rb2": round(float(rel[:, 3].max()), 1),
+                     "rb2": round(float(rel[:, 3].max()), 1) if (t[:, 3] > 0).any() else None,
                      # warp 0 of each CTA inside expand: after the bitmap recycle, after the
                      # heavy pass, after the claimed items, after the flush (median over CTAs)
                      "w0": [round(float(np.median(rel[:, k][t[:, k] > 0])), 1) if (t[:, k] > 0).any() else None
-                            for k in (4, 5, 6, 7)]})
+                            for k in (4, 5, 6, 7)],
+                     # barrier #1 phases: last arrival (thread 0 after its atomic), the last
+                     # arriver's serial section up to the publish, after it, the last waiter
+                     # to see the release
+                     "bar": {"arr_max": round(float(rel[:, 8].max()), 1) if (t[:, 8] > 0).any() else None,
+                             "pre_pub": round(float(rel[:, 9][t[:, 9] > 0].max()), 1) if (t[:, 9] > 0).any() else None,
+                             "pub": round(float(rel[:, 10][t[:, 10] > 0].max()), 1) if (t[:, 10] > 0).any() else None,
+                             "seen_max": round(float(rel[:, 11][t[:, 11] > 0].max()), 1) if (t[:, 11] > 0).any() else None}})
         prev = int(t[:, 2].max())
     print(json.dumps({"src": s, "flags": flags, "kernel_us": st.kernel_ns / 1e3, "bu": st.bottom_up_levels,
                       "levels": rows}), flush=True)
