@@ -357,7 +357,8 @@ class SimResult:
     steps: int
     kills: int
     forks: int
-    mid_kills: int = 0           # kills at chunk boundaries inside an interval
+    mid_kills: int = 0           # kills at chunk boundaries / between items inside an interval
+    replays: int = 0             # hand-back: replay intervals run by the survivors
 
     @property
     def m_trace(self) -> list[int]:
@@ -384,18 +385,23 @@ class CoopSim:
         self.mode = mode
         if barrier not in ("desugared", "naive", "query"):
             raise ValueError(barrier)
-        if work not in ("stride", "chunk"):
+        if work not in ("stride", "chunk", "handback"):
             raise ValueError(work)
-        if work == "chunk" and d != 1:
-            raise ValueError("the chunk-counter variant is modelled at workgroup granularity (d=1): "
-                             "the GPU claims a chunk CTA-collectively")
-        if (barrier in ("naive", "query") or work == "chunk") and not isinstance(scheduler, ChannelScheduler):
+        if work in ("chunk", "handback") and d != 1:
+            raise ValueError("the chunk-counter and hand-back variants are modelled at workgroup granularity "
+                             "(d=1): the GPU decides to stop and leave CTA-collectively")
+        if work == "handback" and barrier != "query":
+            raise ValueError("hand-back runs with the query barrier (the GPU's SCHEDULER + query path)")
+        if (barrier in ("naive", "query") or work != "stride") and not isinstance(scheduler, ChannelScheduler):
             raise ValueError("naive/query barriers and mid-interval kills are driven by a ChannelScheduler")
         self.barrier = barrier
         self.gbs = 3 if barrier == "desugared" else 2     # global barriers per resizing barrier
         self.work = work
         self.chunk = chunk
         self.counter = [0, 0]                             # chunk counters of n0/n1
+        self.handed: list = []                            # hand-back: items handed back in this interval
+        self.replay_items: list = []                      # ... run by the survivors in a replay interval
+        self.replays = 0
         self.spin_W = 0                                   # query barrier: W broadcast at the release
         self.M_committed = None                           # query barrier: M - W until the spinners left
         self.mid_kills = 0
@@ -469,6 +475,11 @@ class CoopSim:
             return
         if self.barrier == "query":
             yield (GB, 0)
+            if self.replay_items:
+                # hand-back: items handed back in the interval make this episode the start of
+                # a replay interval -- the level is not over: no fork, no query (M' = M)
+                yield (GB, 1)
+                return "replay"
             if t.wg == 0:
                 yield (REQUEST_FORK, which)
                 if t.lid == 0:
@@ -574,6 +585,45 @@ class CoopSim:
             if c >= size:
                 return False
 
+    def _handback_loop(self, t: Thread):
+        """The GPU's SCHEDULER + query distribution (d=1): Fig. 4's static
+        stride over the in-queue; after each item a workgroup with id >=
+        M - demand stops and offers itself (query style); only the top id
+        can go, and it hands the items of its stride it has not run back
+        first; once some workgroup waits at the barrier the others resume and stop
+        offering for the rest of the interval.  A Kill-No-Op withdraws the hand-back."""
+        s = self.sigma
+        env = t.env
+        M = self.get_num_groups()
+        items = s.nodes[env["in_sel"]]["items"]
+        size = s.nodes[env["in_sel"]]["size"]
+        yield "step"
+        i, nostop = t.wg, False
+        while i < size:
+            node = items[i]
+            yield "step"
+            yield from self._process_node(t, node)
+            i += M
+            sched = self.sched
+            stop = not nostop and t.wg != 0 and sched.demand > 0 and t.wg + sched.demand >= self.M
+            yield "step"
+            while stop:
+                sched = self.sched
+                if sched.demand == 0 or t.wg + sched.demand < self.M:
+                    break
+                if t.wg == self.M - 1:
+                    rem = [items[j] for j in range(i, size, M)]
+                    self.handed.extend(rem)                # hand back, then offer
+                    yield (OFFER_KILL, "mid")              # accepted: this generator is dropped
+                    if rem:                                # Kill-No-Op: withdraw
+                        del self.handed[-len(rem):]
+                    break
+                if any(th.blocked is not None and th.blocked[0] == GB for th in self._active()):
+                    nostop = True                         # someone arrived: no more offers
+                    break
+                yield "step"                              # spin
+        return False
+
     def _fig4(self, t: Thread, resume):
         s = self.sigma
         env = t.env
@@ -617,6 +667,21 @@ class CoopSim:
                 env["in_sel"], env["out_sel"] = env["out_sel"], env["in_sel"]
                 yield "step"
                 yield from self._resizing_barrier(t, 1)
+                state = "after_rb1"
+                continue
+            if self.work == "handback":
+                yield from self._handback_loop(t)
+                env["in_sel"], env["out_sel"] = env["out_sel"], env["in_sel"]
+                yield "step"
+                while (yield from self._resizing_barrier(t, 1)) == "replay":
+                    # replay interval: handed-back item j runs on workgroup j mod M
+                    env["in_sel"], env["out_sel"] = env["out_sel"], env["in_sel"]
+                    M = self.get_num_groups()
+                    for j in range(t.wg, len(self.replay_items), M):
+                        yield "step"
+                        yield from self._process_node(t, self.replay_items[j])
+                    env["in_sel"], env["out_sel"] = env["out_sel"], env["in_sel"]
+                    yield "step"
                 state = "after_rb1"
                 continue
             # re-chunk: tid = get_global_id(); stride = get_global_size()
@@ -702,6 +767,9 @@ class CoopSim:
         if idx == 0:
             self._record(e)
             self.interval_M = None
+            if self.work == "handback":                   # the interval's hand-backs are final
+                self.replay_items, self.handed = self.handed, []
+                self.replays += 1 if self.replay_items else 0
         for t in active:
             t.blocked = None
             t.gb_passed += 1
@@ -792,7 +860,7 @@ class CoopSim:
         if self.mode == "bfs":
             vals = [-1 if x == INF else x for x in vals]
         return SimResult(vals, self.frontier_sizes, self.episodes, self.steps, self.kills, self.forks,
-                         self.mid_kills)
+                         self.mid_kills, self.replays)
 
 
 def simulate(g, source, *, mode="bfs", N=4, d=4, M0=None, scheduler=None, chooser=None,

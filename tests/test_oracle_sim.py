@@ -186,20 +186,21 @@ def test_enumeration_detects_a_broken_kernel(monkeypatch):
 
 
 # ---------------- the paper's two barrier implementations and chunked intervals ----------------
-VARIANTS = [(b, w) for b in ("desugared", "naive", "query") for w in ("stride", "chunk")]
+VARIANTS = [(b, w) for b in ("desugared", "naive", "query") for w in ("stride", "chunk")] + [("query", "handback")]
 
 
 @pytest.mark.parametrize("barrier,work", VARIANTS)
 def test_barrier_variants_random_channel_bfs(barrier, work):
-    """Naive and query resizing barriers and the chunk-counter
-    distribution with offer_kill at chunk boundaries: levels equal O1 and the
+    """Naive and query resizing barriers, the chunk-counter
+    distribution with offer_kill at chunk boundaries, and the GPU's static split
+    with offer_kill between items and hand-back: levels equal O1 and the
     frontier sizes equal O1's per-level counts under random interleavings and resource
     messages posted at random times."""
     g = gg.rmat(8, seed=5)
     for s in gg.sample_sources(g, 2):
         ref = tb.bfs(g, s)
         for seed in range(6):
-            d = 1 if work == "chunk" else 2
+            d = 1 if work != "stride" else 2
             sch = cs.ChannelScheduler(seed=seed, rate=0.03, budget=8)
             r = cs.simulate(g, s, N=4, d=d, M0=4, scheduler=sch, barrier=barrier, work=work, chunk=2,
                             chooser=cs.RandomChooser(seed, prims_last=seed % 2 == 0))
@@ -212,7 +213,7 @@ def test_barrier_variants_random_channel_sssp(barrier, work):
     g = gg.with_weights(gg.grid(6, 5), seed=2)
     ref = tb.dijkstra(g, 0)
     for seed in range(4):
-        d = 1 if work == "chunk" else 2
+        d = 1 if work != "stride" else 2
         sch = cs.ChannelScheduler(seed=seed, rate=0.03, budget=8)
         r = cs.simulate(g, 0, mode="sssp", N=4, d=d, M0=3, scheduler=sch, barrier=barrier, work=work,
                         chunk=3, chooser=cs.RandomChooser(seed))
@@ -259,6 +260,26 @@ def test_chunked_interval_kill_between_chunks():
     assert r.mid_kills == 1 and r.kills == 1
     rr, cc = np.divmod(np.arange(25), 5)
     np.testing.assert_array_equal(r.values, rr + cc)
+
+
+def test_handback_kill_between_items_replays_the_rest():
+    """The GPU's mid-interval offer_kill: a demanded top workgroup leaves between the
+    items of its static share and hands the rest back; the survivors run those items in a replay
+    interval before the level ends (no fork, no query there).  Levels stay equal to O1, and
+    hand-backs with items left (replay intervals) do happen under random interleavings."""
+    g = gg.rmat(8, seed=5)
+    s = gg.sample_sources(g, 1)[0]
+    ref = tb.bfs(g, s)
+    replays = mids = 0
+    for seed in range(8):
+        sch = cs.ChannelScheduler(posts={300 + 97 * seed: (2, 0), 3000 + 50 * seed: (0, 2)})
+        r = cs.simulate(g, s, N=4, d=1, M0=4, scheduler=sch, barrier="query", work="handback",
+                        chooser=cs.RandomChooser(seed))
+        np.testing.assert_array_equal(r.values, ref)
+        assert r.frontier_sizes == tb.level_sizes(ref)
+        replays += r.replays
+        mids += r.mid_kills
+    assert mids > 0 and replays > 0
 
 
 def test_naive_barrier_needs_the_published_group_count():
