@@ -489,7 +489,7 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags, 
         q = max(1, (N - 1) // 4)
         blocks = 4 * q
         block_ns = int(E_us * 1000 * (N - 1) / blocks)
-        tt, lat, gat, tasks = [], [], [], 0
+        tt, lat, gat, tasks, tedges, mk, hb, rp = [], [], [], 0, 0, 0, 0, 0
         for i in range(k + 1):
             t, (_, st) = timed(lambda: coop.bfs(g, srcs[i], out, threads_per_wg=args.threads, flags=flags,
                                                 policy=coop.POLICY_SCHEDULER, task_wgs=q, task_blocks=blocks,
@@ -498,6 +498,10 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags, 
             if i:
                 tt.append(t)
                 tasks += st.tasks_completed
+                mk += st.mid_kills
+                hb += st.handbacks
+                rp += st.replays
+                tedges += int(deg[out >= 0].sum().item()) // 2     # Graph500 count (R18), untimed
                 if not args.no_verify:
                     checked.append((srcs[i], out.clone()))          # multitasked levels: same oracle
                 for e in st.task_events:
@@ -514,7 +518,8 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags, 
                     "slowdown_vs_standalone": statistics.median(tt) / statistics.median(t_coop),
                     "kill_latency_us_p50": pct(lat, 0.5), "kill_latency_us_p99": pct(lat, 0.99),
                     "gather_us_p50": pct(gat, 0.5), "gather_us_p99": pct(gat, 0.99),
-                    "tasks_completed": tasks, "gteps": None}
+                    "tasks_completed": tasks, "gteps": tedges / (sum(tt) * 1e-3) / 1e9,
+                    "mid_kills": mk, "handbacks": hb, "replays": rp}
     ex["multitask"] = mt
     # the paper's presets at Q = N/4 (query barrier), BFS looped over sources inside ONE
     # launch for >= 10 s per cell; the full preset x Q x barrier grid is

@@ -48,6 +48,9 @@
 #ifndef COOP_SSSP_PRECHECK
 #define COOP_SSSP_PRECHECK 0  // SSSP: read dist[v] before the atomicMin (fewer atomics, one more dependent round trip: 73.4 vs 68.4 ms on the 2048^2 grid without it)
 #endif
+#ifndef COOP_PROBE_NO_LEVELS
+#define COOP_PROBE_NO_LEVELS 0   // measurement only (wrong output): drop the level stores of claims
+#endif
 #ifndef COOP_BU_DENSE_W
 #define COOP_BU_DENSE_W 16    // bottom-up (compacted): words per item in the first (dense) level
 #endif
@@ -106,6 +109,17 @@ __device__ __forceinline__ unsigned long long ld_hint(const unsigned long long *
 #define LDS(ptr) __ldg(ptr)
 #endif
 
+// BFS levels during the traversal: one byte per vertex (lv8[v] = level + 1, 0 = not
+// reached, 255 = level >= 254, whose int32 is stored directly), 16 MB at RMAT-24 and so
+// L2-resident -- the claims' scattered stores no longer read-modify-write sectors of the
+// 67 MB int32 output in HBM (7 % of the kernel, build variant COOP_PROBE_NO_LEVELS).  The
+// output is written once, coalesced, when the frontier empties (BfsApp::empty).
+__device__ __forceinline__ void store_level(const KParams &p, int64_t v, uint32_t L) {
+    if (COOP_PROBE_NO_LEVELS) return;
+    p.lv8[v] = (uint8_t)(L < 254u ? L + 1u : 255u);
+    if (L >= 254u) p.level_out[v] = (int32_t)L;
+}
+
 template <typename OffT, bool KCOOP = true>
 struct BfsApp {
     static constexpr bool kCoop = KCOOP;
@@ -121,22 +135,11 @@ struct BfsApp {
         const uint64_t tid = (uint64_t)cs.lid * BLOCK + threadIdx.x;
         const uint64_t nth = (uint64_t)cs.M * BLOCK;
         const int64_t V = p.V, s = run_source(p);
-        int32_t *lv = p.level_out;
-        // level[v] = -1 (unreached, reading R10), level[s] = 0; 16-B vector stores on the aligned body
-        const uint64_t head = ((16 - ((uintptr_t)lv & 15)) & 15) / 4;
-        const uint64_t h = head < (uint64_t)V ? head : (uint64_t)V;
-        for (uint64_t i = tid; i < h; i += nth) lv[i] = (int64_t)i == s ? 0 : -1;
-        const uint64_t nvec = ((uint64_t)V - h) / 4;
-        int4 *lv4 = reinterpret_cast<int4 *>(lv + h);
-        for (uint64_t i = tid; i < nvec; i += nth) {
-            int4 x = make_int4(-1, -1, -1, -1);
-            const int64_t b = (int64_t)(h + 4 * i);
-            if (s >= b && s < b + 4) {
-                if (s == b) x.x = 0; else if (s == b + 1) x.y = 0; else if (s == b + 2) x.z = 0; else x.w = 0;
-            }
-            lv4[i] = x;
-        }
-        for (uint64_t i = h + 4 * nvec + tid; i < (uint64_t)V; i += nth) lv[i] = (int64_t)i == s ? 0 : -1;
+        // lv8[v] = 0 (not reached), lv8[s] = 1 (level 0): 4 bytes per thread, the mapping the
+        // output pass of empty() uses, so a source-loop restart never races a slower CTA's pass
+        uint32_t *l4 = reinterpret_cast<uint32_t *>(p.lv8);
+        const uint64_t n4 = ((uint64_t)V + 3) / 4;
+        for (uint64_t i = tid; i < n4; i += nth) l4[i] = (uint64_t)(s >> 2) == i ? 1u << (8 * (s & 3)) : 0u;
         const uint64_t nw = ((uint64_t)V + 31) / 32;
         const uint32_t sw = (uint32_t)(s >> 5), sb = 1u << (s & 31);
         const bool dead_from_iso = p.dopt && COOP_INIT_DEAD && p.iso != nullptr;
@@ -247,7 +250,32 @@ struct BfsApp {
             cs.app_u32[6] = c->n_bu_levels;                  // 1 during the first bottom-up level
         }
         cta_sync();
-        return cs.app_u32[4] == 0;
+        const bool done = cs.app_u32[4] == 0;
+        if (done) {
+            // the traversal's output, once: levels = lv8 - 1 (-1 unreached, reading R10); every
+            // active CTA its stride, 4 vertices per thread (one coalesced 4-B load, 16-B store)
+            const uint64_t V = (uint64_t)p.V, n4 = (V + 3) / 4, nth = (uint64_t)cs.M * blockDim.x;
+            const uint32_t *l4 = reinterpret_cast<const uint32_t *>(p.lv8);
+            for (uint64_t i = (uint64_t)cs.lid * blockDim.x + threadIdx.x; i < n4; i += nth) {
+                const uint32_t b = __ldcg(l4 + i);
+                int32_t o[4];
+                bool direct = false;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t x = (b >> (8 * k)) & 0xFFu;
+                    o[k] = (int32_t)x - 1;
+                    direct |= x == 255u && 4 * i + k < V;
+                }
+                if (!direct && 4 * i + 4 <= V && ((uintptr_t)p.level_out & 15) == 0) {
+                    *reinterpret_cast<int4 *>(p.level_out + 4 * i) = make_int4(o[0], o[1], o[2], o[3]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (4 * i + k < V && ((b >> (8 * k)) & 0xFFu) != 255u) p.level_out[4 * i + k] = o[k];
+                }
+            }
+        }
+        return done;
     }
 
     static constexpr uint32_t kQueueRes = 256;   // per-warp queue reservation (>= 2 * 32 * KB)
@@ -295,7 +323,7 @@ struct BfsApp {
             nb[k] = 0;
             nd[k] = 0;
             if (win[k]) {
-                p.level_out[u[k]] = (int32_t)L1;
+                store_level(p, u[k], L1);
                 nb[k] = __ldg(ro + u[k]);
                 nd[k] = (uint32_t)(__ldg(ro + u[k] + 1) - nb[k]);
                 mfsum += nd[k];
@@ -595,7 +623,7 @@ struct BfsApp {
         for (int k = 0; k < KW; ++k) {
             const uint32_t wins = __ballot_sync(FULL, found[k]);
             if (found[k]) {
-                p.level_out[(w0 + k) * 32 + lane] = (int32_t)L1;
+                store_level(p, (int64_t)((w0 + k) * 32 + lane), L1);
                 mfsum += deg[k];
             }
             if (wins | dead[k]) {
@@ -783,7 +811,7 @@ struct BfsApp {
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 if (found[k]) {
-                    p.level_out[(w0 + own[k]) * 32 + bit[k]] = (int32_t)L1;
+                    store_level(p, (int64_t)((w0 + own[k]) * 32 + bit[k]), L1);
                     atomicOr(&s_found[own[k]], 1u << bit[k]);
                     mfsum += deg[k];
                 }
@@ -802,8 +830,11 @@ struct BfsApp {
 
     static constexpr uint32_t BU_KW = COOP_BU_KW;  // bottom-up: words per warp item
 
-    // per-warp counters -> control block (CTA-collective; before a mid-interval
-    // kill and at the end of the interval: nf decides termination)
+    // per-warp counters -> the CTA's shared accumulators (before a mid-interval kill and at
+    // the end of the interval); thread 0 adds them to the control block right before the
+    // CTA's arrival / kill-CAS (pre_arrive), whose release orders them -- one global atomic
+    // per counter per CTA instead of one per warp plus a fence per warp (4736 warps hit the
+    // same line at the end of every level)
     __device__ __forceinline__ void flush_counts(const KParams &p, CtaState &cs, uint32_t out, uint64_t &edges,
                                                  uint32_t &reached, uint64_t &mfsum) {
         const uint32_t lane = threadIdx.x & 31;
@@ -817,17 +848,25 @@ struct BfsApp {
             if (e) atomicAdd(&cs.edges, (unsigned long long)(e / 32));
             if (reached) {
                 atomicAdd(&cs.reached, (unsigned long long)reached);
-                atomicAdd(&p.ctl->nf[out], (unsigned long long)reached);
+                atomicAdd(&cs.acc[0], (unsigned long long)reached);
             }
-            if (m) atomicAdd(&p.ctl->mf[out], (unsigned long long)m);
-            // the reductions above are fire-and-forget (RED): make them performed before
-            // this warp reaches the CTA barrier that precedes the arrival (the serial
-            // section reads nf / mf; nf decides termination)
-            if (reached || m) __threadfence();
+            if (m) atomicAdd(&cs.acc[1], (unsigned long long)m);
+            cs.acc_sel = out;
         }
         edges = 0;
         reached = 0;
         mfsum = 0;
+    }
+
+    // thread 0, after the CTA barrier that follows every warp's flush_counts, before the
+    // arrival or kill-CAS (both release): the level's counters (nf decides termination)
+    __device__ __forceinline__ void pre_arrive(const KParams &p, CtaState &cs) {
+        const unsigned long long nf = cs.acc[0], mf = cs.acc[1];
+        if (nf | mf) {
+            if (nf) atomicAdd(&p.ctl->nf[cs.acc_sel], nf);
+            if (mf) atomicAdd(&p.ctl->mf[cs.acc_sel], mf);
+            cs.acc[0] = cs.acc[1] = 0;
+        }
     }
 
     template <int BLOCK, int DIST = DIST_STATIC>
@@ -966,6 +1005,7 @@ constexpr uint32_t kNoRound = 0xFFFFFFFFu;   // low word of an SSSP key not push
 template <typename OffT, bool KCOOP = true>
 struct SsspApp {
     static constexpr bool kCoop = KCOOP;
+    __device__ void pre_arrive(const KParams &, CtaState &) {}
     __device__ bool next_run(const KParams &, CtaState &) { return false; }
     __device__ void enter(const KParams &, CtaState &) {}
     template <int BLOCK>
@@ -1228,6 +1268,7 @@ struct SsspApp {
 // across the barrier).  iters resizing barriers in total.
 struct BarrierApp {
     static constexpr bool kCoop = true;
+    __device__ void pre_arrive(const KParams &, CtaState &) {}
     __device__ bool next_run(const KParams &, CtaState &) { return false; }
     __device__ void enter(const KParams &, CtaState &cs) {
         if (threadIdx.x == 0) cs.app_u32[4] = 0;   // no previous interval for a (re)entered CTA

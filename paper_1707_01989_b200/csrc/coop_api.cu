@@ -227,6 +227,7 @@ struct Scratch {
     DevBuf nccl_aux;                  // NCCL data plane: ready, gathered, count send/recv slots
     DevBuf runt;                      // source loop: end time of every run
     DevBuf rep;                       // hand-back entries of mid-interval offer_kill [P][W]
+    DevBuf lv8;                       // BFS: one level byte per vertex during the traversal
     cudaEvent_t done_ev = nullptr;    // handle API: the control block's copy back has landed
     volatile uint32_t *nccl_host = nullptr;     // mapped host mirror of `ready`
     void *nccl_warm = nullptr;                  // communicator already warmed up on nccl_stream
@@ -637,6 +638,8 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
         // slots, refills hold >= 128 entries) plus one open reservation per warp
         const size_t qcap = 2 * V + (size_t)P * (threads / 32) * 256;
         CUDA_TRY(s->visited.ensure(4 * ((V + 31) / 32)));
+        CUDA_TRY(s->lv8.ensure(4 * ((V + 3) / 4)));
+        kp.lv8 = static_cast<uint8_t *>(s->lv8.p);
         CUDA_TRY(s->ql0.ensure(le * qcap));
         CUDA_TRY(s->ql1.ensure(le * qcap));
         const size_t nh = E / kHeavyDeg + 1;

@@ -270,7 +270,7 @@ __device__ void fig4_body(coop_ctx *ctx, const F4Params &p) {
 }
 
 template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) fig4_kernel(coop_dev *d, F4Params p) {
+__global__ void __launch_bounds__(BLOCK) fig4_kernel(coop_dev *d, const __grid_constant__ F4Params p) {
     coop_run(d, [&](coop_ctx *ctx) { fig4_body<BLOCK>(ctx, p); });
 }
 
@@ -446,7 +446,7 @@ __device__ void ws_body(coop_ctx *ctx, const WsParams &p) {
 }
 
 template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) ws_kernel(coop_dev *d, WsParams p) {
+__global__ void __launch_bounds__(BLOCK) ws_kernel(coop_dev *d, const __grid_constant__ WsParams p) {
     coop_run(d, [&](coop_ctx *ctx) { ws_body<BLOCK>(ctx, p); });
 }
 
@@ -740,7 +740,7 @@ __device__ void psssp_body(coop_ctx *ctx, const PnParams &p) {
 }
 
 template <int BLOCK, int APP>
-__global__ void __launch_bounds__(BLOCK) pannotia_kernel(coop_dev *d, PnParams p) {
+__global__ void __launch_bounds__(BLOCK) pannotia_kernel(coop_dev *d, const __grid_constant__ PnParams p) {
     coop_run(d, [&](coop_ctx *ctx) {
         if (APP == 0) color_body<BLOCK>(ctx, p);
         else if (APP == 1) mis_body<BLOCK>(ctx, p);

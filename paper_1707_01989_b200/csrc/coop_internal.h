@@ -207,6 +207,7 @@ struct KParams {
     int64_t source;
     // outputs
     int32_t *level_out;
+    uint8_t *lv8;               // BFS: level + 1 per vertex during the traversal (apps.cuh store_level)
     uint32_t *dist_out;
     // scratch
     Ctl *ctl;

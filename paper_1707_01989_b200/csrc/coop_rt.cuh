@@ -79,6 +79,15 @@
 #define COOP_WARP_WAIT 1      // waiters poll the release word with all of warp 0 (converged at the CTA barrier)
 #endif
 
+#ifndef COOP_POLL_CYCLES
+#define COOP_POLL_CYCLES 2000 // DIST_MID: a CTA reads the demand word at most once per this many SM
+                              // cycles (~1 us; every warp reading it with every item: 4736 warps on
+                              // one L2 line, +12 % kernel time on RMAT-24)
+#endif
+#ifndef COOP_MID_INLINE
+#define COOP_MID_INLINE 0     // 1: the DIST_MID / DIST_REPLAY expand instances inlined into run_body
+#endif
+
 #ifndef COOP_TRACE
 #define COOP_TRACE 0          // 1: clock64 breakdown of the barrier, CTA 0 (coop_debug_trace)
 #endif
@@ -201,11 +210,13 @@ struct CtaState {
     uint32_t stop, nostop;                         // DIST_MID: asked to surrender / stop offering this interval
     uint32_t replay, rep_M;                        // a replay interval follows this barrier; survivors' M in it
     uint32_t rk[32];                               // DIST_MID: next static item index per warp
+    unsigned long long poll_t;                     // DIST_MID: %globaltimer of the CTA's last demand poll
 #if COOP_TRACE
     unsigned long long tr[12];
     long long tr_last;
 #endif
-    unsigned long long acc[2];                     // app counters flushed before a mid-interval kill
+    unsigned long long acc[2];                     // app per-CTA level counters (BFS: nf, mf), added to the
+    uint32_t acc_sel;                              //   control block by pre_arrive; their parity
     uint32_t app_u32[8];                           // app broadcast scratch
 };
 
@@ -397,6 +408,7 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
 #endif
     if (threadIdx.x == 0) {
         const uint32_t g = cs.gen;
+        app.pre_arrive(p, cs);                           // the CTA's counters, released by the arrival
         if (cs.lid == 0 && (p.flags & COOP_FLAG_CHECK)) {  // WG 0's transmit state, for the check
             c->tx0.level = cs.level;
             c->tx0.in_sel = cs.in_sel;
@@ -620,6 +632,7 @@ __device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, 
     for (uint32_t spins = 0;;) {
         if (threadIdx.x == 0) {
             uint32_t act = ACT_CONT, serial = 0, Mnew = 0;
+            app.pre_arrive(p, cs);
             __threadfence();                               // release this CTA's work of the interval
             unsigned long long w = ld_relaxed64(&c->W);
             for (;;) {
@@ -750,39 +763,43 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
             return ACT_CONT;
         } else {
             volatile uint32_t *stopf = &cs.stop;
-            if (threadIdx.x == 0) { cs.stop = 0; cs.nostop = 0; }
+            volatile unsigned long long *pollt = &cs.poll_t;
+            if (threadIdx.x == 0) { cs.stop = 0; cs.nostop = 0; cs.poll_t = clock64(); }
             cta_sync();
-            // has this CTA been asked to surrender?  (lane 0; d was loaded before the item)
-            auto asked = [&](uint32_t d) {
-                return d && cs.lid != 0 && !cs.nostop && cs.lid + d >= w_M(ld_relaxed64(&p.ctl->W));
+            // lane 0, after an item: read the demand word if COOP_POLL_CYCLES passed since the
+            // CTA's last read (whichever warp is first), and raise the CTA's stop flag if this
+            // id is asked to surrender.  Nothing of it is live across the item (the item's
+            // registers are the static loop's), and only the polling warp waits for the load.
+            auto poll = [&]() {
+                const unsigned long long now = clock64();     // the SM's clock: cheap, CTA-consistent
+                if (cs.lid == 0 || cs.nostop || now - *pollt < COOP_POLL_CYCLES) return;
+                *pollt = now;
+                const uint32_t d = ld_relaxed32(&p.ctl->demand);
+                if (d && cs.lid + d >= w_M(ld_relaxed64(&p.ctl->W))) *stopf = 1u;
             };
-            uint64_t k = 0;
+            // lane 0 decides, the warp follows (fn is warp-collective)
+            auto stopped = [&]() { return __shfl_sync(FULL, lane == 0 ? *stopf : 0u, 0) != 0; };
+            uint64_t it = gw;
             for (;;) {
-                // lane 0 decides, the warp follows (fn is warp-collective)
-                auto stopped = [&]() { return __shfl_sync(FULL, lane == 0 ? *stopf : 0u, 0) != 0; };
-                for (;; ++k) {
-                    const uint64_t it = gw + k * TW;
-                    if (it >= n_static || stopped()) break;
-                    uint32_t d = 0;
-                    if (lane == 0) d = ld_relaxed32(&p.ctl->demand);
+                for (; it < n_static; it += TW) {
+                    if (stopped()) break;
                     fn(it);
-                    if (lane == 0 && asked(d)) *stopf = 1u;
+                    if (lane == 0) poll();
                 }
-                if (lane == 0) cs.rk[warp] = (uint32_t)k;
+                if (lane == 0) cs.rk[warp] = (uint32_t)((it - gw) / TW);
                 if (tail16 && n_static < n_items && !stopped()) {
                     uint32_t t = 0;
                     if (lane == 0) t = atomicAdd(counter, 1u);
                     for (;;) {
-                        const uint64_t it = n_static + __shfl_sync(FULL, t, 0);
-                        if (it >= n_items) break;
-                        uint32_t d = 0, more = 0;
+                        const uint64_t ti = n_static + __shfl_sync(FULL, t, 0);
+                        if (ti >= n_items) break;
+                        uint32_t more = 0;
                         if (lane == 0) {
                             more = *stopf ? 0u : 1u;
                             if (more) t = atomicAdd(counter, 1u);     // next claim in flight
-                            d = ld_relaxed32(&p.ctl->demand);
                         }
-                        fn(it);                                       // a claimed item is always run
-                        if (lane == 0 && asked(d)) *stopf = 1u;
+                        fn(ti);                                       // a claimed item is always run
+                        if (lane == 0) poll();
                         if (!__shfl_sync(FULL, more, 0)) break;
                     }
                 }
@@ -790,7 +807,6 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
                 if (!cs.stop) return ACT_CONT;
                 const uint32_t r = offer_kill_mid<BLOCK>(p, cs, app, flush, n_static, TW);
                 if (r != ACT_CONT) return r;                          // killed (or abort): nothing stranded
-                k = cs.rk[warp];
             }
         }
     }
@@ -798,8 +814,13 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
 
 // ---------------------------------------------------------------- body
 // the expand instances of the scheduler-armed path (DIST_MID, DIST_REPLAY) out of line
+#if COOP_MID_INLINE
+#define COOP_EXPAND_DIST_ATTR __forceinline__
+#else
+#define COOP_EXPAND_DIST_ATTR __noinline__
+#endif
 template <class App, int BLOCK, int DIST>
-__device__ __noinline__ uint32_t expand_dist(const KParams &p, CtaState &cs, App &app) {
+__device__ COOP_EXPAND_DIST_ATTR uint32_t expand_dist(const KParams &p, CtaState &cs, App &app) {
     return app.template expand<BLOCK, DIST>(p, cs);
 }
 
@@ -1085,6 +1106,7 @@ __device__ __forceinline__ void kernel_body(const KParams &p, CtaState &cs, App 
         cs.consumed = 0;
         cs.wait_rel = 0;
         cs.lid = blockIdx.x; cs.M = p.M0; cs.gen = 0; cs.level = 0; cs.in_sel = 0;
+        cs.acc[0] = cs.acc[1] = 0; cs.acc_sel = 0;
         if (blockIdx.x == 0) p.ctl->t_start = t0;
     }
     cta_sync();
@@ -1117,8 +1139,11 @@ __device__ __forceinline__ void kernel_body(const KParams &p, CtaState &cs, App 
 }
 
 
+// __grid_constant__: the parameter block is addressed in place by the out-of-line runtime
+// functions (const KParams &), so no thread copies the ~0.9 KB struct to its stack at launch
+// (without it every thread of the grid did: ~140 MB of local-memory stores per launch)
 template <class App, int BLOCK, int MINB>
-__global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(KParams p) {
+__global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(const __grid_constant__ KParams p) {
     __shared__ CtaState cs;
     __shared__ uint32_t s_last;
     App app;

@@ -31,6 +31,12 @@ lib = ctypes.CDLL(lib_path)
 lib.coop_debug_ltrace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 
 flags = int(sys.argv[1]) if len(sys.argv) > 1 else coop.FLAG_DIROPT
+# LT_POLICY=scheduler: the scheduler-armed arm (scheduler CTA, no task), N-1 workers
+extra = {}
+if os.environ.get("LT_POLICY") == "scheduler":
+    extra = dict(policy=coop.POLICY_SCHEDULER)
+if os.environ.get("LT_WORKERS"):
+    extra["max_wgs"] = int(os.environ["LT_WORKERS"])
 nsrc = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 g = gg.rmat(24, seed=1, device="cuda", chunk=1 << 26)
 out = torch.empty(g.num_vertices, dtype=torch.int32, device="cuda")
@@ -38,7 +44,7 @@ buf = np.zeros((64, 1184, 12), dtype=np.uint64)
 for s in gg.sample_sources(g, nsrc, seed=2):
     for rep in range(2):
         lib.coop_debug_ltrace(None, 0)
-        _, st = coop.bfs(g, s, out, threads_per_wg=512, flags=flags, level_cap=64)
+        _, st = coop.bfs(g, s, out, threads_per_wg=512, flags=flags, level_cap=64, **extra)
     torch.cuda.synchronize()
     rc = lib.coop_debug_ltrace(buf.ctypes.data, buf.size)
     assert rc == 0

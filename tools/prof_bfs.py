@@ -22,6 +22,8 @@ ap.add_argument("--n", type=int, default=1)
 ap.add_argument("--threads", type=int, default=512)
 ap.add_argument("--app", default="bfs")
 ap.add_argument("--flags", type=int, default=2, help="2 = COOP_FLAG_DIROPT, 0 = top-down")
+ap.add_argument("--policy", default="never", help="never | scheduler (the armed arm: scheduler CTA, no task)")
+ap.add_argument("--src", type=int, default=-1, help="fixed source index (default: cycle over 8)")
 args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
@@ -30,7 +32,10 @@ if args.app == "bfs":
     srcs = gg.sample_sources(g, 8, seed=2)
     out = torch.empty(g.num_vertices, dtype=torch.int32, device=dev)
     for i in range(args.warm + args.n):
-        _, st = coop.bfs(g, srcs[i % 8], out, threads_per_wg=args.threads, flags=args.flags)
+        kw = dict(policy=coop.POLICY_SCHEDULER) if args.policy == "scheduler" else {}
+        N = coop.device_query(0, args.threads)["max_coresident"] - 1
+        s = srcs[args.src] if args.src >= 0 else srcs[i % 8]
+        _, st = coop.bfs(g, s, out, threads_per_wg=args.threads, flags=args.flags, max_wgs=N, **kw)
         print(f"call {i}: kernel_ms={st.kernel_ns / 1e6:.3f} edges={st.edges_scanned} levels={st.levels}", flush=True)
 else:
     g = gg.with_weights(gg.grid(2048, 2048, device=dev), seed=1)
