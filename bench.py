@@ -419,6 +419,8 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags, 
     ex = {}
     N = info["max_coresident"]
 
+    deg = g.degrees()                   # Graph500 edge counts of the multitasked runs (R18)
+
     def timed(fn):
         flush.fill_(1)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -48,6 +48,18 @@
 #ifndef COOP_SSSP_PRECHECK
 #define COOP_SSSP_PRECHECK 0  // SSSP: read dist[v] before the atomicMin (fewer atomics, one more dependent round trip: 73.4 vs 68.4 ms on the 2048^2 grid without it)
 #endif
+#ifndef COOP_SERIAL_INLINE
+#define COOP_SERIAL_INLINE 1  // BFS serial-section work inlined (out of line, its parameter reads are generic
+                              // loads through the __grid_constant__ pointer, on the barrier's critical path)
+#endif
+#if COOP_SERIAL_INLINE
+#define COOP_SERIAL_ATTR __forceinline__
+#else
+#define COOP_SERIAL_ATTR __noinline__
+#endif
+#ifndef COOP_TD_SPEC_RO
+#define COOP_TD_SPEC_RO 0     // top-down claims: load the candidate's offsets alongside the claim atomic
+#endif
 #ifndef COOP_PROBE_NO_LEVELS
 #define COOP_PROBE_NO_LEVELS 0   // measurement only (wrong output): drop the level stores of claims
 #endif
@@ -307,25 +319,36 @@ struct BfsApp {
 #pragma unroll
         for (int k = 0; k < K; ++k) cur[k] = u[k] >= 0 ? vis[(uint32_t)u[k] >> 5] : 0xFFFFFFFFu;  // pre-check
         bool win[K];
+        const OffT *ro = static_cast<const OffT *>(p.ro);
+        OffT nb[K], ne[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             win[k] = false;
+            nb[k] = ne[k] = 0;
             if (u[k] >= 0) {
                 const uint32_t bit = 1u << (u[k] & 31);
-                if (!(cur[k] & bit)) win[k] = !(atomicOr(vis + ((uint32_t)u[k] >> 5), bit) & bit);   // claim
+                if (!(cur[k] & bit)) {
+                    win[k] = !(atomicOr(vis + ((uint32_t)u[k] >> 5), bit) & bit);   // claim
+#if COOP_TD_SPEC_RO
+                    // the candidate's offsets alongside the claim (independent of its result):
+                    // one dependent round trip less per batch for the winners
+                    nb[k] = __ldg(ro + u[k]);
+                    ne[k] = __ldg(ro + u[k] + 1);
+#endif
+                }
             }
         }
-        const OffT *ro = static_cast<const OffT *>(p.ro);
-        OffT nb[K];
         uint32_t nd[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            nb[k] = 0;
             nd[k] = 0;
             if (win[k]) {
                 store_level(p, u[k], L1);
+#if !COOP_TD_SPEC_RO
                 nb[k] = __ldg(ro + u[k]);
-                nd[k] = (uint32_t)(__ldg(ro + u[k] + 1) - nb[k]);
+                ne[k] = __ldg(ro + u[k] + 1);
+#endif
+                nd[k] = (uint32_t)(ne[k] - nb[k]);
                 mfsum += nd[k];
                 if (fnext) atomicOr(fnext + ((uint32_t)u[k] >> 5), 1u << (u[k] & 31));
             }
@@ -882,7 +905,10 @@ struct BfsApp {
         uint32_t reached = 0;
         const uint32_t mode = cs.app_u32[5];
         uint32_t *fnext = p.dopt ? p.fbits[(cs.level + 1) % 3] : nullptr;
-        if (p.dopt && DIST != DIST_REPLAY) {   // recycle the bitmap of level L-1 as the next-next frontier (static split)
+        // (a DIST_MID expand resumed after an offer_kill that did not take this CTA skips
+        // the static-split steps it has done already)
+        const bool first = DIST == DIST_STATIC || (DIST == DIST_MID && !cs.resume);
+        if (p.dopt && first) {   // recycle the bitmap of level L-1 as the next-next frontier (static split)
             uint32_t *fold = p.fbits[(cs.level + 2) % 3];
             const uint64_t nw = ((uint64_t)p.V + 31) / 32;
             for (uint64_t i = (uint64_t)cs.lid * BLOCK + threadIdx.x; i < nw; i += (uint64_t)cs.M * BLOCK) fold[i] = 0u;
@@ -916,7 +942,7 @@ struct BfsApp {
                 tdb_group(p, cs, g, fnext, edges, reached, mfsum, res);
             }, flush, COOP_TD_TAIL);
         } else {                                              // item = 32 light frontier entries
-            if (DIST != DIST_REPLAY) expand_heavy(p, cs, gw, TW, fnext, edges, reached, mfsum, res);
+            if (first) expand_heavy(p, cs, gw, TW, fnext, edges, reached, mfsum, res);
             LTRACE(5);
             // entries per warp item: 32 (a full gather) when there are enough items for
             // every warp, else fewer, down to one list per warp -- a small frontier of
@@ -937,7 +963,7 @@ struct BfsApp {
     // Fig. 4 between the barriers: reset(out_nodes); per-level statistics; the
     // direction of the next level (Beamer: TD->BU if m_f > m_u/alpha, BU->TD if
     // n_f < V/beta)
-    __device__ __noinline__ void serial(const KParams &p, CtaState &cs, uint32_t entry, bool resizing) {
+    __device__ COOP_SERIAL_ATTR void serial(const KParams &p, CtaState &cs, uint32_t entry, bool resizing) {
         if (resizing && entry == ENTRY_RESTART) { init_ctl(p, run_source(p)); return; }
         if (!resizing || entry != ENTRY_AFTER_RB1) return;
         Ctl *c = p.ctl;

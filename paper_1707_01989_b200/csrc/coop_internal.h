@@ -12,7 +12,8 @@ constexpr uint64_t kMask40 = (1ull << 40) - 1;
 
 // runtime actions broadcast inside a CTA
 enum : uint32_t { ACT_CONT = 0, ACT_KILLED = 1, ACT_DONE = 2, ACT_ABORT = 3, ACT_RUN_BODY = 4,
-                  ACT_RUN_TASK = 5, ACT_EXIT = 6, ACT_IDLE = 7 };
+                  ACT_RUN_TASK = 5, ACT_EXIT = 6, ACT_IDLE = 7,
+                  ACT_STOP = 8 };   // DIST_MID: asked to surrender mid-interval (counters flushed)
 // body entry points (the paper's "designated point within the kernel")
 // ENTRY_RESTART: the resizing barrier after a new run's init (BFS source loop); a CTA
 // forked there starts at the loop head like ENTRY_AFTER_RB2

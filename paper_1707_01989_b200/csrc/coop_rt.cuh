@@ -87,6 +87,9 @@
 #ifndef COOP_MID_INLINE
 #define COOP_MID_INLINE 0     // 1: the DIST_MID / DIST_REPLAY expand instances inlined into run_body
 #endif
+#ifndef COOP_MID_UNIFIED
+#define COOP_MID_UNIFIED 0    // 1: every policy runs the DIST_MID instance (inline), its checks gated at run time
+#endif
 
 #ifndef COOP_TRACE
 #define COOP_TRACE 0          // 1: clock64 breakdown of the barrier, CTA 0 (coop_debug_trace)
@@ -208,6 +211,8 @@ struct CtaState {
     uint32_t bar_M, bar_naive;                     // barrier: M of the episode, killed on entry (NAIVE)
     uint32_t wait_rel;                             // barrier: this CTA waits for the release word
     uint32_t stop, nostop;                         // DIST_MID: asked to surrender / stop offering this interval
+    uint32_t resume;                               // DIST_MID: expand re-entered after an offer that did not kill
+    uint64_t hb_n, hb_tw;                          // DIST_MID: static items / warp stride of the interval (hand-back)
     uint32_t replay, rep_M;                        // a replay interval follows this barrier; survivors' M in it
     uint32_t rk[32];                               // DIST_MID: next static item index per warp
     unsigned long long poll_t;                     // DIST_MID: %globaltimer of the CTA's last demand poll
@@ -215,6 +220,10 @@ struct CtaState {
     unsigned long long tr[12];
     long long tr_last;
 #endif
+    const KParams *sp;                             // the CTA's shared-memory copy of the kernel parameters:
+                                                   // what the out-of-line functions read (a generic load
+                                                   // through the __grid_constant__ parameter's address
+                                                   // is slow; inlined code keeps the constant bank)
     unsigned long long acc[2];                     // app per-CTA level counters (BFS: nf, mf), added to the
     uint32_t acc_sel;                              //   control block by pre_arrive; their parity
     uint32_t app_u32[8];                           // app broadcast scratch
@@ -331,7 +340,7 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
         Transmit tx0;
         tx0.level = cs.level;
         tx0.in_sel = cs.in_sel;
-        got = fork_from_pool(p, cs, g + 1, M, Mp - M, entry, tx0, wait_fork);
+        got = fork_from_pool(*cs.sp, cs, g + 1, M, Mp - M, entry, tx0, wait_fork);
         Mp = M + got;
     }
     if (lane == 0) {
@@ -622,13 +631,14 @@ __device__ __forceinline__ uint32_t hand_back(const KParams &p, CtaState &cs, ui
     return idx;
 }
 
-template <int BLOCK, class App, class Flush>
-__device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, App &app, Flush &&flush, uint64_t n,
-                                                uint64_t TW) {
+// (the caller flushes the CTA's counters first, inline: a flush lambda handed to this
+// out-of-line function would make the warps' per-item accumulators address-taken, i.e.
+// live on the stack through every item -- measured: +16 M L2 sectors, +13 % kernel time)
+template <int BLOCK, class App>
+__device__ __noinline__ uint32_t offer_kill_mid(const KParams &p, CtaState &cs, App &app) {
     constexpr uint32_t WPB = BLOCK / 32;
     Ctl *c = p.ctl;
-    flush();
-    cta_sync();
+    const uint64_t n = cs.hb_n, TW = cs.hb_tw;
     for (uint32_t spins = 0;;) {
         if (threadIdx.x == 0) {
             uint32_t act = ACT_CONT, serial = 0, Mnew = 0;
@@ -764,12 +774,18 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
         } else {
             volatile uint32_t *stopf = &cs.stop;
             volatile unsigned long long *pollt = &cs.poll_t;
-            if (threadIdx.x == 0) { cs.stop = 0; cs.nostop = 0; cs.poll_t = clock64(); }
+            const bool resumed = cs.resume != 0;
+            if (threadIdx.x == 0) {
+                cs.stop = 0;
+                if (!resumed) cs.nostop = 0;                       // kept by a resumed interval
+                cs.poll_t = clock64();
+            }
             cta_sync();
-            // lane 0, after an item: read the demand word if COOP_POLL_CYCLES passed since the
-            // CTA's last read (whichever warp is first), and raise the CTA's stop flag if this
-            // id is asked to surrender.  Nothing of it is live across the item (the item's
-            // registers are the static loop's), and only the polling warp waits for the load.
+            // Each warp checks, at most once per COOP_POLL_CYCLES of its own clock (one clock
+            // read and a vote per item, one register live across the item): the CTA's stop flag,
+            // and -- lane 0, if COOP_POLL_CYCLES passed since the CTA's last read by any warp --
+            // the demand word, raising the stop flag if this id is asked to surrender.  Nothing
+            // else of it is live across the item, and only a polling warp waits for the load.
             auto poll = [&]() {
                 const unsigned long long now = clock64();     // the SM's clock: cheap, CTA-consistent
                 if (cs.lid == 0 || cs.nostop || now - *pollt < COOP_POLL_CYCLES) return;
@@ -777,17 +793,24 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
                 const uint32_t d = ld_relaxed32(&p.ctl->demand);
                 if (d && cs.lid + d >= w_M(ld_relaxed64(&p.ctl->W))) *stopf = 1u;
             };
-            // lane 0 decides, the warp follows (fn is warp-collective)
-            auto stopped = [&]() { return __shfl_sync(FULL, lane == 0 ? *stopf : 0u, 0) != 0; };
-            uint64_t it = gw;
-            for (;;) {
-                for (; it < n_static; it += TW) {
-                    if (stopped()) break;
+            uint32_t next = (uint32_t)clock() + COOP_POLL_CYCLES;
+            // warp-uniform: true when this warp must stop (checked at most once per period)
+            const bool armed = p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY;
+            auto check = [&]() -> bool {
+                if (!armed || !__any_sync(FULL, (int32_t)((uint32_t)clock() - next) >= 0)) return false;
+                next = (uint32_t)clock() + COOP_POLL_CYCLES;
+                if (lane == 0) poll();
+                return __shfl_sync(FULL, lane == 0 ? *stopf : 0u, 0) != 0;
+            };
+            uint64_t it = resumed ? gw + (uint64_t)cs.rk[warp] * TW : gw;
+            {
+                bool halt = false;
+                for (; !halt && it < n_static; it += TW) {
                     fn(it);
-                    if (lane == 0) poll();
+                    halt = check();
                 }
                 if (lane == 0) cs.rk[warp] = (uint32_t)((it - gw) / TW);
-                if (tail16 && n_static < n_items && !stopped()) {
+                if (tail16 && n_static < n_items && !halt) {
                     uint32_t t = 0;
                     if (lane == 0) t = atomicAdd(counter, 1u);
                     for (;;) {
@@ -799,14 +822,20 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
                             if (more) t = atomicAdd(counter, 1u);     // next claim in flight
                         }
                         fn(ti);                                       // a claimed item is always run
-                        if (lane == 0) poll();
+                        check();
                         if (!__shfl_sync(FULL, more, 0)) break;
                     }
                 }
                 cta_sync();
                 if (!cs.stop) return ACT_CONT;
-                const uint32_t r = offer_kill_mid<BLOCK>(p, cs, app, flush, n_static, TW);
-                if (r != ACT_CONT) return r;                          // killed (or abort): nothing stranded
+                // asked to surrender: counters out, then run_body offers this CTA (out of line,
+                // outside the item loops: a call in here would constrain their registers) and
+                // re-enters the expand with cs.resume if it is not taken
+                flush();
+                if (threadIdx.x == 0) { cs.hb_n = n_static; cs.hb_tw = TW; }
+                cta_sync();
+                (void)app;
+                return ACT_STOP;
             }
         }
     }
@@ -831,7 +860,7 @@ __device__ COOP_RUNBODY_ATTR uint32_t run_body(const KParams &p, CtaState &cs, A
     uint32_t r;
     app.enter(p, cs);
     if (entry == ENTRY_START) {
-        app.template init<BLOCK>(p, cs);
+        app.template init<BLOCK>(*cs.sp, cs);
         r = barrier(p, cs, app, /*resizing=*/false, ENTRY_AFTER_RB2);   // global_barrier
         if (r != ACT_CONT) return r;
         entry = ENTRY_AFTER_RB2;
@@ -845,7 +874,7 @@ __device__ COOP_RUNBODY_ATTR uint32_t run_body(const KParams &p, CtaState &cs, A
                 // the active CTAs, then a resizing barrier (forked CTAs join at the loop head)
                 if (threadIdx.x == 0) { cs.level = 0; cs.in_sel = 0; }
                 cta_sync();
-                app.template init<BLOCK>(p, cs);
+                app.template init<BLOCK>(*cs.sp, cs);
                 r = barrier(p, cs, app, /*resizing=*/true, ENTRY_RESTART);
                 if (r != ACT_CONT) return r;
                 continue;
@@ -855,12 +884,27 @@ __device__ COOP_RUNBODY_ATTR uint32_t run_body(const KParams &p, CtaState &cs, A
             // for workgroups mid-interval (offer_kill at chunk boundaries), else the static one
             const bool midk = App::kCoop && p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY;
             if constexpr (App::kCoop) {
+#if COOP_MID_UNIFIED
+                r = app.template expand<BLOCK, DIST_MID>(p, cs);          // one instance, checks at run time
+#else
                 if (midk)
-                    r = expand_dist<App, BLOCK, DIST_MID>(p, cs, app);     // out of line: keeps the static
+                    r = expand_dist<App, BLOCK, DIST_MID>(*cs.sp, cs, app); // out of line: keeps the static
                 else                                                      // instance's code as tight as
                     r = app.template expand<BLOCK, DIST_STATIC>(p, cs);   // the non-cooperative kernel's
+#endif
             } else {
                 r = app.template expand<BLOCK, DIST_STATIC>(p, cs);
+            }
+            if constexpr (App::kCoop) {
+                while (r == ACT_STOP) {                        // asked to surrender inside the interval
+                    r = offer_kill_mid<BLOCK>(*cs.sp, cs, app);
+                    if (r != ACT_CONT) break;                  // killed (its rest handed back) / abort
+                    if (threadIdx.x == 0) cs.resume = 1;       // not taken: finish the share
+                    cta_sync();
+                    r = expand_dist<App, BLOCK, DIST_MID>(*cs.sp, cs, app);
+                    cta_sync();
+                    if (threadIdx.x == 0) cs.resume = 0;
+                }
             }
             if (r != ACT_CONT) return r;                       // killed inside the interval (offer_kill)
             cta_sync();                                   // every warp is done reading cs
@@ -878,7 +922,7 @@ __device__ COOP_RUNBODY_ATTR uint32_t run_body(const KParams &p, CtaState &cs, A
                         cs.M = (uint32_t)(__ldcg(&p.ctl->rep_tw) / (BLOCK / 32));
                     }
                     cta_sync();
-                    r = expand_dist<App, BLOCK, DIST_REPLAY>(p, cs, app);
+                    r = expand_dist<App, BLOCK, DIST_REPLAY>(*cs.sp, cs, app);
                     if (r != ACT_CONT) return r;
                     cta_sync();
                     if (threadIdx.x == 0) { cs.M = cs.rep_M; cs.in_sel ^= 1u; }
@@ -1058,7 +1102,7 @@ __device__ __noinline__ void park_loop(const KParams &p, CtaState &cs, App &app)
         const uint32_t act = cs.action;
         if (act == ACT_EXIT) return;
         if (act == ACT_RUN_TASK) {
-            run_task_block(p, cs);
+            run_task_block(*cs.sp, cs);
             if (threadIdx.x == 0) { __threadfence(); atomicOr(&c->pool[wi], bit); }
             continue;
         }
@@ -1107,11 +1151,12 @@ __device__ __forceinline__ void kernel_body(const KParams &p, CtaState &cs, App 
         cs.wait_rel = 0;
         cs.lid = blockIdx.x; cs.M = p.M0; cs.gen = 0; cs.level = 0; cs.in_sel = 0;
         cs.acc[0] = cs.acc[1] = 0; cs.acc_sel = 0;
+        cs.resume = 0; cs.stop = 0; cs.nostop = 0;
         if (blockIdx.x == 0) p.ctl->t_start = t0;
     }
     cta_sync();
     if constexpr ((App::kCoop && COOP_BIS_PARK)) {
-        if (p.has_sched && blockIdx.x == p.P) { scheduler_loop(p, cs); return; }
+        if (p.has_sched && blockIdx.x == p.P) { scheduler_loop(*cs.sp, cs); return; }
     }
     if (blockIdx.x < p.M0) {
         uint32_t r = run_body<App, BLOCK>(p, cs, app, ENTRY_START);
@@ -1130,7 +1175,7 @@ __device__ __forceinline__ void kernel_body(const KParams &p, CtaState &cs, App 
         cta_sync();
     }
     if constexpr ((App::kCoop && COOP_BIS_PARK)) {
-        if (p.barrier_mode != COOP_BARRIER_PLAIN) park_loop<App, BLOCK>(p, cs, app);
+        if (p.barrier_mode != COOP_BARRIER_PLAIN) park_loop<App, BLOCK>(*cs.sp, cs, app);
     }
 #if COOP_TRACE
     if (threadIdx.x == 0 && blockIdx.x == 0)
@@ -1146,6 +1191,14 @@ template <class App, int BLOCK, int MINB>
 __global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(const __grid_constant__ KParams p) {
     __shared__ CtaState cs;
     __shared__ uint32_t s_last;
+    __shared__ __align__(16) KParams s_p;
+    {
+        static_assert(sizeof(KParams) % 8 == 0, "KParams copy by 8-byte words");
+        const unsigned long long *src = reinterpret_cast<const unsigned long long *>(&p);
+        unsigned long long *dst = reinterpret_cast<unsigned long long *>(&s_p);
+        for (uint32_t i = threadIdx.x; i < sizeof(KParams) / 8; i += BLOCK) dst[i] = src[i];
+        if (threadIdx.x == 0) cs.sp = &s_p;
+    }
     App app;
     kernel_body<App, BLOCK>(p, cs, app);
     // epilogue: the last CTA out mirrors the control block into host-mapped memory, so the
