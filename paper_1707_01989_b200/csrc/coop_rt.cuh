@@ -214,7 +214,8 @@ struct CtaState {
     uint32_t resume;                               // DIST_MID: expand re-entered after an offer that did not kill
     uint64_t hb_n, hb_tw;                          // DIST_MID: static items / warp stride of the interval (hand-back)
     uint32_t replay, rep_M;                        // a replay interval follows this barrier; survivors' M in it
-    uint32_t rk[32];                               // DIST_MID: next static item index per warp
+    uint32_t rk[32];                               // DIST_MID: next static item index per warp (~0u: none left)
+    uint32_t nextc[32];                            // DIST_MID: per-warp clock of the next stop/poll check
     unsigned long long poll_t;                     // DIST_MID: %globaltimer of the CTA's last demand poll
 #if COOP_TRACE
     unsigned long long tr[12];
@@ -773,44 +774,48 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
             return ACT_CONT;
         } else {
             volatile uint32_t *stopf = &cs.stop;
-            volatile unsigned long long *pollt = &cs.poll_t;
             const bool resumed = cs.resume != 0;
             if (threadIdx.x == 0) {
                 cs.stop = 0;
                 if (!resumed) cs.nostop = 0;                       // kept by a resumed interval
                 cs.poll_t = clock64();
             }
+            if (lane == 0) cs.nextc[warp] = (uint32_t)clock() + COOP_POLL_CYCLES;
             cta_sync();
-            // Each warp checks, at most once per COOP_POLL_CYCLES of its own clock (one clock
-            // read and a vote per item, one register live across the item): the CTA's stop flag,
-            // and -- lane 0, if COOP_POLL_CYCLES passed since the CTA's last read by any warp --
-            // the demand word, raising the stop flag if this id is asked to surrender.  Nothing
-            // else of it is live across the item, and only a polling warp waits for the load.
-            auto poll = [&]() {
-                const unsigned long long now = clock64();     // the SM's clock: cheap, CTA-consistent
-                if (cs.lid == 0 || cs.nostop || now - *pollt < COOP_POLL_CYCLES) return;
-                *pollt = now;
-                const uint32_t d = ld_relaxed32(&p.ctl->demand);
-                if (d && cs.lid + d >= w_M(ld_relaxed64(&p.ctl->W))) *stopf = 1u;
-            };
-            uint32_t next = (uint32_t)clock() + COOP_POLL_CYCLES;
-            // warp-uniform: true when this warp must stop (checked at most once per period)
-            const bool armed = p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY;
-            auto check = [&]() -> bool {
-                if (!armed || !__any_sync(FULL, (int32_t)((uint32_t)clock() - next) >= 0)) return false;
-                next = (uint32_t)clock() + COOP_POLL_CYCLES;
-                if (lane == 0) poll();
+            // After an item, each warp checks at most once per COOP_POLL_CYCLES of the SM clock
+            // (its next check time in shared memory: the item loop keeps exactly the static
+            // loop's registers -- anything more live across the item spilled the bottom-up item
+            // body, +9 % kernel time): the CTA's stop flag and, lane 0 if COOP_POLL_CYCLES passed
+            // since the CTA's last read, the demand word (raising the stop flag if this id is
+            // asked to surrender, query style).  Only a polling warp waits for that load.
+            auto check = [&]() -> bool {                             // warp-uniform
+                if (!(p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY)) return false;
+                volatile uint32_t *nx = &cs.nextc[warp];
+                uint32_t due = (int32_t)((uint32_t)clock() - *nx) >= 0 ? 1u : 0u;
+                if (!__shfl_sync(FULL, due, 0)) return false;
+                if (lane == 0) {
+                    const unsigned long long now = clock64();
+                    *nx = (uint32_t)now + COOP_POLL_CYCLES;
+                    volatile unsigned long long *pollt = &cs.poll_t;
+                    if (cs.lid != 0 && !cs.nostop && now - *pollt >= COOP_POLL_CYCLES) {
+                        *pollt = now;
+                        const uint32_t d = ld_relaxed32(&p.ctl->demand);
+                        if (d && cs.lid + d >= w_M(ld_relaxed64(&p.ctl->W))) *stopf = 1u;
+                    }
+                }
                 return __shfl_sync(FULL, lane == 0 ? *stopf : 0u, 0) != 0;
             };
-            uint64_t it = resumed ? gw + (uint64_t)cs.rk[warp] * TW : gw;
             {
-                bool halt = false;
-                for (; !halt && it < n_static; it += TW) {
+                uint64_t it = resumed ? gw + (uint64_t)cs.rk[warp] * TW : gw;
+                bool halted = false;
+                for (; it < n_static; it += TW) {
                     fn(it);
-                    halt = check();
+                    if (check()) { halted = true; it += TW; break; }
                 }
-                if (lane == 0) cs.rk[warp] = (uint32_t)((it - gw) / TW);
-                if (tail16 && n_static < n_items && !halt) {
+                // next static item of this warp (all done: past the end)
+                if (lane == 0)
+                    cs.rk[warp] = halted ? (uint32_t)((it - ((uint64_t)cs.lid * WPB + warp)) / TW) : 0xFFFFFFFFu;
+                if (tail16 && n_static < n_items && !halted) {
                     uint32_t t = 0;
                     if (lane == 0) t = atomicAdd(counter, 1u);
                     for (;;) {
@@ -860,7 +865,14 @@ __device__ COOP_RUNBODY_ATTR uint32_t run_body(const KParams &p, CtaState &cs, A
     uint32_t r;
     app.enter(p, cs);
     if (entry == ENTRY_START) {
+#if COOP_LTRACE
+        if (threadIdx.x == 0 && blockIdx.x < 1184) g_ltrace[63][blockIdx.x][1] = globaltimer();   // init start
+#endif
         app.template init<BLOCK>(*cs.sp, cs);
+#if COOP_LTRACE
+        cta_sync();
+        if (threadIdx.x == 0 && blockIdx.x < 1184) g_ltrace[63][blockIdx.x][2] = globaltimer();   // init done
+#endif
         r = barrier(p, cs, app, /*resizing=*/false, ENTRY_AFTER_RB2);   // global_barrier
         if (r != ACT_CONT) return r;
         entry = ENTRY_AFTER_RB2;
@@ -884,27 +896,27 @@ __device__ COOP_RUNBODY_ATTR uint32_t run_body(const KParams &p, CtaState &cs, A
             // for workgroups mid-interval (offer_kill at chunk boundaries), else the static one
             const bool midk = App::kCoop && p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY;
             if constexpr (App::kCoop) {
+                // one call site of the expand: asked to surrender inside the interval (ACT_STOP,
+                // counters flushed), the CTA offers itself out of line; not taken, it re-enters
+                // the expand to finish its share (cs.resume)
+                for (;;) {
 #if COOP_MID_UNIFIED
-                r = app.template expand<BLOCK, DIST_MID>(p, cs);          // one instance, checks at run time
+                    r = app.template expand<BLOCK, DIST_MID>(p, cs);      // checks gated at run time
 #else
-                if (midk)
-                    r = expand_dist<App, BLOCK, DIST_MID>(*cs.sp, cs, app); // out of line: keeps the static
-                else                                                      // instance's code as tight as
-                    r = app.template expand<BLOCK, DIST_STATIC>(p, cs);   // the non-cooperative kernel's
+                    if (midk)
+                        r = expand_dist<App, BLOCK, DIST_MID>(*cs.sp, cs, app); // out of line: keeps the
+                    else                                                        // static instance as tight
+                        r = app.template expand<BLOCK, DIST_STATIC>(p, cs);     // as the non-coop kernel's
 #endif
-            } else {
-                r = app.template expand<BLOCK, DIST_STATIC>(p, cs);
-            }
-            if constexpr (App::kCoop) {
-                while (r == ACT_STOP) {                        // asked to surrender inside the interval
+                    if (r != ACT_STOP) break;
                     r = offer_kill_mid<BLOCK>(*cs.sp, cs, app);
                     if (r != ACT_CONT) break;                  // killed (its rest handed back) / abort
-                    if (threadIdx.x == 0) cs.resume = 1;       // not taken: finish the share
+                    if (threadIdx.x == 0) cs.resume = 1;
                     cta_sync();
-                    r = expand_dist<App, BLOCK, DIST_MID>(*cs.sp, cs, app);
-                    cta_sync();
-                    if (threadIdx.x == 0) cs.resume = 0;
                 }
+                if (threadIdx.x == 0) cs.resume = 0;
+            } else {
+                r = app.template expand<BLOCK, DIST_STATIC>(p, cs);
             }
             if (r != ACT_CONT) return r;                       // killed inside the interval (offer_kill)
             cta_sync();                                   // every warp is done reading cs
@@ -1146,6 +1158,9 @@ __device__ __forceinline__ void kernel_body(const KParams &p, CtaState &cs, App 
         cs.tr_last = 0;
 #endif
         cs.deadline = t0 + p.timeout_ns;
+#if COOP_LTRACE
+        if (blockIdx.x < 1184) g_ltrace[63][blockIdx.x][0] = t0;                                 // kernel entry
+#endif
         cs.edges = cs.frontier = cs.reached = 0;
         cs.consumed = 0;
         cs.wait_rel = 0;

@@ -72,5 +72,12 @@ for s in gg.sample_sources(g, nsrc, seed=2):
                              "pub": round(float(rel[:, 10][t[:, 10] > 0].max()), 1) if (t[:, 10] > 0).any() else None,
                              "seen_max": round(float(rel[:, 11][t[:, 11] > 0].max()), 1) if (t[:, 11] > 0).any() else None}})
         prev = int(t[:, 2].max())
+    # kernel entry / init start / init done per CTA (slots of row 63), relative to the first entry
+    e = buf[63, :n_cta, :3].astype(np.int64)
+    t0 = int(e[:, 0][e[:, 0] > 0].min()) if (e[:, 0] > 0).any() else 0
+    init = {"entry_max": round(float((e[:, 0].max() - t0) / 1e3), 1),
+            "init_done_med": round(float((np.median(e[:, 2]) - t0) / 1e3), 1),
+            "init_done_max": round(float((e[:, 2].max() - t0) / 1e3), 1),
+            "L0_start_min": round(float((buf[0, :n_cta, 0].astype(np.int64).min() - t0) / 1e3), 1)} if t0 else None
     print(json.dumps({"src": s, "flags": flags, "kernel_us": st.kernel_ns / 1e3, "bu": st.bottom_up_levels,
-                      "levels": rows}), flush=True)
+                      "init": init, "levels": rows}), flush=True)
