@@ -147,6 +147,7 @@ __device__ __forceinline__ void lvl_reset(Ctl *c, uint32_t par) {
 template <typename OffT, bool KCOOP = true>
 struct BfsApp {
     static constexpr bool kCoop = KCOOP;
+    static constexpr bool kBetween = false;          // no CTA work between Fig. 4's barriers
     using LE = typename std::conditional<sizeof(OffT) == 4, LightEntry, LightEntry64>::type;
     static constexpr int KB = 4;   // 32-edge windows per warp iteration (32*KB <= kHeavyDeg)
 
@@ -1052,6 +1053,7 @@ constexpr uint32_t kNoRound = 0xFFFFFFFFu;   // low word of an SSSP key not push
 template <typename OffT, bool KCOOP = true>
 struct SsspApp {
     static constexpr bool kCoop = KCOOP;
+    static constexpr bool kBetween = false;
     __device__ void pre_arrive(const KParams &, CtaState &) {}
     __device__ bool next_run(const KParams &, CtaState &) { return false; }
     __device__ void enter(const KParams &, CtaState &) {}
@@ -1315,6 +1317,7 @@ struct SsspApp {
 // across the barrier).  iters resizing barriers in total.
 struct BarrierApp {
     static constexpr bool kCoop = true;
+    static constexpr bool kBetween = false;
     __device__ void pre_arrive(const KParams &, CtaState &) {}
     __device__ bool next_run(const KParams &, CtaState &) { return false; }
     __device__ void enter(const KParams &, CtaState &cs) {

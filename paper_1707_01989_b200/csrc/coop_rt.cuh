@@ -70,8 +70,13 @@
 #ifndef COOP_RUNBODY_NOINLINE
 #define COOP_RUNBODY_NOINLINE 0
 #endif
+#ifndef COOP_RUNBODY_INLINE
+#define COOP_RUNBODY_INLINE 0 // 1: force run_body inline at both call sites (kernel body, park loop)
+#endif
 #if COOP_RUNBODY_NOINLINE
 #define COOP_RUNBODY_ATTR __noinline__
+#elif COOP_RUNBODY_INLINE
+#define COOP_RUNBODY_ATTR __forceinline__
 #else
 #define COOP_RUNBODY_ATTR
 #endif
@@ -407,11 +412,18 @@ __device__ __forceinline__ uint32_t mhist_get(const KParams &p, uint32_t gen) {
 // Resizing (or plain, resizing=false) global barrier for the whole CTA.
 // Returns ACT_CONT (survived; cs.M / cs.gen updated), ACT_KILLED or ACT_ABORT.
 template <class App>
-__device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resizing, uint32_t entry) {
+__device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resizing, uint32_t entry,
+                            bool swap = false) {
 #if COOP_TRACE
     long long tr0 = clock64();
 #endif
     cta_sync();
+    // Fig. 4's swap(&in_nodes, &out_nodes) before barrier #1: after the entry CTA barrier every
+    // warp is done reading the interval's in_sel (no CTA barrier of its own)
+    if (swap && threadIdx.x == 0) {
+        LTRACE(1);
+        cs.in_sel ^= 1u;
+    }
     Ctl *c = p.ctl;
 #if COOP_TRACE
     long long tr1 = clock64(), tr2 = 0, tr3 = 0;
@@ -919,10 +931,7 @@ __device__ COOP_RUNBODY_ATTR uint32_t run_body(const KParams &p, CtaState &cs, A
                 r = app.template expand<BLOCK, DIST_STATIC>(p, cs);
             }
             if (r != ACT_CONT) return r;                       // killed inside the interval (offer_kill)
-            cta_sync();                                   // every warp is done reading cs
-            LTRACE(1);
-            if (threadIdx.x == 0) cs.in_sel ^= 1u;            // swap(&in_nodes, &out_nodes)
-            r = barrier(p, cs, app, true, ENTRY_AFTER_RB1);   // resizing_global_barrier() #1
+            r = barrier(p, cs, app, true, ENTRY_AFTER_RB1, /*swap=*/true);   // swap; resizing_global_barrier() #1
             if constexpr (App::kCoop) {
                 // hand-back: workgroups left inside the interval with static items undone; the
                 // survivors run them (items numbered by the donors' interval: cs.M = its M for
@@ -945,8 +954,10 @@ __device__ COOP_RUNBODY_ATTR uint32_t run_body(const KParams &p, CtaState &cs, A
             LTRACE(2);
         }
         skip_to_rb1 = false;
-        app.template between<BLOCK>(p, cs);                   // CTA work between Fig. 4's two barriers
-        cta_sync();                                           // every warp has read the barrier's result
+        if constexpr (App::kBetween) {
+            app.template between<BLOCK>(p, cs);               // CTA work between Fig. 4's two barriers
+            cta_sync();                                       // every warp is done with it
+        }
         if (threadIdx.x == 0) cs.level += 1;                  // reset(out_nodes) done in serial; level++
         if (p.bpl == 2) {
             r = barrier(p, cs, app, true, ENTRY_AFTER_RB2);   // resizing_global_barrier() #2

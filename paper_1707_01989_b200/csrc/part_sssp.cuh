@@ -30,6 +30,7 @@ namespace coop {
 template <typename OffT>
 struct PartSsspApp {
     static constexpr bool kCoop = true;
+    static constexpr bool kBetween = true;           // the exchange step between the two barriers
     __device__ void pre_arrive(const KParams &, CtaState &) {}
     __device__ bool next_run(const KParams &, CtaState &) { return false; }
     __device__ void enter(const KParams &, CtaState &) {}

@@ -10,7 +10,7 @@ timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/${T}_gputests.log 2
 timeout 600 python bench.py > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err
 timeout 600 bash tools/ncu_capture.sh ${T}_ncu_bfs_diropt python tools/prof_bfs.py --flags 2
 timeout 600 bash tools/ncu_capture.sh ${T}_ncu_bfs_topdown python tools/prof_bfs.py --flags 0
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"coop_kernel|ctl_init" -c 400 --csv \
     --log-file gpurun_out/${T}_launches_bench_quick.csv python bench.py --steps 2 --warmup 3 --quick --no-cpu \
     > gpurun_out/${T}_launches_run.log 2>&1
 timeout 900 python tools/sweep.py c4 > gpurun_out/${T}_c4_barrier_sweep.log 2>&1
