@@ -132,18 +132,6 @@ __device__ __forceinline__ void store_level(const KParams &p, int64_t v, uint32_
     if (L >= 254u) p.level_out[v] = (int32_t)L;
 }
 
-// the sharded BFS level counters (Ctl::lvl): totals and reset of one parity
-__device__ __forceinline__ unsigned long long lvl_total(const Ctl *c, uint32_t k) {
-    unsigned long long t = 0;
-#pragma unroll
-    for (uint32_t s = 0; s < kLvlShards; ++s) t += c->lvl[s][k];
-    return t;
-}
-__device__ __forceinline__ void lvl_reset(Ctl *c, uint32_t par) {
-#pragma unroll
-    for (uint32_t s = 0; s < kLvlShards; ++s) c->lvl[s][par] = c->lvl[s][2 + par] = 0;
-}
-
 template <typename OffT, bool KCOOP = true>
 struct BfsApp {
     static constexpr bool kCoop = KCOOP;
@@ -160,13 +148,11 @@ struct BfsApp {
         const uint64_t tid = (uint64_t)cs.lid * BLOCK + threadIdx.x;
         const uint64_t nth = (uint64_t)cs.M * BLOCK;
         const int64_t V = p.V, s = run_source(p);
-        // lv8[v] = 0 (not reached), lv8[s] = 1 (level 0): 16 bytes per thread (one vector store),
-        // the mapping the output pass of empty() uses, so a source-loop restart never races a
-        // slower CTA's pass
-        uint4 *l16 = reinterpret_cast<uint4 *>(p.lv8);
-        const uint64_t n16 = ((uint64_t)V + 15) / 16;
-        for (uint64_t i = tid; i < n16; i += nth) l16[i] = make_uint4(0u, 0u, 0u, 0u);
-        if (tid == (uint64_t)(s >> 4) % nth) p.lv8[s] = 1;        // the thread that zeroed s's 16 bytes
+        // lv8[v] = 0 (not reached), lv8[s] = 1 (level 0): 4 bytes per thread, the mapping the
+        // output pass of empty() uses, so a source-loop restart never races a slower CTA's pass
+        uint32_t *l4 = reinterpret_cast<uint32_t *>(p.lv8);
+        const uint64_t n4 = ((uint64_t)V + 3) / 4;
+        for (uint64_t i = tid; i < n4; i += nth) l4[i] = (uint64_t)(s >> 2) == i ? 1u << (8 * (s & 3)) : 0u;
         const uint64_t nw = ((uint64_t)V + 31) / 32;
         const uint32_t sw = (uint32_t)(s >> 5), sb = 1u << (s & 31);
         const bool dead_from_iso = p.dopt && COOP_INIT_DEAD && p.iso != nullptr;
@@ -238,8 +224,8 @@ struct BfsApp {
                 static_cast<LE *>(p.qlight[0])[0] = le;
                 p.ctl->qsize[0] = 1;
             }
-            p.ctl->lvl[0][0] = 1;        // n_f, m_f of level 0 (the other shards are 0)
-            p.ctl->lvl[0][2] = deg;
+            p.ctl->nf[0] = 1;
+            p.ctl->mf[0] = deg;
             p.ctl->vis_edges = deg;
             p.ctl->bmode[0] = BFS_TDQ;
             if (p.level_cap) p.level_sizes[0] = 1;
@@ -272,7 +258,7 @@ struct BfsApp {
             cs.app_u32[1] = (uint32_t)(hv >> 40);
             cs.app_u32[2] = (uint32_t)Eh;
             cs.app_u32[3] = (uint32_t)(Eh >> 32);
-            cs.app_u32[4] = lvl_total(c, in) ? 1u : 0u;
+            cs.app_u32[4] = c->nf[in] ? 1u : 0u;
             cs.app_u32[5] = c->bmode[in];
             cs.app_u32[6] = c->n_bu_levels;                  // 1 during the first bottom-up level
         }
@@ -281,31 +267,24 @@ struct BfsApp {
         if (done) {
             // the traversal's output, once: levels = lv8 - 1 (-1 unreached, reading R10); every
             // active CTA its stride, 4 vertices per thread (one coalesced 4-B load, 16-B store)
-            const uint64_t V = (uint64_t)p.V, n16 = (V + 15) / 16, nth = (uint64_t)cs.M * blockDim.x;
-            const uint4 *l16 = reinterpret_cast<const uint4 *>(p.lv8);
-            const bool al = ((uintptr_t)p.level_out & 15) == 0;
-            for (uint64_t i = (uint64_t)cs.lid * blockDim.x + threadIdx.x; i < n16; i += nth) {
-                const uint4 b4 = __ldcg(l16 + i);                       // 16 vertices
-                const uint32_t bw[4] = {b4.x, b4.y, b4.z, b4.w};
+            const uint64_t V = (uint64_t)p.V, n4 = (V + 3) / 4, nth = (uint64_t)cs.M * blockDim.x;
+            const uint32_t *l4 = reinterpret_cast<const uint32_t *>(p.lv8);
+            for (uint64_t i = (uint64_t)cs.lid * blockDim.x + threadIdx.x; i < n4; i += nth) {
+                const uint32_t b = __ldcg(l4 + i);
+                int32_t o[4];
+                bool direct = false;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint64_t v0 = 16 * i + 4 * q;
-                    const uint32_t b = bw[q];
-                    int32_t o[4];
-                    bool direct = false;
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t x = (b >> (8 * k)) & 0xFFu;
+                    o[k] = (int32_t)x - 1;
+                    direct |= x == 255u && 4 * i + k < V;
+                }
+                if (!direct && 4 * i + 4 <= V && ((uintptr_t)p.level_out & 15) == 0) {
+                    *reinterpret_cast<int4 *>(p.level_out + 4 * i) = make_int4(o[0], o[1], o[2], o[3]);
+                } else {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint32_t x = (b >> (8 * k)) & 0xFFu;
-                        o[k] = (int32_t)x - 1;
-                        direct |= x == 255u && v0 + k < V;
-                    }
-                    if (!direct && v0 + 4 <= V && al) {
-                        *reinterpret_cast<int4 *>(p.level_out + v0) = make_int4(o[0], o[1], o[2], o[3]);
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            if (v0 + k < V && ((b >> (8 * k)) & 0xFFu) != 255u) p.level_out[v0 + k] = o[k];
-                    }
+                    for (int k = 0; k < 4; ++k)
+                        if (4 * i + k < V && ((b >> (8 * k)) & 0xFFu) != 255u) p.level_out[4 * i + k] = o[k];
                 }
             }
         }
@@ -908,9 +887,8 @@ struct BfsApp {
     __device__ __forceinline__ void pre_arrive(const KParams &p, CtaState &cs) {
         const unsigned long long nf = cs.acc[0], mf = cs.acc[1];
         if (nf | mf) {
-            const uint32_t sh = cs.lid % kLvlShards;
-            if (nf) atomicAdd(&p.ctl->lvl[sh][cs.acc_sel], nf);
-            if (mf) atomicAdd(&p.ctl->lvl[sh][2 + cs.acc_sel], mf);
+            if (nf) atomicAdd(&p.ctl->nf[cs.acc_sel], nf);
+            if (mf) atomicAdd(&p.ctl->mf[cs.acc_sel], mf);
             cs.acc[0] = cs.acc[1] = 0;
         }
     }
@@ -994,13 +972,14 @@ struct BfsApp {
         // every load first, as one batch of independent round trips (this runs on
         // the critical path of the barrier, while all other CTAs wait)
         const uint32_t prev = c->bmode[out];
-        const unsigned long long nf = lvl_total(c, in), mf = lvl_total(c, 2 + in);
+        const unsigned long long nf = c->nf[in], mf = c->mf[in];
         const unsigned long long vis = c->vis_edges + mf, ftot = c->frontier_total;
         const uint32_t nlev = c->levels, nbu = c->n_bu_levels;
         c->qsize[out] = 0;
         c->heavy[out] = 0;
         reset_claims(c, out);
-        lvl_reset(c, out);
+        c->nf[out] = 0;
+        c->mf[out] = 0;
         c->vis_edges = vis;
         uint32_t mode = BFS_TDQ;
         if (p.dopt) {
@@ -1029,8 +1008,8 @@ struct BfsApp {
                 c->heavy[0] = c->heavy[1] = 0;
                 reset_claims(c, 0);
                 reset_claims(c, 1);
-                lvl_reset(c, 0);
-                lvl_reset(c, 1);
+                c->nf[0] = c->nf[1] = 0;
+                c->mf[0] = c->mf[1] = 0;
                 c->bmode[0] = c->bmode[1] = BFS_TDQ;
                 c->n_bu_levels = 0;
             }

@@ -638,7 +638,7 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
         // slots, refills hold >= 128 entries) plus one open reservation per warp
         const size_t qcap = 2 * V + (size_t)P * (threads / 32) * 256;
         CUDA_TRY(s->visited.ensure(4 * ((V + 31) / 32)));
-        CUDA_TRY(s->lv8.ensure(16 * ((V + 15) / 16)));
+        CUDA_TRY(s->lv8.ensure(4 * ((V + 3) / 4)));
         kp.lv8 = static_cast<uint8_t *>(s->lv8.p);
         CUDA_TRY(s->ql0.ensure(le * qcap));
         CUDA_TRY(s->ql1.ensure(le * qcap));

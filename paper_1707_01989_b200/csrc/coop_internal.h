@@ -55,7 +55,6 @@ struct TaskEventDev {
 
 // Control block in device memory.  Hot words sit on their own 128-B lines.
 constexpr uint32_t kClaimShards = 8;
-constexpr uint32_t kLvlShards = 8;
 
 struct __align__(128) Ctl {
     unsigned long long W;              // barrier word {gen:32 | M:16 | arrived:16} (arrivals)
@@ -104,8 +103,8 @@ struct __align__(128) Ctl {
     uint32_t chunk[2];                 // dynamic work distribution: next chunk per level parity
     uint32_t mid_kills;                // workgroups that left at a chunk boundary (mid-interval offer_kill)
     uint32_t pad_m;
-    unsigned long long nf_unused[2];   // (BFS level counters moved to lvl[][] below)
-    unsigned long long mf_unused[2];
+    unsigned long long nf[2];          // vertices discovered
+    unsigned long long mf[2];          // sum of their degrees
     unsigned long long vis_edges;      // sum of degrees of every vertex discovered so far
     uint32_t bmode[2];                 // BFS_* mode of the level that reads parity p
     uint32_t n_bu_levels;              // statistics: bottom-up levels executed
@@ -145,10 +144,6 @@ struct __align__(128) Ctl {
     unsigned long long rep_tw;         // warp stride M*W of the interval the items come from
     uint32_t handbacks, replays;       // statistics
     uint32_t pad_hb[26];
-    // BFS level counters, sharded by CTA id over kLvlShards 128-B lines so the arrivals' count
-    // atomics do not queue on one line ahead of the serial section's reads: lvl[s][par] =
-    // vertices discovered (n_f), lvl[s][2 + par] = the sum of their degrees (m_f), par = level parity
-    unsigned long long lvl[kLvlShards][16];
 };
 
 // one warp's handed-back static items: start, start + tw, ... (count of them), at flat
