@@ -94,18 +94,37 @@ static void *pick_block(uint32_t threads) {
     }
 }
 
+// the scheduler-armed specialisation (SCHEDULER + query: mid-interval offer_kill with
+// hand-back), BFS and SSSP at 256 and 512 threads per workgroup; other block sizes run the
+// general kernel, whose mid-interval instance is out of line
+template <class App, int BLOCK>
+static void *armed_kernel_ptr() {
+    constexpr int MINB = BLOCK >= COOP_THREADS_PER_SM ? 1 : COOP_THREADS_PER_SM / BLOCK;
+    return reinterpret_cast<void *>(&coop_kernel<App, BLOCK, MINB, true>);
+}
+template <class App>
+static void *pick_block_armed(uint32_t threads) {
+    switch (threads) {
+        case 256: return armed_kernel_ptr<App, 256>();
+        case 512: return armed_kernel_ptr<App, 512>();
+        default: return pick_block<App>(threads);
+    }
+}
+
 // plain (COOP_BARRIER_PLAIN): the separately compiled non-cooperative persistent
 // kernel of the same traversal (kCoop = false: no scheduler, pool, mailboxes,
 // kill/fork or chunk-claim code), the T2 baseline
-static void *select_kernel(uint32_t app, int off64, uint32_t threads, bool plain) {
+static void *select_kernel(uint32_t app, int off64, uint32_t threads, bool plain, bool armed = false) {
     if (app == APP_PBFS) return off64 ? pick_block<PartBfsApp<int64_t>>(threads) : pick_block<PartBfsApp<uint32_t>>(threads);
     if (app == APP_PSSSP) return off64 ? pick_block<PartSsspApp<int64_t>>(threads) : pick_block<PartSsspApp<uint32_t>>(threads);
     if (app == APP_BFS) {
         if (plain) return off64 ? pick_block<BfsApp<int64_t, false>>(threads) : pick_block<BfsApp<uint32_t, false>>(threads);
+        if (armed) return off64 ? pick_block_armed<BfsApp<int64_t>>(threads) : pick_block_armed<BfsApp<uint32_t>>(threads);
         return off64 ? pick_block<BfsApp<int64_t>>(threads) : pick_block<BfsApp<uint32_t>>(threads);
     }
     if (app == APP_SSSP) {
         if (plain) return off64 ? pick_block<SsspApp<int64_t, false>>(threads) : pick_block<SsspApp<uint32_t, false>>(threads);
+        if (armed) return off64 ? pick_block_armed<SsspApp<int64_t>>(threads) : pick_block_armed<SsspApp<uint32_t>>(threads);
         return off64 ? pick_block<SsspApp<int64_t>>(threads) : pick_block<SsspApp<uint32_t>>(threads);
     }
     switch (threads) {
@@ -577,7 +596,8 @@ static coop_status prepare(const RunReq &r, Prepared *pr) {
         if (r.app == APP_BFS) kp.level_out = static_cast<int32_t *>(r.out);
         else kp.dist_out = static_cast<uint32_t *>(r.out);
     }
-    void *kern = select_kernel(r.app, off64, threads, o.barrier_mode == COOP_BARRIER_PLAIN);
+    void *kern = select_kernel(r.app, off64, threads, o.barrier_mode == COOP_BARRIER_PLAIN,
+                               o.policy == COOP_POLICY_SCHEDULER && o.barrier_mode == COOP_BARRIER_QUERY);
     if (!kern) return fail(COOP_ERR_INVALID_ARG, "threads_per_wg %u not supported", threads);
     int sms = 0, per = 0;
     st = occupancy(kern, threads, &sms, &per);

@@ -872,7 +872,7 @@ __device__ COOP_EXPAND_DIST_ATTR uint32_t expand_dist(const KParams &p, CtaState
 
 // Fig. 4 with the app's process_node; entry points are the
 // program points after each resizing barrier (forked CTAs start there).
-template <class App, int BLOCK>
+template <class App, int BLOCK, bool ARMED = false>
 __device__ COOP_RUNBODY_ATTR uint32_t run_body(const KParams &p, CtaState &cs, App &app, uint32_t entry) {
     uint32_t r;
     app.enter(p, cs);
@@ -912,14 +912,21 @@ __device__ COOP_RUNBODY_ATTR uint32_t run_body(const KParams &p, CtaState &cs, A
                 // counters flushed), the CTA offers itself out of line; not taken, it re-enters
                 // the expand to finish its share (cs.resume)
                 for (;;) {
+                    if constexpr (ARMED) {
+                        // the scheduler-armed kernel (SCHEDULER + query): the mid-interval instance
+                        // inlined in a kernel of its own -- its own register allocation, parameters
+                        // from the constant bank -- while the NEVER kernel keeps only the static one
+                        r = app.template expand<BLOCK, DIST_MID>(p, cs);
+                    } else {
 #if COOP_MID_UNIFIED
-                    r = app.template expand<BLOCK, DIST_MID>(p, cs);      // checks gated at run time
+                        r = app.template expand<BLOCK, DIST_MID>(p, cs);      // checks gated at run time
 #else
-                    if (midk)
-                        r = expand_dist<App, BLOCK, DIST_MID>(*cs.sp, cs, app); // out of line: keeps the
-                    else                                                        // static instance as tight
-                        r = app.template expand<BLOCK, DIST_STATIC>(p, cs);     // as the non-coop kernel's
+                        if (midk)
+                            r = expand_dist<App, BLOCK, DIST_MID>(*cs.sp, cs, app); // out of line: keeps the
+                        else                                                        // static instance as tight
+                            r = app.template expand<BLOCK, DIST_STATIC>(p, cs);     // as the non-coop kernel's
 #endif
+                    }
                     if (r != ACT_STOP) break;
                     r = offer_kill_mid<BLOCK>(*cs.sp, cs, app);
                     if (r != ACT_CONT) break;                  // killed (its rest handed back) / abort
@@ -1077,7 +1084,7 @@ __device__ __noinline__ void scheduler_loop(const KParams &p, CtaState &cs) {
 // ---------------------------------------------------------------- park loop
 // The megakernel worker pool: wait for a fork assignment,
 // otherwise run blocks of the competing task; exit at termination.
-template <class App, int BLOCK>
+template <class App, int BLOCK, bool ARMED>
 __device__ __noinline__ void park_loop(const KParams &p, CtaState &cs, App &app) {
     Ctl *c = p.ctl;
     const uint32_t phys = blockIdx.x;
@@ -1143,7 +1150,7 @@ __device__ __noinline__ void park_loop(const KParams &p, CtaState &cs, App &app)
         }
         cta_sync();
         if (cs.stop) return;
-        uint32_t r = run_body<App, BLOCK>(p, cs, app, cs.entry);
+        uint32_t r = run_body<App, BLOCK, ARMED>(p, cs, app, cs.entry);
         flush_stats(p, cs);
         if (r == ACT_DONE) {
             if (threadIdx.x == 0 && cs.lid == 0) {
@@ -1160,7 +1167,7 @@ __device__ __noinline__ void park_loop(const KParams &p, CtaState &cs, App &app)
 }
 
 // ---------------------------------------------------------------- kernel
-template <class App, int BLOCK>
+template <class App, int BLOCK, bool ARMED>
 __device__ __forceinline__ void kernel_body(const KParams &p, CtaState &cs, App &app) {
     if (threadIdx.x == 0) {
         const uint64_t t0 = globaltimer();
@@ -1185,7 +1192,7 @@ __device__ __forceinline__ void kernel_body(const KParams &p, CtaState &cs, App 
         if (p.has_sched && blockIdx.x == p.P) { scheduler_loop(*cs.sp, cs); return; }
     }
     if (blockIdx.x < p.M0) {
-        uint32_t r = run_body<App, BLOCK>(p, cs, app, ENTRY_START);
+        uint32_t r = run_body<App, BLOCK, ARMED>(p, cs, app, ENTRY_START);
         flush_stats(p, cs);
         if (r == ACT_DONE) {
             if (threadIdx.x == 0 && cs.lid == 0) {
@@ -1201,7 +1208,7 @@ __device__ __forceinline__ void kernel_body(const KParams &p, CtaState &cs, App 
         cta_sync();
     }
     if constexpr ((App::kCoop && COOP_BIS_PARK)) {
-        if (p.barrier_mode != COOP_BARRIER_PLAIN) park_loop<App, BLOCK>(*cs.sp, cs, app);
+        if (p.barrier_mode != COOP_BARRIER_PLAIN) park_loop<App, BLOCK, ARMED>(*cs.sp, cs, app);
     }
 #if COOP_TRACE
     if (threadIdx.x == 0 && blockIdx.x == 0)
@@ -1213,7 +1220,7 @@ __device__ __forceinline__ void kernel_body(const KParams &p, CtaState &cs, App 
 // __grid_constant__: the parameter block is addressed in place by the out-of-line runtime
 // functions (const KParams &), so no thread copies the ~0.9 KB struct to its stack at launch
 // (without it every thread of the grid did: ~140 MB of local-memory stores per launch)
-template <class App, int BLOCK, int MINB>
+template <class App, int BLOCK, int MINB, bool ARMED = false>
 __global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(const __grid_constant__ KParams p) {
     __shared__ CtaState cs;
     __shared__ uint32_t s_last;
@@ -1226,7 +1233,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) coop_kernel(const __grid_constant
         if (threadIdx.x == 0) cs.sp = &s_p;
     }
     App app;
-    kernel_body<App, BLOCK>(p, cs, app);
+    kernel_body<App, BLOCK, ARMED>(p, cs, app);
     // epilogue: the last CTA out mirrors the control block into host-mapped memory, so the
     // host reads status and statistics without a device-to-host copy operation per call
     if (p.ctl_mirror) {
