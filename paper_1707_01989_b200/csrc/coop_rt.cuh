@@ -92,6 +92,9 @@
 #ifndef COOP_MID_INLINE
 #define COOP_MID_INLINE 0     // 1: the DIST_MID / DIST_REPLAY expand instances inlined into run_body
 #endif
+#ifndef COOP_MID_NOCHECK
+#define COOP_MID_NOCHECK 0    // measurement only: the mid-interval instance without its per-item checks
+#endif
 #ifndef COOP_MID_UNIFIED
 #define COOP_MID_UNIFIED 0    // 1: every policy runs the DIST_MID instance (inline), its checks gated at run time
 #endif
@@ -801,6 +804,7 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
             // since the CTA's last read, the demand word (raising the stop flag if this id is
             // asked to surrender, query style).  Only a polling warp waits for that load.
             auto check = [&]() -> bool {                             // warp-uniform
+                if (COOP_MID_NOCHECK) return false;                     // measurement only: no kills
                 if (!(p.policy == COOP_POLICY_SCHEDULER && p.barrier_mode == COOP_BARRIER_QUERY)) return false;
                 volatile uint32_t *nx = &cs.nextc[warp];
                 uint32_t due = (int32_t)((uint32_t)clock() - *nx) >= 0 ? 1u : 0u;
