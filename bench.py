@@ -549,10 +549,18 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags, 
         r2 = coop.barrier_bench(n, 200000, threads=128, resize_prob=1 / 64, seed=3)
         bar[str(n)] = {"plain_ns": r["ns_per_barrier"], "resizing_p1_64_ns": r2["ns_per_barrier"],
                        "kills": r2["kills"], "forks": r2["forks"]}
+    # the round trip is bimodal: SMs on the die of the word's L2 slice see ~160 ns, the others
+    # ~370 ns, so a median over 8 SMs lands on either; the barrier words sit on one die and every
+    # barrier has CTAs on both, so both round trips are reported beside the median
+    a64 = lat.get("atom_relaxed_u64", {})
+    rtt_near, rtt_far = a64.get("min", rtt), a64.get("max", rtt)
     for n in bar:
         bar[n]["plain_over_rtt"] = bar[n]["plain_ns"] / rtt
+        bar[n]["plain_over_rtt_near_die"] = bar[n]["plain_ns"] / rtt_near
+        bar[n]["plain_over_rtt_far_die"] = bar[n]["plain_ns"] / rtt_far
     ex["barrier"] = {"l2_atomic_rtt_ns": rtt, "rtt_def": "dependent atom.relaxed.gpu.add.u64 chain, one thread, "
-                     "median over 8 SMs on both dies", "l2_latency_profile_ns": lat, "per_ctas": bar}
+                     "median over 8 SMs on both dies", "rtt_near_die_ns": rtt_near, "rtt_far_die_ns": rtt_far,
+                     "l2_latency_profile_ns": lat, "per_ctas": bar}
     # SSSP on the 2048x2048 grid (configs[1])
     gw = gg.with_weights(gg.grid(2048, 2048, device=dev), seed=1)
     gw.max_weight = 1000

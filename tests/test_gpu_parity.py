@@ -348,12 +348,14 @@ def test_sssp_near_far_under_resizes(coop):
 
 
 # ---------------------------------------------------------------- mid-interval offer_kill
-def test_mid_interval_offer_kill_keeps_results_exact(coop):
+@pytest.mark.parametrize("threads", [256, 1024])
+def test_mid_interval_offer_kill_keeps_results_exact(coop, threads):
     """Demanded workgroups leave between the items of their static share (offer_kill
     inside the level) instead of waiting for the next resizing barrier,
     handing the rest of their share back; the survivors run it in a replay interval
-    before the level ends.  Levels / distances stay bit-exact."""
-    info = coop.device_query(0, 256)
+    before the level ends.  Levels / distances stay bit-exact.  256 threads per workgroup run
+    the scheduler-armed kernel specialisation, 1024 the general kernel's out-of-line instance."""
+    info = coop.device_query(0, threads)
     N = info["max_coresident"] - 1
     g = gg.rmat(18, seed=3)
     gd = _dev(g)
@@ -362,7 +364,7 @@ def test_mid_interval_offer_kill_keeps_results_exact(coop):
     mids = hbs = reps = 0
     for flags in (0, coop.FLAG_DIROPT):
         for q in (1, N // 2, N - 1):
-            lv, st = coop.bfs(gd, s, flags=flags | coop.FLAG_CHECK, threads_per_wg=256, policy=coop.POLICY_SCHEDULER,
+            lv, st = coop.bfs(gd, s, flags=flags | coop.FLAG_CHECK, threads_per_wg=threads, policy=coop.POLICY_SCHEDULER,
                               task_wgs=q, task_blocks=N, task_block_ns=3_000, task_period_ns=15_000,
                               event_cap=1024)
             np.testing.assert_array_equal(lv.cpu().numpy(), ref)
@@ -370,9 +372,11 @@ def test_mid_interval_offer_kill_keeps_results_exact(coop):
             hbs += st.handbacks
             reps += st.replays
             assert st.handbacks <= st.mid_kills and (st.replays > 0) == (st.handbacks > 0)
-    assert mids > 0 and hbs > 0 and reps > 0
+    assert mids > 0
+    if threads == 256:          # many CTAs with items left when asked: hand-backs and replays happen
+        assert hbs > 0 and reps > 0
     gw = SSSP_GRAPHS["grid_w"]()
-    d, st = coop.sssp(_dev(gw), 0, sssp_delta=500, threads_per_wg=256, policy=coop.POLICY_SCHEDULER, task_wgs=N // 2,
+    d, st = coop.sssp(_dev(gw), 0, sssp_delta=500, threads_per_wg=threads, policy=coop.POLICY_SCHEDULER, task_wgs=N // 2,
                       task_blocks=N, task_block_ns=2_000, task_period_ns=10_000, flags=coop.FLAG_CHECK)
     np.testing.assert_array_equal(_u32(d), tb.dijkstra(gw, 0))
 
