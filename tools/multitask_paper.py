@@ -64,8 +64,8 @@ class MultitaskRunner:
 
     def standalone(self, loop_s, barriers=("query",)):
         """The loop with the scheduler armed and no task, per resizing-barrier implementation
-        (the query barrier's intervals are chunk-distributed for mid-interval offer_kill, the
-        naive barrier's are not), so a cell's slowdown compares like with like."""
+        (the query barrier runs the scheduler-armed kernel with mid-interval offer_kill and
+        hand-back, the naive barrier the general one), so a cell's slowdown compares like with like."""
         coop = self.coop
         self.base = getattr(self, "base", {})
         for b in barriers:
