@@ -91,8 +91,19 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
 }
 
 // ---------------------------------------------------------------- protocol steps
+__device__ __forceinline__ bool is_last(unsigned long long old);
 // arrive: returns the word before this CTA's increment; last iff arrived + 1 == M
 __device__ __forceinline__ unsigned long long arrive(unsigned long long *W) { return atom_add_acq_rel64(W, 1ull); }
+
+// arrive_release: the release-only form -- a waiter acquires through the release word R, so
+// only the last arriver needs the acquire, which it takes with a fence after the atomic (an
+// acquire pattern: fence.acq_rel after the read of the release sequence's last value)
+__device__ __forceinline__ unsigned long long arrive_release(unsigned long long *W) {
+    unsigned long long old;
+    asm volatile("atom.release.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(W), "l"(1ull) : "memory");
+    if (is_last(old)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    return old;
+}
 __device__ __forceinline__ bool is_last(unsigned long long old) { return w_arr(old) + 1u == w_M(old); }
 
 // arrive_fenced: the same step for bodies that may leave other warps' fire-and-forget

@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcoop.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("coop_api.cu", "coop_dev_api.cu", "coop_layout.cu")]
 DEPS = SOURCES + sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))) + \
-    [os.path.join(ROOT, "include", f) for f in ("coop.h", "coop_device.cuh")]
+    [os.path.join(ROOT, "include", f) for f in ("coop.h", "coop_device.cuh", "coop_protocol.cuh")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [

@@ -49,6 +49,10 @@
 #ifndef COOP_ARRIVE_ACQREL
 #define COOP_ARRIVE_ACQREL 1
 #endif
+#ifndef COOP_ARRIVE_REL
+#define COOP_ARRIVE_REL 0     // 1: release-only arrival, fence.acq_rel by the last arriver only (measured
+                              // slower: 3.14 vs 2.76 us per plain barrier at 148 CTAs, profiles/r02g_variants.log)
+#endif
 
 // bisection switches (A/B of the cooperative machinery's cost; 1 = shipped code)
 #ifndef COOP_BIS_SERIAL
@@ -487,7 +491,10 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
         } else {
             // arrive: release the CTA's writes of this interval (bar.sync + cumulative
             // release) and, for the last arriver, acquire everybody else's
-#if COOP_ARRIVE_ACQREL
+#if COOP_ARRIVE_REL
+            old = coop_proto::arrive_release(&c->W);
+            last = coop_proto::is_last(old) ? 1u : 0u;
+#elif COOP_ARRIVE_ACQREL
             old = coop_proto::arrive(&c->W);
             last = coop_proto::is_last(old) ? 1u : 0u;
 #else
