@@ -431,6 +431,21 @@ def run_extras(args, g, srcs, out, flush, stream, dev, info, base_times, flags, 
         return e0.elapsed_time(e1), r
 
     k = min(args.steps, 8)
+    # C3 as SURVEY 8(d) states it: the 64 sources, one call each (L2 flushed, CUDA events around the
+    # call), GTEPS aggregated by harmonic mean (Graph500); every 8th output is checked by the oracle
+    per, perk = [], []
+    for i, s64 in enumerate(srcs[:64]):
+        t, (_, st) = timed(lambda: coop.bfs(g, s64, out, threads_per_wg=args.threads, flags=flags))
+        e = int(deg[out >= 0].sum().item()) // 2
+        per.append(e / (t * 1e-3) / 1e9)
+        perk.append(e / (st.kernel_ns * 1e-9) / 1e9)
+        if not args.no_verify and i % 8 == 0:
+            checked.append((s64, out.clone()))
+    hmean = lambda xs: len(xs) / sum(1.0 / x for x in xs)
+    ex["c3_64_sources"] = {"sources": len(per), "gteps_harmonic_mean": hmean(per),
+                           "gteps_harmonic_mean_kernel": hmean(perk), "gteps_min": min(per), "gteps_max": max(per),
+                           "timing": "one call per source (not pipelined), CUDA events around the call, L2 flushed; "
+                                     "_kernel: the kernel's own %globaltimer span"}
     # T2 analogue: the cooperative kernel with no competing task against the
     # separately compiled non-cooperative persistent kernel (kCoop = false: plain barrier,
     # static split, no scheduler/pool/mailbox code), all at the same N worker CTAs.  Two
