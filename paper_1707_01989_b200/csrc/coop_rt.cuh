@@ -386,8 +386,8 @@ __device__ void serial_section(const KParams &p, CtaState &cs, App &app, uint32_
         LTRACE(10);
         // statistics after the release: nobody waits for them (the host reads them at the end)
         if constexpr ((App::kCoop && COOP_BIS_SERIAL)) {
-            const uint64_t now = globaltimer();
             if (take > 0) {   // gather bookkeeping of the task instance in flight
+                const uint64_t now = globaltimer();
                 uint32_t cur = c->cur_task;
                 if (cur && cur - 1 < p.events_cap) {
                     TaskEventDev *e = p.events + (cur - 1);
@@ -1212,14 +1212,18 @@ __device__ __forceinline__ void kernel_body(const KParams &p, CtaState &cs, App 
             }
         }
         if (r == ACT_ABORT) return;
-        if ((App::kCoop && COOP_BIS_PARK) && p.barrier_mode != COOP_BARRIER_PLAIN && threadIdx.x == 0) {   // killed or finished: join the pool
+        // killed or finished: join the pool -- unless no CTA can ever be forked or run a task
+        // (NEVER: no scheduler, no resize), then leave the kernel at once
+        if ((App::kCoop && COOP_BIS_PARK) && p.barrier_mode != COOP_BARRIER_PLAIN && p.policy != COOP_POLICY_NEVER &&
+            threadIdx.x == 0) {
             __threadfence();
             atomicOr(&p.ctl->pool[blockIdx.x >> 5], 1u << (blockIdx.x & 31));
         }
         cta_sync();
     }
     if constexpr ((App::kCoop && COOP_BIS_PARK)) {
-        if (p.barrier_mode != COOP_BARRIER_PLAIN) park_loop<App, BLOCK, ARMED>(*cs.sp, cs, app);
+        if (p.barrier_mode != COOP_BARRIER_PLAIN && p.policy != COOP_POLICY_NEVER)
+            park_loop<App, BLOCK, ARMED>(*cs.sp, cs, app);
     }
 #if COOP_TRACE
     if (threadIdx.x == 0 && blockIdx.x == 0)
