@@ -623,6 +623,17 @@ __device__ uint32_t barrier(const KParams &p, CtaState &cs, App &app, bool resiz
 // ACT_KILLED, ACT_CONT (resume the static share) or ACT_ABORT; `flush` is called
 // (CTA-collective) before the CTA can be counted out.
 
+// the static slot of warp w of CTA lid among the M*W warps of an interval.  COOP_CTA_INTERLEAVE:
+// consecutive items go to consecutive CTAs (warp-major), so a small interval's few items spread
+// over the SMs instead of filling the warps of the first CTAs
+#ifndef COOP_CTA_INTERLEAVE
+#define COOP_CTA_INTERLEAVE 0
+#endif
+template <int WPB>
+__device__ __forceinline__ uint64_t warp_slot(uint32_t lid, uint32_t M, uint32_t w) {
+    return COOP_CTA_INTERLEAVE ? (uint64_t)w * M + lid : (uint64_t)lid * WPB + w;
+}
+
 // thread 0: hand back what is left of this CTA's static share (cs.rk[w] = the next
 // item index of warp w; warp w's items are gw, gw + TW, ... below n); returns the donor
 // index, or ~0u when nothing is left
@@ -632,7 +643,7 @@ __device__ __forceinline__ uint32_t hand_back(const KParams &p, CtaState &cs, ui
     uint64_t start[WPB], cnt[WPB], tot = 0;
 #pragma unroll
     for (uint32_t w = 0; w < WPB; ++w) {
-        start[w] = (uint64_t)cs.lid * WPB + w + (uint64_t)cs.rk[w] * TW;
+        start[w] = warp_slot<WPB>(cs.lid, (uint32_t)(TW / WPB), w) + (uint64_t)cs.rk[w] * TW;
         cnt[w] = start[w] < n ? (n - start[w] + TW - 1) / TW : 0;
         tot += cnt[w];
     }
@@ -764,7 +775,7 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
         const uint64_t total = rw & kMask44, npairs = (rw >> 44) * WPB;
         const uint64_t TWi = __ldcg(&c->rep_tw);
         const uint64_t TWs = (uint64_t)cs.rep_M * WPB;
-        for (uint64_t f = (uint64_t)cs.lid * WPB + warp; f < total; f += TWs) {
+        for (uint64_t f = warp_slot<WPB>(cs.lid, cs.rep_M, warp); f < total; f += TWs) {
             uint64_t lo = 0, hi = npairs - 1;                 // last entry with prefix <= f
             while (lo < hi) {
                 const uint64_t mid = (lo + hi + 1) >> 1;
@@ -779,7 +790,7 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
     } else {
         constexpr bool mid = DIST == DIST_MID && App::kCoop && COOP_BIS_CLAIM;
         const uint64_t TW = (uint64_t)cs.M * WPB;
-        const uint64_t gw = (uint64_t)cs.lid * WPB + warp;
+        const uint64_t gw = warp_slot<WPB>(cs.lid, cs.M, warp);
         if constexpr (!mid) {
             for (uint64_t it = gw; it < n_static; it += TW) fn(it);
             if (tail16 && n_static < n_items) {
@@ -837,7 +848,7 @@ __device__ uint32_t claim_items(const KParams &p, CtaState &cs, App &app, uint32
                 }
                 // next static item of this warp (all done: past the end)
                 if (lane == 0)
-                    cs.rk[warp] = halted ? (uint32_t)((it - ((uint64_t)cs.lid * WPB + warp)) / TW) : 0xFFFFFFFFu;
+                    cs.rk[warp] = halted ? (uint32_t)((it - gw) / TW) : 0xFFFFFFFFu;
                 if (tail16 && n_static < n_items && !halted) {
                     uint32_t t = 0;
                     if (lane == 0) t = atomicAdd(counter, 1u);
